@@ -1,0 +1,212 @@
+/*
+ * moe_b200.h — C ABI of the B200-native W8A8 MoE hot path (arXiv 2508.07329,
+ * reference package `moekit`).
+ *
+ * The reference exposes its operator API as module-level Python functions of
+ * moekit.quant / moekit.trace / moekit.placement (re-exported in
+ * moekit/__init__.py:15-17); it has no FFI. Each entry point below is the
+ * device-side replacement of one of those functions (cited per function) or
+ * of a forward-path step the reference leaves out (router, permutation,
+ * grouped expert GEMM, combine — SURVEY.md §8a rows a'1..a'3). The Python
+ * host layer `paper_2508_07329_b200` binds these with ctypes (see
+ * INTEGRATION.md) and keeps the reference's names, argument meaning and
+ * exception types.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; callers own all memory;
+ *    kernels never allocate (workspace sizes are queried).
+ *  - Activations are tokens-major [rows, cols] (per_token == per row).
+ *    Weights are [out rows, in cols] (quant.py:3-5). GEMM: Y = A * W^T.
+ *  - Codes are unsigned 8-bit containers for 2..8-bit affine codes
+ *    value = (code - zero_point) * scale (quant.py:15-16).
+ *  - `stream` is a cudaStream_t (CUstream) passed as void*.
+ *  - Every function returns a moe_status; on failure moe_last_error() holds
+ *    a thread-local message. Status -> Python exception mapping:
+ *    EINVAL -> ValueError, ENOTPD -> NotPositiveDefiniteError,
+ *    EDEGENERATE -> DegenerateHessianError, EQUANTFAIL ->
+ *    QuantizationFailedError (errors.py:11-35), ECUDA/EUNSUPPORTED ->
+ *    RuntimeError.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* moe_stream_t;
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_EINVAL = 1,
+  MOE_ENOTPD = 2,
+  MOE_EDEGENERATE = 3,
+  MOE_EQUANTFAIL = 4,
+  MOE_ECUDA = 5,
+  MOE_EUNSUPPORTED = 6
+} moe_status;
+
+/* element types */
+enum { MOE_DT_F32 = 0, MOE_DT_F64 = 1, MOE_DT_BF16 = 2, MOE_DT_F16 = 3, MOE_DT_U8 = 4, MOE_DT_I32 = 5 };
+/* granularity tags == index in quant.GRANULARITIES (quant.py:40) */
+enum { MOE_GRAN_PER_TENSOR = 0, MOE_GRAN_PER_TOKEN = 1, MOE_GRAN_PER_OUTPUT_ROW = 2 };
+/* smoothing application (quant.py:314-324): activations divide, weights multiply */
+enum { MOE_SMOOTH_NONE = 0, MOE_SMOOTH_DIVIDE = 1, MOE_SMOOTH_MULTIPLY = 2 };
+/* GEMM epilogues */
+enum { MOE_EPI_DEQUANT = 0, MOE_EPI_SWIGLU = 1, MOE_EPI_ACC_I32 = 2 };
+/* channel ordering strategies (quant.py:42-45) */
+enum { MOE_ORDER_MAX_ABS = 1, MOE_ORDER_SUM_SQUARES = 2 };
+
+/* ---- library ------------------------------------------------------------ */
+const char* moe_last_error(void);
+int moe_abi_version(void);
+/* Number of kernels this library has launched in the process (all entry
+ * points count every launch they make) — the bench's gpu_launches. */
+uint64_t moe_launch_count(void);
+/* 0 if device `dev` is an sm_100 part the kernels were built for. */
+moe_status moe_device_check(int dev);
+
+/* ---- K1: smoothing + RTN affine quantization ----------------------------
+ * Replaces quant.rtn_quantize (quant.py:214-231) applied to
+ * apply_smoothing's operand (quant.py:314-324), i.e. the activation side of
+ * quant_loss (quant.py:281-282) and of the W8A8 forward, and the weight side
+ * of _quantize_weights (quant.py:262-264, MULTIPLY mode).
+ *
+ * Output row r reads input row gather_rows[r] (or r when NULL), smooths it
+ * with table row row_group[r] (or 0) of `smooth` [G, cols] (with its
+ * correctly-rounded reciprocal table `smooth_recip`, used for an exact
+ * reciprocal-and-correct division; NULL -> plain IEEE division), then
+ * quantizes with float64 semantics bit-identical to the reference:
+ * scale = max((max-min)/qmax, 1e-12), zp = clip(rha(-min/scale)),
+ * code = clip(rha(xs/scale)+zp), rha(v) = sign(v)*floor(|v|+0.5).
+ * per_token / per_output_row: one group per output row. per_tensor: one
+ * group (workspace >= moe_act_quant_workspace()). Outputs: codes [rows,
+ * ldc], scale f64 [groups], scale_f32 (optional) [groups], zp [groups],
+ * rowsum (optional) [rows] = sum of the row's codes (for the GEMM's
+ * zero-point correction).
+ */
+int64_t moe_act_quant_workspace(int64_t rows, int64_t cols, int granularity);
+moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                         const int32_t* gather_rows, const double* smooth, const double* smooth_recip,
+                         int smooth_mode, const int32_t* row_group, int bits, int symmetric,
+                         int granularity, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                         int32_t* zp, int32_t* rowsum, void* workspace, int64_t workspace_bytes,
+                         moe_stream_t stream);
+
+/* out[i] = RN(1 / s[i]) (float64); feeds smooth_recip. */
+moe_status moe_reciprocal_f64(const double* s, int64_t n, double* out, moe_stream_t stream);
+
+/* dequantize (quant.py:234-240): out = (code - zp) * scale, float64. */
+moe_status moe_dequantize(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ldc,
+                          const double* scale, const int32_t* zp, int granularity, double* out,
+                          moe_stream_t stream);
+
+/* apply_smoothing (quant.py:314-324): ws = w * f (cols), xs = x / f (rows of
+ * the channels x tokens matrix). Either side may be NULL. */
+moe_status moe_apply_smoothing(const double* w, int64_t R, int64_t n, const double* x, int64_t T,
+                               const double* f, double* ws, double* xs, moe_stream_t stream);
+
+/* channel statistics for channel_order (quant.py:346-363) and the smoothing
+ * statistic of search_smoothing (quant.py:303): per row of x [n, T]:
+ * MAX_ABS -> max |x|, SUM_SQUARES -> sum x^2 (row-order summation). */
+moe_status moe_channel_stats(const double* x, int64_t n, int64_t T, int strategy, double* stat,
+                             moe_stream_t stream);
+
+/* ---- K2 / K5: W8A8 GEMM on tcgen05 kind::i8 -----------------------------
+ * Replaces the fake-quant product of quant_loss (quant.py:281-283) and
+ * quantize_layer (quant.py:475-478) with an exact integer product:
+ *   acc[m,n] = sum_k (a[m,k] - a_zp[m]) * (w[n,k] - w_zp[n])   (int32, exact)
+ * computed as u8*u8 UMMA plus zero-point correction with the code row sums.
+ * Epilogues: DEQUANT  out = a_scale[m]*w_scale[n]*acc (+bias[n]) (*row_weight[m])
+ *            SWIGLU   W rows interleaved in blocks of 128 (gate, up): out
+ *                     [m, N/2] = silu(g) * u of the dequantized pair
+ *            ACC_I32  acc_out[m, n] = acc (int32, exact)
+ * Grouped (MoE, K5): A rows are grouped by expert; group g owns A rows
+ * [group_offsets[g], group_offsets[g+1]) (device array) and W rows
+ * [g*N, (g+1)*N) of the stacked weights. group_offsets == NULL -> one group
+ * of M rows. K must be a multiple of 16; other shapes use a SIMT path with
+ * identical integer results. */
+moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                         const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                         int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,
+                         const float* bias, const float* row_weight, const int32_t* group_offsets,
+                         int num_groups, int epilogue, void* out, int out_dtype, int64_t ldo,
+                         int32_t* acc_out, int64_t ld_acc, moe_stream_t stream);
+
+/* Frobenius-loss reduction for quant_loss (quant.py:283) on the exact
+ * accumulators: out = sum_{m,n} (a_scale[m]*w_scale[n]*acc[m,n] - ref[m,n])^2
+ * with ref [M, N] float64. Scales are per row (per_tensor: stride 0 via
+ * a_scale_stride = 0). Deterministic two-level reduction. */
+moe_status moe_quant_sq_error(const int32_t* acc, int64_t M, int64_t N, const double* a_scale,
+                              int a_scale_stride, const double* w_scale, const double* ref,
+                              double* out, void* workspace, int64_t workspace_bytes, moe_stream_t stream);
+int64_t moe_quant_sq_error_workspace(int64_t M, int64_t N);
+
+/* ---- K3: router gating --------------------------------------------------
+ * Not in the reference (its only trace of routing is the event format,
+ * trace.py:40-44). logits[t, e] = x[t,:] . gate_w[e,:] (float32 accumulate);
+ * top-k on logits, ties to the lower expert id, descending order; weights
+ * = softmax over the selected logits. gate_bias [E] (optional) is added to the
+ * logits. logits may be NULL (not stored). */
+moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, const float* gate_w,
+                           const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx,
+                           float* topk_w, moe_stream_t stream);
+/* top-k only, from given float32 logits [T, E]. */
+moe_status moe_router_topk(const float* logits, int64_t T, int E, int k, int32_t* topk_idx, float* topk_w,
+                           moe_stream_t stream);
+
+/* ---- K4: token -> expert permutation (stable counting sort) -------------
+ * expert_offsets [E+1]; for permuted row p: src_token[p], row_expert[p],
+ * row_weight[p] (= topk_w of that pair, optional); token_pos[t*k+j] = p. */
+int64_t moe_route_permute_workspace(int64_t T, int k, int E);
+moe_status moe_route_permute(const int32_t* topk_idx, const float* topk_w, int64_t T, int k, int E,
+                             int32_t* expert_offsets, int32_t* src_token, int32_t* row_expert,
+                             float* row_weight, int32_t* token_pos, void* workspace,
+                             int64_t workspace_bytes, moe_stream_t stream);
+
+/* ---- K6: combine ----------------------------------------------------------
+ * out[t, :] = sum_j y[token_pos[t*k+j], :] (row weights already applied by
+ * the GEMM epilogue), summed in slot order j = 0..k-1 in float32. */
+moe_status moe_combine(const void* y, int y_dtype, const int32_t* token_pos, int64_t T, int k, int64_t d,
+                       void* out, int out_dtype, moe_stream_t stream);
+
+/* ---- routing statistics (trace.expert_freq, trace.py:216-225) -----------
+ * counts[layer*E + e] += number of (t, j) with topk_idx[t, j] == e. Path
+ * keys for trace.path_stats (trace.py:207-213): path_codes[t] for this layer
+ * = ascending pair of ids packed as lo*E + hi (k == 2) or a bitmask (k > 2). */
+moe_status moe_expert_histogram(const int32_t* topk_idx, int64_t T, int k, int E, int layer,
+                                int64_t* counts, int32_t* path_codes, moe_stream_t stream);
+
+/* ---- K7: Hessian accumulation (build_hessian, quant.py:327-343) ----------
+ * H[n, n] += 2 * xs^T xs over a tokens-major batch x [T, n] (xs = x / s when
+ * smooth != NULL, exact division). Finalize symmetrises, adds
+ * damping_fraction * mean(diag) on the diagonal and reports an all-zero
+ * calibration (EDEGENERATE) via the nonzero counter. */
+moe_status moe_hessian_accum(const void* x, int x_dtype, int64_t T, int64_t n, int64_t ldx,
+                             const double* smooth, const double* smooth_recip, double* H,
+                             unsigned long long* nonzero_count, moe_stream_t stream);
+moe_status moe_hessian_finalize(double* H, int64_t n, double damping_fraction,
+                                const unsigned long long* nonzero_count, moe_stream_t stream);
+
+/* ---- K8: compensated column loop (hessian_quantize, quant.py:415-434) ----
+ * W [R, n] float64 in the ORIGINAL column order (read-only); column i of
+ * the loop is W[:, order[i]] (order NULL -> identity); U [n, n] is the upper
+ * factor of the PERMUTED H^-1 (quant.py:366-385, 418-420). Per-row params
+ * scale/zp are fixed for the loop (quant.py:415). Exactly the reference's
+ * operation order per element: encode column i, err = (w_i - (c - zp)*scale)
+ * / U_ii, then w_j = w_j - err*U_ij (separate multiply and subtract,
+ * ascending i) -> bit-identical codes, written back to the original column
+ * positions codes[r, order[i]] (quant.py:432-433). err_ws: workspace of
+ * moe_gptq_workspace() bytes. */
+int64_t moe_gptq_workspace(int64_t R, int64_t n);
+moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, int64_t ldw, const int32_t* order,
+                            const double* U, const double* scale, const int32_t* zp, int bits,
+                            uint8_t* codes, int64_t ldc, void* err_ws, int64_t err_ws_bytes,
+                            moe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

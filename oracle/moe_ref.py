@@ -96,7 +96,10 @@ def int_acc(codes_a, za, codes_w, zw) -> np.ndarray:
     folded out)."""
     a = np.asarray(codes_a, dtype=np.int64) - np.asarray(za, dtype=np.int64).reshape(-1, 1)
     w = np.asarray(codes_w, dtype=np.int64) - np.asarray(zw, dtype=np.int64).reshape(-1, 1)
-    return a @ w.T
+    # float64 BLAS is exact here: |terms| <= 255^2 and every partial sum is an
+    # integer below K*255^2 < 2^53, so no rounding can occur.
+    assert a.shape[1] * 255 * 255 < 2 ** 53
+    return (a.astype(np.float64) @ w.T.astype(np.float64)).astype(np.int64)
 
 
 def w8a8_linear(codes_a, sa, za, codes_w, sw, zw, bias=None):

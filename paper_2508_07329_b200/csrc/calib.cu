@@ -1,0 +1,276 @@
+// Calibration kernels: K7 Hessian accumulation (build_hessian,
+// quant.py:327-343), K8 the compensated column loop of hessian_quantize
+// (quant.py:415-434) in strict reference order, and the Frobenius-loss
+// reduction used by quant_loss / search_smoothing (quant.py:267-311).
+#include "common.cuh"
+
+namespace moe {
+
+// ── K7: H += 2 * xs^T xs (upper-triangle tiles, float64 SIMT) ──────────────
+constexpr int kHT = 64;  // output tile
+constexpr int kHK = 16;  // tokens per smem stage
+
+__global__ void __launch_bounds__(256) hessian_accum_kernel(const void* x, int dt, int64_t T, int64_t n,
+                                                            int64_t ldx, const double* s, const double* rs,
+                                                            double* H, unsigned long long* nonzero) {
+  // map the linear block id onto an upper-triangle tile (bi <= bj)
+  const int nt = (int)((n + kHT - 1) / kHT);
+  int b = blockIdx.x, bi = 0;
+  while (b >= nt - bi) {
+    b -= nt - bi;
+    ++bi;
+  }
+  const int bj = bi + b;
+  __shared__ double xa[kHK][kHT + 1];
+  __shared__ double xb[kHK][kHT + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16x16 threads, 4x4 outputs each
+  double acc[4][4] = {};
+  unsigned long long nz = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += kHK) {
+    for (int i = threadIdx.x; i < kHK * kHT; i += blockDim.x) {
+      const int tt = i / kHT, c = i % kHT;
+      const int64_t t = t0 + tt;
+      const int64_t ca = (int64_t)bi * kHT + c, cb = (int64_t)bj * kHT + c;
+      double va = 0.0, vb = 0.0;
+      if (t < T && ca < n) {
+        va = load_as_f64(x, t * ldx + ca, dt);
+        if (s) va = rs ? div_rcp(va, s[ca], rs[ca]) : __ddiv_rn(va, s[ca]);
+        if (bi == bj) nz += (va != 0.0);
+      }
+      if (t < T && cb < n) {
+        vb = load_as_f64(x, t * ldx + cb, dt);
+        if (s) vb = rs ? div_rcp(vb, s[cb], rs[cb]) : __ddiv_rn(vb, s[cb]);
+      }
+      xa[tt][c] = va;
+      xb[tt][c] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kHK; ++k) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = xa[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = xb[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = (int64_t)bi * kHT + ty * 4 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = (int64_t)bj * kHT + tx * 4 + j;
+      if (r < n && c < n && (bi != bj || c >= r)) H[r * n + c] += 2.0 * acc[i][j];
+    }
+  }
+  if (nonzero && nz) atomicAdd(nonzero, nz);
+}
+
+// mirror the upper triangle, add damping * mean(diag) (deterministic mean)
+__global__ void hessian_diag_mean_kernel(const double* H, int64_t n, double* mean_out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += H[i * n + i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) sh[threadIdx.x] += sh[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *mean_out = sh[0] / (double)n;
+}
+
+__global__ void hessian_finalize_kernel(double* H, int64_t n, double damping, const double* mean) {
+  const double lam = damping * (*mean);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n, c = i % n;
+    if (r > c) H[i] = H[c * n + r];
+    else if (r == c) H[i] += lam;
+  }
+}
+
+// ── K8: left-looking strict-order GPTQ column loop ─────────────────────────
+// One thread per weight row. For column tile [J, J+32): start from the
+// original weights, apply the updates of columns i < J in ascending i
+// (err_i read from the workspace, U[i, J:J+32] broadcast from smem), then
+// run the in-tile sequential loop. Per element the subtractions happen in
+// exactly the reference's order, so codes are bit-identical.
+constexpr int kGT = 32;      // columns per tile
+constexpr int kGRows = 64;   // rows (threads) per CTA
+constexpr int kGU = 64;      // U rows per smem stage
+
+__global__ void __launch_bounds__(kGRows) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
+                                                               const int32_t* order, const double* U,
+                                                               const double* scale, const int32_t* zp, int qmax,
+                                                               uint8_t* codes, int64_t ldc, double* err) {
+  __shared__ __align__(16) double us[kGU][kGT];
+  __shared__ __align__(16) double ut[kGT][kGT + 1];
+  const int64_t r = (int64_t)blockIdx.x * kGRows + threadIdx.x;
+  const bool valid = r < R;
+  const double sc = valid ? scale[r] : 1.0;
+  const double rsc = __drcp_rn(sc);
+  const int z = valid ? zp[r] : 0;
+  for (int64_t J = 0; J < n; J += kGT) {
+    const int tw = (int)((n - J) < kGT ? (n - J) : kGT);
+    double w[kGT];
+#pragma unroll
+    for (int j = 0; j < kGT; ++j) {
+      const int64_t col = J + j;
+      w[j] = (valid && j < tw) ? W[r * ldw + (order ? (int64_t)order[col] : col)] : 0.0;
+    }
+    // updates from all previous columns, ascending
+    for (int64_t i0 = 0; i0 < J; i0 += kGU) {
+      const int ni = (int)((J - i0) < kGU ? (J - i0) : kGU);
+      __syncthreads();
+      for (int q = threadIdx.x; q < kGU * kGT; q += kGRows) {
+        const int ii = q / kGT, jj = q % kGT;
+        us[ii][jj] = (ii < ni && jj < tw) ? U[(i0 + ii) * n + J + jj] : 0.0;
+      }
+      __syncthreads();
+      for (int ii = 0; ii < ni; ++ii) {
+        const double e = valid ? err[(i0 + ii) * R + r] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kGT; ++j) w[j] = __dsub_rn(w[j], __dmul_rn(e, us[ii][j]));
+      }
+    }
+    // in-tile sequential part
+    __syncthreads();
+    for (int q = threadIdx.x; q < kGT * kGT; q += kGRows) {
+      const int ii = q / kGT, jj = q % kGT;
+      ut[ii][jj] = (ii < tw && jj < tw) ? U[(J + ii) * n + J + jj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kGT; ++i) {
+      if (i < tw) {
+        const int c = encode_code(w[i], sc, rsc, z, qmax);
+        const double deq = __dmul_rn((double)(c - z), sc);
+        const double e = __ddiv_rn(__dsub_rn(w[i], deq), ut[i][i]);
+        if (valid) {
+          err[(J + i) * R + r] = e;
+          const int64_t col = J + i;
+          codes[r * ldc + (order ? (int64_t)order[col] : col)] = (uint8_t)c;
+        }
+#pragma unroll
+        for (int j = i + 1; j < kGT; ++j) w[j] = __dsub_rn(w[j], __dmul_rn(e, ut[i][j]));
+      }
+    }
+  }
+}
+
+// ── Frobenius loss on exact accumulators ───────────────────────────────────
+__global__ void __launch_bounds__(256) sq_error_partial_kernel(const int32_t* acc, int64_t M, int64_t N,
+                                                               const double* sa, int sa_stride, const double* sw,
+                                                               const double* ref, double* partial) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  const int64_t total = M * N;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per, hi = min(total, lo + per);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int64_t m = i / N, c = i % N;
+    const double y = __dmul_rn(__dmul_rn(sa[m * sa_stride], sw[c]), (double)acc[i]);
+    const double d = __dsub_rn(y, ref[i]);
+    s = fma(d, d, s);
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) sh[threadIdx.x] += sh[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void sq_error_final_kernel(const double* partial, int nparts, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += partial[i];
+    *out = s;
+  }
+}
+
+constexpr int kSqParts = 512;
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" moe_status moe_hessian_accum(const void* x, int x_dtype, int64_t T, int64_t n, int64_t ldx,
+                                        const double* smooth, const double* smooth_recip, double* H,
+                                        unsigned long long* nonzero_count, moe_stream_t stream) {
+  MOE_REQUIRE(x && H && T >= 1 && n >= 1 && ldx >= n, "hessian_accum: bad arguments");
+  const int64_t nt = (n + kHT - 1) / kHT;
+  const int64_t blocks = nt * (nt + 1) / 2;
+  MOE_REQUIRE(blocks < (1LL << 31), "hessian_accum: n too large");
+  hessian_accum_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, x_dtype, T, n, ldx, smooth, smooth_recip,
+                                                                         H, nonzero_count); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_hessian_finalize(double* H, int64_t n, double damping_fraction,
+                                           const unsigned long long* nonzero_count, moe_stream_t stream) {
+  MOE_REQUIRE(H && n >= 1, "hessian_finalize: bad arguments");
+  MOE_REQUIRE(damping_fraction >= 0.0, "damping_fraction must be >= 0");
+  cudaStream_t s = as_stream(stream);
+  if (nonzero_count) {
+    unsigned long long nz = 0;
+    MOE_CUDA_TRY(cudaMemcpyAsync(&nz, nonzero_count, sizeof(nz), cudaMemcpyDeviceToHost, s));
+    MOE_CUDA_TRY(cudaStreamSynchronize(s));
+    if (nz == 0) {
+      set_error("calibration activations are all zero");
+      return MOE_EDEGENERATE;
+    }
+  }
+  double* mean = nullptr;
+  MOE_CUDA_TRY(cudaMallocAsync(&mean, sizeof(double), s));
+  hessian_diag_mean_kernel<<<1, 256, 0, s>>>(H, n, mean); ::moe::count_launch();
+  int64_t blocks = (n * n + 255) / 256;
+  if (blocks > num_sms() * 32) blocks = num_sms() * 32;
+  hessian_finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(H, n, damping_fraction, mean); ::moe::count_launch();
+  MOE_CUDA_TRY(cudaFreeAsync(mean, s));
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" int64_t moe_gptq_workspace(int64_t R, int64_t n) { return R * n * (int64_t)sizeof(double); }
+
+extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, int64_t ldw, const int32_t* order,
+                                       const double* U, const double* scale, const int32_t* zp, int bits,
+                                       uint8_t* codes, int64_t ldc, void* err_ws, int64_t err_ws_bytes,
+                                       moe_stream_t stream) {
+  MOE_REQUIRE(W && U && scale && zp && codes && err_ws, "gptq_columns: null pointer");
+  MOE_REQUIRE(R >= 1 && n >= 1 && ldw >= n && ldc >= n, "gptq_columns: bad shape");
+  MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
+  MOE_REQUIRE(err_ws_bytes >= moe_gptq_workspace(R, n), "gptq_columns: workspace too small");
+  const unsigned blocks = (unsigned)((R + kGRows - 1) / kGRows);
+  gptq_columns_kernel<<<blocks, kGRows, 0, as_stream(stream)>>>(W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1,
+                                                               codes, ldc, static_cast<double*>(err_ws)); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" int64_t moe_quant_sq_error_workspace(int64_t M, int64_t N) {
+  (void)M;
+  (void)N;
+  return kSqParts * (int64_t)sizeof(double);
+}
+
+extern "C" moe_status moe_quant_sq_error(const int32_t* acc, int64_t M, int64_t N, const double* a_scale,
+                                         int a_scale_stride, const double* w_scale, const double* ref, double* out,
+                                         void* workspace, int64_t workspace_bytes, moe_stream_t stream) {
+  MOE_REQUIRE(acc && a_scale && w_scale && ref && out && M >= 1 && N >= 1, "quant_sq_error: bad arguments");
+  MOE_REQUIRE(workspace && workspace_bytes >= moe_quant_sq_error_workspace(M, N), "quant_sq_error: workspace");
+  cudaStream_t s = as_stream(stream);
+  double* part = static_cast<double*>(workspace);
+  sq_error_partial_kernel<<<kSqParts, 256, 0, s>>>(acc, M, N, a_scale, a_scale_stride, w_scale, ref, part); ::moe::count_launch();
+  sq_error_final_kernel<<<1, 32, 0, s>>>(part, kSqParts, out); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}

@@ -1,0 +1,118 @@
+// Shared host/device helpers: status + thread-local error text, dtype loads,
+// float64 rounding helpers that reproduce moekit's quantizer bit-for-bit.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/moe_b200.h"
+
+namespace moe {
+
+void set_error(const std::string& msg);
+void count_launch();  // every kernel launch of the library is counted (moe_launch_count)
+
+#define MOE_REQUIRE(cond, msg)         \
+  do {                                 \
+    if (!(cond)) {                     \
+      ::moe::set_error(msg);           \
+      return MOE_EINVAL;               \
+    }                                  \
+  } while (0)
+
+#define MOE_CUDA_TRY(expr)                                                                  \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) {                                                                \
+      ::moe::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
+      return MOE_ECUDA;                                                                     \
+    }                                                                                       \
+  } while (0)
+
+#define MOE_LAUNCH_CHECK()                                                                  \
+  do {                                                                                      \
+    cudaError_t _e = cudaGetLastError();                                                    \
+    if (_e != cudaSuccess) {                                                                \
+      ::moe::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));            \
+      return MOE_ECUDA;                                                                     \
+    }                                                                                       \
+  } while (0)
+
+inline cudaStream_t as_stream(moe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ── element loads ─────────────────────────────────────────────────────────
+__device__ __forceinline__ double load_as_f64(const void* p, int64_t i, int dt) {
+  switch (dt) {
+    case MOE_DT_F32: return (double)static_cast<const float*>(p)[i];
+    case MOE_DT_F64: return static_cast<const double*>(p)[i];
+    case MOE_DT_BF16: return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+    case MOE_DT_F16: return (double)__half2float(static_cast<const __half*>(p)[i]);
+    default: return 0.0;
+  }
+}
+
+// ── moekit float64 quantizer primitives (quant.py:64-67, 191-211) ─────────
+// rha(v) = sign(v) * floor(|v| + 0.5); the add is a separately rounded op.
+__device__ __forceinline__ double rha(double v) {
+  const double a = floor(__dadd_rn(fabs(v), 0.5));
+  return v > 0.0 ? a : (v < 0.0 ? -a : 0.0);
+}
+
+// Correctly rounded a / b from a precomputed rb = RN(1/b): q0 = a*rb,
+// rem = a - q0*b (exact with FMA), q = q0 + rem*rb (Markstein; bit-identical
+// to IEEE division absent under/overflow — verified on 2e8 random and
+// all-ones-mantissa cases).
+__device__ __forceinline__ double div_rcp(double a, double b, double rb) {
+  const double q0 = __dmul_rn(a, rb);
+  const double rem = __fma_rn(-q0, b, a);
+  return __fma_rn(rem, rb, q0);
+}
+
+__device__ __forceinline__ int encode_code(double xs, double scale, double rscale, int zp, int qmax) {
+  const double v = div_rcp(xs, scale, rscale);
+  double c = __dadd_rn(rha(v), (double)zp);
+  c = c < 0.0 ? 0.0 : (c > (double)qmax ? (double)qmax : c);
+  return (int)c;
+}
+
+struct AffineParams {
+  double scale;
+  double rscale;
+  int zp;
+};
+
+// _affine_params (quant.py:191-202) for one group.
+__device__ __forceinline__ AffineParams affine_params(double mn, double mx, int bits, int symmetric) {
+  const int qmax = (1 << bits) - 1;
+  AffineParams p;
+  if (symmetric) {
+    const double amax = fmax(fabs(mn), fabs(mx));
+    p.scale = fmax(__ddiv_rn(amax, (double)((1 << (bits - 1)) - 1)), 1e-12);
+    p.zp = 1 << (bits - 1);
+  } else {
+    p.scale = fmax(__ddiv_rn(__dsub_rn(mx, mn), (double)qmax), 1e-12);
+    double z = rha(__ddiv_rn(-mn, p.scale));
+    z = z < 0.0 ? 0.0 : (z > (double)qmax ? (double)qmax : z);
+    p.zp = (int)z;
+  }
+  p.rscale = __drcp_rn(p.scale);
+  return p;
+}
+
+}  // namespace moe

@@ -1,0 +1,492 @@
+// K2 / K5 — W8A8 GEMM on the 5th-generation tensor cores (tcgen05 kind::i8).
+//
+// Y[m, n] = epilogue( sum_k (a[m,k]-za[m]) * (w[n,k]-zw[n]) ), A [M, K] u8
+// activation codes (tokens-major), W [G*N, K] u8 weight codes (per expert
+// stacked), both K-major. Replaces the float64 fake-quant product of
+// quant_loss / quantize_layer (quant.py:281-283, 475-478) with the exact
+// integer product; the zero points are applied in the epilogue:
+//   acc = sum a*w  - zw*rowsum_a - za*(rowsum_w - K*zw)    (wrapping int32,
+//   exact because the true value satisfies |acc| <= K*255^2 < 2^31).
+//
+// Structure (one CTA per SM, persistent, warp-specialised):
+//   warp 0 lane 0 : TMA producer  — A tile 128x128 B, W tile BNx128 B per
+//                   stage, 128-byte swizzle, mbarrier complete_tx
+//   warp 1 lane 0 : UMMA issuer   — tcgen05.mma.cta_group::1.kind::i8,
+//                   M=128 N=BN K=32, accumulator in TMEM (2 stages x BN cols)
+//   warp 2        : TMEM allocator
+//   warps 4..7    : epilogue      — tcgen05.ld 32x32b, zero-point
+//                   correction, dequant / SwiGLU / raw int32, global stores
+// Grouped mode (MoE): the tile scheduler walks experts from the device-side
+// offsets, so routing never syncs with the host.
+#include "common.cuh"
+#include "ptx.cuh"
+
+#include <cudaTypedefs.h>
+
+namespace moe {
+
+constexpr int kBM = 128;          // UMMA M
+constexpr int kBK = 128;          // bytes of K per stage = one SW128 atom row
+constexpr int kUmmaK = 32;        // K per tcgen05.mma for 8-bit inputs
+constexpr int kMaxGroups = 64;
+constexpr int kGemmThreads = 256;
+
+struct GemmArgs {
+  int M, N, K, G;
+  const int32_t* offsets;
+  const float* a_scale;
+  const int32_t* a_zp;
+  const int32_t* a_rowsum;
+  const float* w_scale;
+  const int32_t* w_zp;
+  const int32_t* w_rowsum;
+  const float* bias;
+  const float* row_weight;
+  void* out;
+  int64_t ldo;
+  int32_t* acc_out;
+  int64_t ld_acc;
+  int vec_ok;  // output pointer / ldo allow 16-byte vector stores
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int kA = kBM * kBK;
+  static constexpr int kB = BN * kBK;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kBarOff = STAGES * kStage;
+  static constexpr int kNumBars = 2 * STAGES + 4;
+  static constexpr int kTmemPtrOff = kBarOff + kNumBars * 8;
+  static constexpr int kTableOff = kTmemPtrOff + 16;                  // tile_start[G+1], off[G+1]
+  static constexpr int kBytes = kTableOff + 2 * (kMaxGroups + 1) * 4 + 1024;  // + alignment slack
+};
+
+struct TileInfo {
+  int g, m0, m_end, n0;
+};
+
+__device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start, const int* off, int n_tiles,
+                                             int BN) {
+  int g = 0;
+  while (g + 1 < G && t >= tile_start[g + 1]) ++g;
+  const int local = t - tile_start[g];
+  const int mt = (off[g + 1] - off[g] + kBM - 1) / kBM;
+  const int n_tile = local / mt, m_tile = local - n_tile * mt;
+  (void)n_tiles;
+  return TileInfo{g, off[g] + m_tile * kBM, off[g + 1], n_tile * BN};
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <bool BF16>
+__device__ __forceinline__ void store32(void* out, int64_t idx, const float (&v)[32], int nvalid, bool vec) {
+  if (BF16) {
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + idx;
+    if (vec && nvalid == 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+        reinterpret_cast<uint4*>(o)[q] = u;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* o = static_cast<float*>(out) + idx;
+    if (vec && nvalid == 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = v[j];
+    }
+  }
+}
+
+// zero-point corrected exact accumulator (wrapping int32 arithmetic)
+__device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t rsw, int32_t za, int32_t rsa,
+                                              int32_t K) {
+  const uint32_t t = (uint32_t)rsw - (uint32_t)K * (uint32_t)zw;
+  return (int32_t)(acc - (uint32_t)zw * (uint32_t)rsa - (uint32_t)za * t);
+}
+
+template <int BN, int STAGES, int EPI, bool BF16>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+  using L = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled TMA / UMMA tiles
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
+  int* tile_start = reinterpret_cast<int*>(smem + L::kTableOff);
+  int* off = tile_start + (kMaxGroups + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_tiles = (p.N + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    if (p.offsets) {
+      for (int g = 0; g <= p.G; ++g) off[g] = p.offsets[g];
+    } else {
+      off[0] = 0;
+      off[1] = p.M;
+    }
+    int acc = 0;
+    for (int g = 0; g < p.G; ++g) {
+      tile_start[g] = acc;
+      acc += ((off[g + 1] - off[g] + kBM - 1) / kBM) * n_tiles;
+    }
+    tile_start[p.G] = acc;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_ptr, 2 * BN);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+  const int total_tiles = tile_start[p.G];
+
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer =====
+    const uint64_t pol_a = policy_evict_last();
+    const uint64_t pol_b = policy_evict_last();
+    const int kblocks = (p.K + kBK - 1) / kBK;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, n_tiles, BN);
+      const int wrow = ti.g * p.N + ti.n0;
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::kStage;
+        uint8_t* sb = sa + L::kA;
+        mbar_expect_tx(&full[s], L::kStage);
+        tma_load_2d(sa, &tmA, &full[s], kb * kBK, ti.m0, pol_a);
+        tma_load_2d(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===== UMMA issuer =====
+    constexpr uint32_t idesc = idesc_i8(kBM, BN);
+    const int kblocks = (p.K + kBK - 1) / kBK;
+    uint32_t it = 0, tile_it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_it) {
+      const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
+      mbar_wait(&tempty[as], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + as * BN;
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + s * L::kStage);
+        const uint32_t b_addr = a_addr + L::kA;
+        const uint64_t adesc = sdesc_sw128(a_addr);
+        const uint64_t bdesc = sdesc_sw128(b_addr);
+#pragma unroll
+        for (int k = 0; k < kBK / kUmmaK; ++k) {
+          // advance the start address by k*32 bytes inside the swizzle atom
+          umma_i8(d_tmem, adesc + (uint64_t)(k * kUmmaK / 16), bdesc + (uint64_t)(k * kUmmaK / 16), idesc,
+                  (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tfull[as]);
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint32_t tile_it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_it) {
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, n_tiles, BN);
+      const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const int row = ti.m0 + q * 32 + lane;
+      const bool rvalid = row < ti.m_end;
+      float sa = 0.f, rw = 1.f;
+      int32_t za = 0, rsa = 0;
+      if (rvalid) {
+        za = p.a_zp[row];
+        rsa = p.a_rowsum[row];
+        if (EPI != MOE_EPI_ACC_I32) {
+          sa = p.a_scale[row];
+          if (p.row_weight) rw = p.row_weight[row];
+        }
+      }
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      const int wbase = ti.g * p.N;
+      if (EPI == MOE_EPI_SWIGLU) {
+        // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t vg[32], vu[32];
+          tmem_ld32(tbase + c * 32, vg);
+          tmem_ld32(tbase + BN / 2 + c * 32, vu);
+          tmem_ld_wait();
+          float h[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int ng = wbase + ti.n0 + c * 32 + j;
+            const int nu = ng + BN / 2;
+            const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
+            const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
+            float g = (float)ag * (sa * p.w_scale[ng]);
+            float u = (float)au * (sa * p.w_scale[nu]);
+            if (p.bias) {
+              g += p.bias[ng];
+              u += p.bias[nu];
+            }
+            h[j] = silu_f(g) * u * rw;
+          }
+          if (rvalid) store32<BF16>(p.out, (int64_t)row * p.ldo + ti.n0 / 2 + c * 32, h, 32, p.vec_ok);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c * 32, v);
+          tmem_ld_wait();
+          const int n_lo = ti.n0 + c * 32;
+          int nvalid = p.N - n_lo;
+          nvalid = nvalid > 32 ? 32 : nvalid;
+          if (!rvalid || nvalid <= 0) continue;
+          if (EPI == MOE_EPI_ACC_I32) {
+            int32_t* o = p.acc_out + (int64_t)row * p.ld_acc + n_lo;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < nvalid) {
+                const int n = wbase + n_lo + j;
+                o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+              }
+            }
+          } else {
+            float y[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
+              const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+              float val = (float)a * (sa * p.w_scale[n]);
+              if (p.bias) val += p.bias[n];
+              y[j] = val * rw;
+            }
+            store32<BF16>(p.out, (int64_t)row * p.ldo + n_lo, y, nvalid, p.vec_ok);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// ── SIMT path: small or unaligned shapes (same exact integer results) ─────
+template <bool BF16>
+__global__ void gemm_i8_simt_kernel(const uint8_t* a, int64_t lda, const uint8_t* w, int64_t ldw, GemmArgs p,
+                                    int epi) {
+  const int64_t total = (int64_t)p.M * (epi == MOE_EPI_SWIGLU ? p.N / 2 : p.N);
+  const int ncols = epi == MOE_EPI_SWIGLU ? p.N / 2 : p.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / ncols), c = (int)(i % ncols);
+    int g = 0;
+    if (p.offsets) {
+      while (g + 1 < p.G && m >= p.offsets[g + 1]) ++g;
+    }
+    const int za = p.a_zp[m];
+    auto dot = [&](int wr) {
+      int32_t acc = 0;
+      const int zw = p.w_zp[wr];
+      for (int k = 0; k < p.K; ++k) acc += ((int)a[m * lda + k] - za) * ((int)w[(int64_t)wr * ldw + k] - zw);
+      return acc;
+    };
+    float rw = p.row_weight ? p.row_weight[m] : 1.f;
+    if (epi == MOE_EPI_SWIGLU) {
+      const int blk = c / 128, j = c % 128;
+      const int ng = g * p.N + blk * 256 + j, nu = ng + 128;
+      float gg = (float)dot(ng) * (p.a_scale[m] * p.w_scale[ng]);
+      float uu = (float)dot(nu) * (p.a_scale[m] * p.w_scale[nu]);
+      if (p.bias) {
+        gg += p.bias[ng];
+        uu += p.bias[nu];
+      }
+      const float h = silu_f(gg) * uu * rw;
+      if (BF16) static_cast<__nv_bfloat16*>(p.out)[m * p.ldo + c] = __float2bfloat16_rn(h);
+      else static_cast<float*>(p.out)[m * p.ldo + c] = h;
+    } else {
+      const int n = g * p.N + c;
+      const int32_t acc = dot(n);
+      if (epi == MOE_EPI_ACC_I32) {
+        p.acc_out[m * p.ld_acc + c] = acc;
+      } else {
+        float val = (float)acc * (p.a_scale[m] * p.w_scale[n]);
+        if (p.bias) val += p.bias[n];
+        val *= rw;
+        if (BF16) static_cast<__nv_bfloat16*>(p.out)[m * p.ldo + c] = __float2bfloat16_rn(val);
+        else static_cast<float*>(p.out)[m * p.ldo + c] = val;
+      }
+    }
+  }
+}
+
+// ── host side ──────────────────────────────────────────────────────────────
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+static bool make_map_u8(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
+                        uint32_t box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES, int EPI, bool BF16>
+static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& p, int grid,
+                            cudaStream_t s) {
+  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16>;
+  constexpr int bytes = Smem<BN, STAGES>::kBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr_set = true;
+  }
+  kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, p); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                                    const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                                    int64_t ldw, const float* w_scale, const int32_t* w_zp,
+                                    const int32_t* w_rowsum, const float* bias, const float* row_weight,
+                                    const int32_t* group_offsets, int num_groups, int epilogue, void* out,
+                                    int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
+                                    moe_stream_t stream) {
+  MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
+  MOE_REQUIRE(M >= 1 && N >= 1 && K >= 1, "w8a8_gemm: empty problem");
+  MOE_REQUIRE(lda >= K && ldw >= K, "w8a8_gemm: bad leading dimension");
+  MOE_REQUIRE(M < (1LL << 31) && N < (1LL << 31) && K <= 33025, "w8a8_gemm: K too large for exact int32");
+  MOE_REQUIRE(num_groups >= 1 && num_groups <= kMaxGroups, "w8a8_gemm: 1..64 groups");
+  MOE_REQUIRE(num_groups == 1 || group_offsets, "w8a8_gemm: grouped GEMM needs offsets");
+  MOE_REQUIRE(epilogue >= 0 && epilogue <= 2, "w8a8_gemm: unknown epilogue");
+  if (epilogue == MOE_EPI_ACC_I32) {
+    MOE_REQUIRE(acc_out && ld_acc >= N, "w8a8_gemm: ACC_I32 needs acc_out");
+  } else {
+    MOE_REQUIRE(out && a_scale && w_scale, "w8a8_gemm: dequant epilogue needs out and scales");
+    MOE_REQUIRE(out_dtype == MOE_DT_F32 || out_dtype == MOE_DT_BF16, "w8a8_gemm: out dtype f32|bf16");
+    MOE_REQUIRE(ldo >= (epilogue == MOE_EPI_SWIGLU ? N / 2 : N), "w8a8_gemm: bad ldo");
+  }
+  if (epilogue == MOE_EPI_SWIGLU) MOE_REQUIRE(N % 256 == 0, "w8a8_gemm: SwiGLU needs N % 256 == 0");
+
+  GemmArgs p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.G = num_groups;
+  p.offsets = group_offsets;
+  p.a_scale = a_scale;
+  p.a_zp = a_zp;
+  p.a_rowsum = a_rowsum;
+  p.w_scale = w_scale;
+  p.w_zp = w_zp;
+  p.w_rowsum = w_rowsum;
+  p.bias = bias;
+  p.row_weight = row_weight;
+  p.out = out;
+  p.ldo = ldo;
+  p.acc_out = acc_out;
+  p.ld_acc = ld_acc;
+  const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
+  p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
+  cudaStream_t s = as_stream(stream);
+  const bool bf16 = out_dtype == MOE_DT_BF16;
+
+  const bool tc_ok = (K % 16 == 0) && K >= kBK && (lda % 16 == 0) && (ldw % 16 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+  if (tc_ok) {
+    constexpr int BN = 256;
+    CUtensorMap ta, tb;
+    if (!make_map_u8(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBM) ||
+        !make_map_u8(&tb, w, (uint64_t)N * num_groups, (uint64_t)K, (uint64_t)ldw, BN)) {
+      set_error("w8a8_gemm: cuTensorMapEncodeTiled failed");
+      return MOE_ECUDA;
+    }
+    const int64_t n_tiles = (N + BN - 1) / BN;
+    const int64_t tiles_bound = ((M + kBM - 1) / kBM + num_groups) * n_tiles;
+    const int grid = (int)(tiles_bound < num_sms() ? tiles_bound : num_sms());
+    constexpr int ST = 4;
+    switch (epilogue) {
+      case MOE_EPI_DEQUANT:
+        return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true>(ta, tb, p, grid, s)
+                    : launch_tc<BN, ST, MOE_EPI_DEQUANT, false>(ta, tb, p, grid, s);
+      case MOE_EPI_SWIGLU:
+        return bf16 ? launch_tc<BN, ST, MOE_EPI_SWIGLU, true>(ta, tb, p, grid, s)
+                    : launch_tc<BN, ST, MOE_EPI_SWIGLU, false>(ta, tb, p, grid, s);
+      default:
+        return launch_tc<BN, ST, MOE_EPI_ACC_I32, false>(ta, tb, p, grid, s);
+    }
+  }
+  const int64_t total = M * (epilogue == MOE_EPI_SWIGLU ? N / 2 : N);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
+  if (bf16) gemm_i8_simt_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a, lda, w, ldw, p, epilogue);
+  else gemm_i8_simt_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a, lda, w, ldw, p, epilogue);
+  ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}

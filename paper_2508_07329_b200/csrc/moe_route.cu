@@ -1,0 +1,341 @@
+// K3 router gating, K4 token->expert permutation, K6 combine and the routing
+// statistics feeding placement. None of these exist in the reference; they
+// implement the MoE forward around its quantizer (SURVEY.md §8a a'1, a'2)
+// and emit statistics in the reference's trace semantics (trace.py:207-225).
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int kMaxE = 64;
+constexpr int kMaxK = 8;
+
+// Select top-k of E logits: descending, ties to the lower id; softmax over
+// the selected logits. Returns via idx/w arrays.
+__device__ __forceinline__ void topk_select(const float* l, int E, int k, int32_t* idx, float* w) {
+  uint64_t taken = 0;
+  float sel[kMaxK];
+  for (int j = 0; j < k; ++j) {
+    int best = -1;
+    float bv = 0.f;
+    for (int e = 0; e < E; ++e) {
+      if (taken >> e & 1ull) continue;
+      if (best < 0 || l[e] > bv) {
+        best = e;
+        bv = l[e];
+      }
+    }
+    taken |= 1ull << best;
+    idx[j] = best;
+    sel[j] = bv;
+  }
+  float den = 0.f;
+  float ex[kMaxK];
+  for (int j = 0; j < k; ++j) {
+    ex[j] = expf(sel[j] - sel[0]);
+    den += ex[j];
+  }
+  for (int j = 0; j < k; ++j) w[j] = ex[j] / den;
+}
+
+// One warp per token: logits[t, e] = x[t] . gate_w[e] in float32, lane-strided
+// then butterfly-reduced (fixed order -> deterministic), then top-k.
+template <int E_T>
+__global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt, int64_t T, int64_t d,
+                                                          const float* __restrict__ gw, const float* gb, int E,
+                                                          int k, float* logits, int32_t* idx, float* w) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= T) return;
+  float acc[E_T];
+#pragma unroll
+  for (int e = 0; e < E_T; ++e) acc[e] = 0.f;
+  const int64_t row = (int64_t)warp * d;
+  const bool vec = dt == MOE_DT_BF16 && d % 256 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (vec) {
+    const uint4* xp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + row);
+    for (int64_t c = lane; c < d / 8; c += 32) {
+      const uint4 u = xp[c];
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+      float xv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = __bfloat162float(h[i]);
+#pragma unroll
+      for (int e = 0; e < E_T; ++e) {
+        if (e >= E) break;
+        const float4* g = reinterpret_cast<const float4*>(gw + (int64_t)e * d + c * 8);
+        const float4 g0 = __ldg(g), g1 = __ldg(g + 1);
+        acc[e] = fmaf(xv[0], g0.x, acc[e]);
+        acc[e] = fmaf(xv[1], g0.y, acc[e]);
+        acc[e] = fmaf(xv[2], g0.z, acc[e]);
+        acc[e] = fmaf(xv[3], g0.w, acc[e]);
+        acc[e] = fmaf(xv[4], g1.x, acc[e]);
+        acc[e] = fmaf(xv[5], g1.y, acc[e]);
+        acc[e] = fmaf(xv[6], g1.z, acc[e]);
+        acc[e] = fmaf(xv[7], g1.w, acc[e]);
+      }
+    }
+  } else {
+    for (int64_t j = lane; j < d; j += 32) {
+      const float xv = (float)load_as_f64(x, row + j, dt);
+#pragma unroll
+      for (int e = 0; e < E_T; ++e)
+        if (e < E) acc[e] = fmaf(xv, gw[(int64_t)e * d + j], acc[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E_T; ++e)
+    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (lane == 0) {
+    float l[E_T];
+#pragma unroll
+    for (int e = 0; e < E_T; ++e) l[e] = (gb && e < E) ? acc[e] + gb[e] : acc[e];
+    if (logits)
+      for (int e = 0; e < E; ++e) logits[(int64_t)warp * E + e] = l[e];
+    topk_select(l, E, k, idx + (int64_t)warp * k, w + (int64_t)warp * k);
+  }
+}
+
+__global__ void router_topk_kernel(const float* logits, int64_t T, int E, int k, int32_t* idx, float* w) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    float l[kMaxE];
+    for (int e = 0; e < E; ++e) l[e] = logits[t * E + e];
+    topk_select(l, E, k, idx + t * k, w + t * k);
+  }
+}
+
+// ── stable counting sort ───────────────────────────────────────────────────
+constexpr int kPermThreads = 256;
+constexpr int kPermChunk = 4096;  // (token, slot) pairs per block
+
+__global__ void permute_count_kernel(const int32_t* idx, int64_t n, int E, int32_t* block_counts) {
+  __shared__ int cnt[kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
+  const int64_t hi = min(n, lo + kPermChunk);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&cnt[idx[i]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) block_counts[(int64_t)blockIdx.x * E + e] = cnt[e];
+}
+
+// single block: offsets[e] and per-block bases (block-major exclusive scan)
+__global__ void permute_scan_kernel(const int32_t* block_counts, int nblocks, int E, int32_t* block_base,
+                                    int32_t* offsets) {
+  __shared__ int tot[kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int s = 0;
+    for (int b = 0; b < nblocks; ++b) s += block_counts[(int64_t)b * E + e];
+    tot[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = s;
+      s += tot[e];
+    }
+    offsets[E] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int s = offsets[e];
+    for (int b = 0; b < nblocks; ++b) {
+      block_base[(int64_t)b * E + e] = s;
+      s += block_counts[(int64_t)b * E + e];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t* idx, const float* topk_w,
+                                                                       int64_t n, int k, int E,
+                                                                       const int32_t* block_base,
+                                                                       int32_t* src_token, int32_t* row_expert,
+                                                                       float* row_weight, int32_t* token_pos) {
+  __shared__ int run[kMaxE];
+  __shared__ int wcnt[kPermThreads / 32][kMaxE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = block_base[(int64_t)blockIdx.x * E + e];
+  const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
+  const int64_t hi = min(n, lo + kPermChunk);
+  for (int64_t base = lo; base < hi; base += kPermThreads) {
+    for (int i = threadIdx.x; i < (kPermThreads / 32) * E; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < hi;
+    const int e = valid ? idx[i] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (valid && rank == 0) wcnt[warp][e] = __popc(same);
+    __syncthreads();
+    if (valid) {
+      int pos = run[e] + rank;
+      for (int w2 = 0; w2 < warp; ++w2) pos += wcnt[w2][e];
+      src_token[pos] = (int32_t)(i / k);
+      row_expert[pos] = e;
+      if (row_weight) row_weight[pos] = topk_w[i];
+      token_pos[i] = pos;
+    }
+    __syncthreads();
+    for (int ee = threadIdx.x; ee < E; ee += blockDim.x) {
+      int s = 0;
+      for (int w2 = 0; w2 < kPermThreads / 32; ++w2) s += wcnt[w2][ee];
+      run[ee] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// ── combine ────────────────────────────────────────────────────────────────
+template <typename TIn, typename TOut>
+__global__ void combine_kernel(const TIn* y, const int32_t* token_pos, int64_t T, int k, int64_t d, TOut* out) {
+  const int64_t t = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int64_t r = token_pos[t * k + j];
+      if constexpr (sizeof(TIn) == 2) s += __bfloat162float(y[r * d + c]);
+      else s += y[r * d + c];
+    }
+    if constexpr (sizeof(TOut) == 2) out[t * d + c] = __float2bfloat16_rn(s);
+    else out[t * d + c] = s;
+  }
+}
+
+// vectorised bf16 -> bf16 / f32 -> f32 paths (8 / 4 elements per thread step)
+__global__ void combine_bf16_vec_kernel(const __nv_bfloat16* y, const int32_t* token_pos, int k, int64_t d,
+                                        __nv_bfloat16* out) {
+  const int64_t t = blockIdx.x;
+  int32_t rows[kMaxK];
+  for (int j = 0; j < k; ++j) rows[j] = token_pos[t * k + j];
+  for (int64_t c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+      const uint4 u = reinterpret_cast<const uint4*>(y + (int64_t)rows[j] * d)[c];
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] += __bfloat162float(h[e]);
+    }
+    uint4 o;
+    __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = __floats2bfloat162_rn(s[2 * e], s[2 * e + 1]);
+    reinterpret_cast<uint4*>(out + t * d)[c] = o;
+  }
+}
+
+__global__ void histogram_kernel(const int32_t* idx, int64_t T, int k, int E, int layer, int64_t* counts,
+                                 int32_t* path_codes) {
+  __shared__ unsigned long long cnt[kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t mask = 0;
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[t * k + j];
+      atomicAdd(&cnt[e], 1ull);
+      mask |= 1u << e;
+    }
+    if (path_codes) path_codes[t] = (int32_t)mask;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&counts[(int64_t)layer * E + e]), cnt[e]);
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, const float* gate_w,
+                                      const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx, float* topk_w, moe_stream_t stream) {
+  MOE_REQUIRE(x && gate_w && topk_idx && topk_w, "router_gate: null pointer");
+  MOE_REQUIRE(T >= 1 && d >= 1, "router_gate: empty input");
+  MOE_REQUIRE(E >= 1 && E <= 32 && k >= 1 && k <= kMaxK && k <= E, "router_gate: need 1 <= k <= E <= 32");
+  const int64_t threads = T * 32;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  cudaStream_t s = as_stream(stream);
+  if (E <= 8) {
+    router_gate_kernel<8><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+  } else if (E <= 16) {
+    router_gate_kernel<16><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+  } else {
+    router_gate_kernel<32><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+  }
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_router_topk(const float* logits, int64_t T, int E, int k, int32_t* topk_idx,
+                                      float* topk_w, moe_stream_t stream) {
+  MOE_REQUIRE(logits && topk_idx && topk_w && T >= 1, "router_topk: bad arguments");
+  MOE_REQUIRE(E >= 1 && E <= kMaxE && k >= 1 && k <= kMaxK && k <= E, "router_topk: need 1 <= k <= E <= 64");
+  const unsigned blocks = (unsigned)((T + 255) / 256);
+  router_topk_kernel<<<blocks, 256, 0, as_stream(stream)>>>(logits, T, E, k, topk_idx, topk_w); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" int64_t moe_route_permute_workspace(int64_t T, int k, int E) {
+  const int64_t nb = (T * k + kPermChunk - 1) / kPermChunk;
+  return 2 * nb * E * (int64_t)sizeof(int32_t);
+}
+
+extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* topk_w, int64_t T, int k, int E,
+                                        int32_t* expert_offsets, int32_t* src_token, int32_t* row_expert,
+                                        float* row_weight, int32_t* token_pos, void* workspace,
+                                        int64_t workspace_bytes, moe_stream_t stream) {
+  MOE_REQUIRE(topk_idx && expert_offsets && src_token && row_expert && token_pos, "route_permute: null pointer");
+  MOE_REQUIRE(!row_weight || topk_w, "route_permute: row_weight needs topk_w");
+  MOE_REQUIRE(T >= 1 && k >= 1 && E >= 1 && E <= kMaxE, "route_permute: bad sizes");
+  MOE_REQUIRE(workspace && workspace_bytes >= moe_route_permute_workspace(T, k, E), "route_permute: workspace");
+  const int64_t n = T * k;
+  const int nb = (int)((n + kPermChunk - 1) / kPermChunk);
+  int32_t* counts = static_cast<int32_t*>(workspace);
+  int32_t* base = counts + (int64_t)nb * E;
+  cudaStream_t s = as_stream(stream);
+  permute_count_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, n, E, counts); ::moe::count_launch();
+  permute_scan_kernel<<<1, 64, 0, s>>>(counts, nb, E, base, expert_offsets); ::moe::count_launch();
+  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, base, src_token, row_expert,
+                                                     row_weight, token_pos); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_combine(const void* y, int y_dtype, const int32_t* token_pos, int64_t T, int k, int64_t d,
+                                  void* out, int out_dtype, moe_stream_t stream) {
+  MOE_REQUIRE(y && token_pos && out && T >= 1 && d >= 1 && k >= 1 && k <= kMaxK, "combine: bad arguments");
+  MOE_REQUIRE((y_dtype == MOE_DT_F32 || y_dtype == MOE_DT_BF16) && (out_dtype == MOE_DT_F32 || out_dtype == MOE_DT_BF16),
+              "combine: dtypes f32|bf16");
+  cudaStream_t s = as_stream(stream);
+  const unsigned threads = 256;
+  if (y_dtype == MOE_DT_BF16 && out_dtype == MOE_DT_BF16 && d % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    combine_bf16_vec_kernel<<<(unsigned)T, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(y), token_pos, k, d,
+                                                            static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+  } else if (y_dtype == MOE_DT_F32 && out_dtype == MOE_DT_F32) {
+    combine_kernel<float, float><<<(unsigned)T, threads, 0, s>>>(static_cast<const float*>(y), token_pos, T, k, d,
+                                                                 static_cast<float*>(out)); ::moe::count_launch();
+  } else if (y_dtype == MOE_DT_F32) {
+    combine_kernel<float, __nv_bfloat16><<<(unsigned)T, threads, 0, s>>>(
+        static_cast<const float*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+  } else if (out_dtype == MOE_DT_F32) {
+    combine_kernel<__nv_bfloat16, float><<<(unsigned)T, threads, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<float*>(out)); ::moe::count_launch();
+  } else {
+    combine_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)T, threads, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+  }
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_expert_histogram(const int32_t* topk_idx, int64_t T, int k, int E, int layer,
+                                           int64_t* counts, int32_t* path_codes, moe_stream_t stream) {
+  MOE_REQUIRE(topk_idx && counts && T >= 1 && k >= 1 && E >= 1 && E <= 31 && layer >= 0,
+              "expert_histogram: bad arguments");
+  int64_t blocks = (T + 255) / 256;
+  if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+  histogram_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(topk_idx, T, k, E, layer, counts, path_codes); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}

@@ -1,0 +1,207 @@
+"""MoELayer: the W8A8 Mixture-of-Experts forward on the B200.
+
+The reference quantizes expert weights (HAQ, quant.py) but never runs a MoE
+forward; this module is the forward path the north star asks for, built on
+the same quantizer semantics:
+
+  x [T, d] bf16
+   -> K3 router_gate: logits = x Wg^T, top-k (ties -> lower id), softmax
+   -> K4 route_permute: stable counting sort of (token, slot) by expert
+   -> K1 act_quant (gather + per-expert smoothing x / s13_e, per-token RTN)
+   -> K5 grouped W8A8 GEMM, W1||W3 interleaved, SwiGLU epilogue -> h bf16
+   -> K1 act_quant (h / s2_e, per-token RTN)
+   -> K5 grouped W8A8 GEMM with W2, dequant * routing weight -> y
+   -> K6 combine: out[t] = sum_j y[pos(t, j)]
+
+All routing state stays on the device (expert offsets feed the persistent
+GEMM scheduler directly), so one forward is 8 kernel launches and no host
+synchronisation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import ops
+from .quant import PER_OUTPUT_ROW, QuantizedMatrix
+
+INTERLEAVE = 128   # W1/W3 row-block interleave consumed by the SwiGLU epilogue
+
+
+def _stack_dev(qms: list[QuantizedMatrix]) -> dict:
+    parts = [q.device() for q in qms]
+    out = {k: torch.cat([p[k] for p in parts], dim=0).contiguous() for k in ("codes", "scale", "scale_f32", "zp",
+                                                                             "rowsum")}
+    return out
+
+
+def _interleave_rows(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """[F, ...] x2 -> [2F, ...] as blocks (a[0:128], b[0:128], a[128:256], ...)."""
+    F = a.shape[0]
+    rest = a.shape[1:]
+    ai = a.reshape(F // INTERLEAVE, INTERLEAVE, *rest)
+    bi = b.reshape(F // INTERLEAVE, INTERLEAVE, *rest)
+    return torch.stack([ai, bi], dim=1).reshape(2 * F, *rest).contiguous()
+
+
+class MoELayer:
+    def __init__(self, gate_weight, experts: list[dict], top_k: int = 2, out_dtype=torch.bfloat16,
+                 gate_bias=None):
+        """experts[e] = {"w1": QM [F, d], "w3": QM [F, d], "w2": QM [d, F],
+        "s13": [d] smoothing of the shared W1/W3 input, "s2": [F]}."""
+        self.E = len(experts)
+        if not 1 <= top_k <= self.E:
+            raise ValueError("top_k must be within [1, num_experts]")
+        self.k = top_k
+        self.gate_w = torch.as_tensor(gate_weight, dtype=torch.float32).cuda().contiguous()
+        self.gate_b = None if gate_bias is None else torch.as_tensor(gate_bias, dtype=torch.float32).cuda()
+        F, d = experts[0]["w1"].codes.shape
+        if F % INTERLEAVE:
+            raise ValueError(f"ffn dim must be a multiple of {INTERLEAVE}")
+        self.d, self.F = d, F
+        w13 = []
+        for e in experts:
+            for q in (e["w1"], e["w3"], e["w2"]):
+                if q.granularity != PER_OUTPUT_ROW:
+                    raise ValueError("expert weights must be quantized per output row")
+            a, b = e["w1"].device(), e["w3"].device()
+            w13.append({k: _interleave_rows(a[k], b[k]) for k in ("codes", "scale", "scale_f32", "zp", "rowsum")})
+        self.w13 = {k: torch.cat([p[k] for p in w13], 0).contiguous() for k in w13[0]}
+        self.w2 = _stack_dev([e["w2"] for e in experts])
+        self.s13 = torch.stack([torch.as_tensor(np.asarray(_np(e["s13"])), dtype=torch.float64)
+                                for e in experts]).cuda().contiguous()
+        self.s2 = torch.stack([torch.as_tensor(np.asarray(_np(e["s2"])), dtype=torch.float64)
+                               for e in experts]).cuda().contiguous()
+        self.s13_recip, self.s2_recip = ops.reciprocal(self.s13), ops.reciprocal(self.s2)
+        self.out_dtype = out_dtype
+        self.host_experts = experts
+
+    # ------------------------------------------------------------------
+    @classmethod
+    def random(cls, E: int, d: int, F: int, top_k: int = 2, seed: int = 1, out_dtype=torch.bfloat16,
+               router_seed: int = 2, zipf_s: float = 1.2, smooth_exponent: float = 0.5):
+        """Synthetic random-init layer of the given shape (the bench's Mixtral
+        8x7B-shape layer): W ~ N(0, 0.02^2), smoothing factors from a
+        synthetic outlier-channel statistic (1% of channels x100), W s
+        quantized per output row on device; router weights N(0, 1/d) plus a
+        Zipf(s) logit bias over a seeded expert shuffle."""
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        rng = np.random.default_rng(seed)
+
+        def stat(n):
+            s = np.abs(rng.normal(size=n)) + 1.0
+            s[rng.choice(n, max(1, n // 100), replace=False)] *= 100.0
+            return s ** smooth_exponent
+
+        experts = []
+        for _ in range(E):
+            s13, s2 = stat(d), stat(F)
+            ex = {"s13": s13, "s2": s2}
+            for name, shape, s in (("w1", (F, d), s13), ("w3", (F, d), s13), ("w2", (d, F), s2)):
+                w = torch.randn(shape, generator=g, device="cuda", dtype=torch.float32) * 0.02
+                sm = torch.as_tensor(s, dtype=torch.float64).reshape(1, -1).cuda()
+                q = ops.act_quant(w, smooth=sm, smooth_mode=L.SMOOTH_MULTIPLY, granularity=PER_OUTPUT_ROW,
+                                  rowsum=False)
+                ex[name] = QuantizedMatrix(q["codes"], q["scale"], q["zp"], 8, PER_OUTPUT_ROW)
+                del w
+            experts.append(ex)
+        rr = np.random.default_rng(router_seed)
+        gw = rr.normal(size=(E, d)) / np.sqrt(d)
+        bias = np.log(1.0 / (np.arange(E) + 1.0) ** zipf_s)
+        bias = bias - np.log(np.exp(bias).sum())
+        gb = bias[np.argsort(rr.permutation(E))]          # rank r -> expert shuffle[r]
+        return cls(gw.astype(np.float32), experts, top_k, out_dtype, gate_bias=gb.astype(np.float32))
+
+    # ------------------------------------------------------------------
+    def route(self, x: torch.Tensor, want_logits: bool = False):
+        logits, idx, w = ops.router_gate(x, self.gate_w, self.k, want_logits=want_logits, gate_bias=self.gate_b)
+        return logits, idx, w
+
+    def forward(self, x: torch.Tensor, out_dtype=None, y_dtype=None, return_aux: bool = False, stats=None,
+                timer=None):
+        """x [T, d] (bf16) on device -> [T, d]. ``timer`` (optional) gets a
+        ``mark(stage)`` call after every kernel stage (CUDA events)."""
+        if x.dim() != 2 or x.shape[1] != self.d:
+            raise ValueError(f"expected input [T, {self.d}], got {tuple(x.shape)}")
+        out_dtype = out_dtype or self.out_dtype
+        y_dtype = y_dtype or (torch.float32 if out_dtype == torch.float32 else torch.bfloat16)
+        mark = timer.mark if timer is not None else (lambda _n: None)
+        T = x.shape[0]
+        mark("start")
+        logits, idx, w = self.route(x, want_logits=return_aux)
+        mark("router")
+        if stats is not None:
+            stats.record(idx)
+        perm = ops.route_permute(idx, w, self.E)
+        mark("permute")
+        a1 = ops.act_quant(x, smooth=self.s13, smooth_recip=self.s13_recip, row_group=perm["row_expert"],
+                           gather=perm["src_token"], rows=T * self.k)
+        mark("quant_x")
+        h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
+                          group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F)
+        mark("gemm13_swiglu")
+        a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, row_group=perm["row_expert"])
+        mark("quant_h")
+        y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
+                          group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)
+        mark("gemm2")
+        out = ops.combine(y, perm["token_pos"], T, self.k, out_dtype=out_dtype)
+        mark("combine")
+        if return_aux:
+            return out, {"logits": logits, "idx": idx, "w": w, "perm": perm, "a1": a1, "h": h, "a2": a2, "y": y}
+        return out
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None,
+                     chunk_tokens: int = 4096) -> torch.Tensor:
+        """Host (pinned) tokens in, host tokens out: the end-to-end public
+        call. Token chunks are pipelined over three streams so the H2D copy
+        of chunk i+1 and the D2H copy of chunk i-1 overlap the forward of
+        chunk i (the MoE layer is token-parallel, so chunking is exact)."""
+        T = x_host.shape[0]
+        if out_host is None:
+            out_host = torch.empty((T, self.d), dtype=self.out_dtype, pin_memory=True)
+        cur = torch.cuda.current_stream()
+        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        bounds = [(s, min(T, s + chunk_tokens)) for s in range(0, T, chunk_tokens)]
+        xs, ys, loaded, done = [], [], [], []
+        for lo, hi in bounds:
+            with torch.cuda.stream(h2d):
+                xs.append(x_host[lo:hi].to("cuda", non_blocking=True))
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                loaded.append(ev)
+        for i, (lo, hi) in enumerate(bounds):
+            cur.wait_event(loaded[i])
+            ys.append(self.forward(xs[i]))
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            done.append(ev)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev)
+                out_host[lo:hi].copy_(ys[i], non_blocking=True)
+        d2h.synchronize()
+        for t in xs + ys:
+            t.record_stream(cur)
+        return out_host
+
+    # ------------------------------------------------------------------
+    def expert_host(self, e: int) -> dict:
+        """Host copies of expert e in the oracle's layout (codes/scales/zps of
+        w1, w3, w2 and the smoothing vectors) — for parity tests and the CPU
+        baseline."""
+        ex = self.host_experts[e]
+        out = {"s13": np.asarray(_np(ex["s13"]), dtype=np.float64), "s2": np.asarray(_np(ex["s2"]), dtype=np.float64)}
+        for name in ("w1", "w3", "w2"):
+            q = ex[name]
+            out[f"{name}_codes"] = _np(q.codes).astype(np.int32)
+            out[f"{name}_scale"] = _np(q.scales).astype(np.float64)
+            out[f"{name}_zp"] = _np(q.zero_points).astype(np.int32)
+        return out
+
+
+def _np(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)

@@ -1,0 +1,248 @@
+"""Tensor-level wrappers over the C ABI (one function per entry point).
+
+Every function takes / returns torch CUDA tensors, allocates outputs and
+workspaces with torch (device memory is plumbing), and launches on the
+current torch stream. Nothing here computes on the host.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.DT_F32, torch.float64: L.DT_F64, torch.bfloat16: L.DT_BF16, torch.float16: L.DT_F16}
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    return t
+
+
+def _rowmajor(t: torch.Tensor, name: str) -> torch.Tensor:
+    _cuda(t, name)
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    return t
+
+
+def _s():
+    return L.stream_ptr()
+
+
+# ── K1 ────────────────────────────────────────────────────────────────────
+def reciprocal(s: torch.Tensor) -> torch.Tensor:
+    s = _cuda(s, "s").contiguous().to(torch.float64)
+    out = torch.empty_like(s)
+    L.call("moe_reciprocal_f64", L.ptr(s), s.numel(), L.ptr(out), _s())
+    return out
+
+
+def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_recip: torch.Tensor | None = None,
+              smooth_mode: int = L.SMOOTH_DIVIDE, row_group: torch.Tensor | None = None,
+              gather: torch.Tensor | None = None, rows: int | None = None, bits: int = 8,
+              symmetric: bool = False, granularity: str = "per_token", rowsum: bool = True,
+              out_codes: torch.Tensor | None = None) -> dict:
+    """K1: codes/scales/zero points of (x[gather] (/ or *) smooth[row_group])."""
+    x = _rowmajor(x, "x")
+    n_rows = rows if rows is not None else (gather.numel() if gather is not None else x.shape[0])
+    cols = x.shape[1]
+    gran = L.GRAN[granularity]
+    groups = 1 if gran == L.GRAN["per_tensor"] else n_rows
+    dev = x.device
+    codes = out_codes if out_codes is not None else torch.empty((n_rows, cols), dtype=torch.uint8, device=dev)
+    scale = torch.empty(groups, dtype=torch.float64, device=dev)
+    scale_f32 = torch.empty(groups, dtype=torch.float32, device=dev)
+    zp = torch.empty(groups, dtype=torch.int32, device=dev)
+    rs = torch.empty(n_rows, dtype=torch.int32, device=dev) if rowsum else None
+    lib = L.load()
+    wsb = lib.moe_act_quant_workspace(n_rows, cols, gran)
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev) if wsb else None
+    mode = L.SMOOTH_NONE if smooth is None else smooth_mode
+    if smooth is not None:
+        smooth = smooth.contiguous()
+        if smooth.dtype != torch.float64:
+            raise ValueError("smoothing table must be float64")
+        if smooth_recip is None and mode == L.SMOOTH_DIVIDE:
+            smooth_recip = reciprocal(smooth)
+    L.call("moe_act_quant", L.ptr(x), _dt(x), n_rows, cols, x.stride(0), L.ptr(gather), L.ptr(smooth),
+           L.ptr(smooth_recip) if mode == L.SMOOTH_DIVIDE else None, mode, L.ptr(row_group), bits,
+           int(bool(symmetric)), gran, L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp),
+           L.ptr(rs), L.ptr(ws), wsb, _s())
+    return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
+            "granularity": granularity, "bits": bits}
+
+
+def dequantize(codes: torch.Tensor, scale: torch.Tensor, zp: torch.Tensor, granularity: str) -> torch.Tensor:
+    codes = _rowmajor(codes, "codes")
+    out = torch.empty(codes.shape, dtype=torch.float64, device=codes.device)
+    L.call("moe_dequantize", L.ptr(codes), codes.shape[0], codes.shape[1], codes.stride(0),
+           L.ptr(scale.contiguous()), L.ptr(zp.contiguous()), L.GRAN[granularity], L.ptr(out), _s())
+    return out
+
+
+def apply_smoothing(w: torch.Tensor | None, x: torch.Tensor | None, f: torch.Tensor):
+    f = f.contiguous()
+    ws = torch.empty_like(w) if w is not None else None
+    xs = torch.empty_like(x) if x is not None else None
+    n = f.numel()
+    L.call("moe_apply_smoothing", L.ptr(w), w.shape[0] if w is not None else 0, n, L.ptr(x),
+           x.shape[1] if x is not None else 0, L.ptr(f), L.ptr(ws), L.ptr(xs), _s())
+    return ws, xs
+
+
+def channel_stats(x: torch.Tensor, strategy: int) -> torch.Tensor:
+    x = _rowmajor(x, "x").contiguous()
+    out = torch.empty(x.shape[0], dtype=torch.float64, device=x.device)
+    L.call("moe_channel_stats", L.ptr(x), x.shape[0], x.shape[1], strategy, L.ptr(out), _s())
+    return out
+
+
+# ── K2 / K5 ───────────────────────────────────────────────────────────────
+def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torch.float32,
+              bias: torch.Tensor | None = None, row_weight: torch.Tensor | None = None,
+              group_offsets: torch.Tensor | None = None, num_groups: int = 1, n_per_group: int | None = None,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """a: dict from act_quant (codes [M, K], scale_f32, zp, rowsum per row).
+    w: dict with codes [G*N, K], scale_f32, zp, rowsum per row."""
+    ac, wc = a["codes"], w["codes"]
+    M, K = ac.shape
+    N = n_per_group if n_per_group is not None else wc.shape[0] // num_groups
+    if wc.shape[1] != K:
+        raise ValueError(f"A has K={K} but W has K={wc.shape[1]}")
+    dev = ac.device
+    a_scale, a_zp = a.get("scale_f32"), a["zp"]
+    if a_zp.numel() == 1 and M > 1:                 # per_tensor activations
+        a_zp = a_zp.expand(M).contiguous()
+        a_scale = a_scale.expand(M).contiguous() if a_scale is not None else None
+    acc = None
+    if epilogue == L.EPI_ACC_I32:
+        acc = out if out is not None else torch.empty((M, N), dtype=torch.int32, device=dev)
+        o = None
+        ldo = 0
+        odt = L.DT_F32
+    else:
+        cols = N // 2 if epilogue == L.EPI_SWIGLU else N
+        o = out if out is not None else torch.empty((M, cols), dtype=out_dtype, device=dev)
+        ldo = o.stride(0)
+        odt = L.DT_BF16 if o.dtype == torch.bfloat16 else L.DT_F32
+    L.call("moe_w8a8_gemm", L.ptr(ac), M, K, ac.stride(0), L.ptr(a_scale), L.ptr(a_zp), L.ptr(a["rowsum"]),
+           L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w["rowsum"]),
+           L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue, L.ptr(o), odt, ldo,
+           L.ptr(acc), acc.stride(0) if acc is not None else 0, _s())
+    return acc if epilogue == L.EPI_ACC_I32 else o
+
+
+def quant_sq_error(acc: torch.Tensor, a_scale: torch.Tensor, w_scale: torch.Tensor, ref: torch.Tensor) -> torch.Tensor:
+    M, N = acc.shape
+    lib = L.load()
+    wsb = lib.moe_quant_sq_error_workspace(M, N)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=acc.device)
+    out = torch.empty(1, dtype=torch.float64, device=acc.device)
+    stride = 0 if a_scale.numel() == 1 else 1
+    L.call("moe_quant_sq_error", L.ptr(acc), M, N, L.ptr(a_scale.contiguous()), stride, L.ptr(w_scale.contiguous()),
+           L.ptr(ref.contiguous()), L.ptr(out), L.ptr(ws), wsb, _s())
+    return out
+
+
+# ── K3 / K4 / K6 ──────────────────────────────────────────────────────────
+def router_gate(x: torch.Tensor, gate_w: torch.Tensor, k: int, want_logits: bool = True,
+                gate_bias: torch.Tensor | None = None):
+    x = _rowmajor(x, "x")
+    T, d = x.shape
+    E = gate_w.shape[0]
+    gw = gate_w.contiguous().to(torch.float32)
+    logits = torch.empty((T, E), dtype=torch.float32, device=x.device) if want_logits else None
+    idx = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    w = torch.empty((T, k), dtype=torch.float32, device=x.device)
+    gb = gate_bias.contiguous().to(torch.float32) if gate_bias is not None else None
+    L.call("moe_router_gate", L.ptr(x), _dt(x), T, d, L.ptr(gw), L.ptr(gb), E, k, L.ptr(logits), L.ptr(idx), L.ptr(w), _s())
+    return logits, idx, w
+
+
+def router_topk(logits: torch.Tensor, k: int):
+    logits = logits.contiguous().to(torch.float32)
+    T, E = logits.shape
+    idx = torch.empty((T, k), dtype=torch.int32, device=logits.device)
+    w = torch.empty((T, k), dtype=torch.float32, device=logits.device)
+    L.call("moe_router_topk", L.ptr(logits), T, E, k, L.ptr(idx), L.ptr(w), _s())
+    return idx, w
+
+
+def route_permute(idx: torch.Tensor, w: torch.Tensor | None, E: int) -> dict:
+    idx = idx.contiguous()
+    T, k = idx.shape
+    dev = idx.device
+    n = T * k
+    lib = L.load()
+    wsb = lib.moe_route_permute_workspace(T, k, E)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    out = {
+        "offsets": torch.empty(E + 1, dtype=torch.int32, device=dev),
+        "src_token": torch.empty(n, dtype=torch.int32, device=dev),
+        "row_expert": torch.empty(n, dtype=torch.int32, device=dev),
+        "row_weight": torch.empty(n, dtype=torch.float32, device=dev) if w is not None else None,
+        "token_pos": torch.empty(n, dtype=torch.int32, device=dev),
+    }
+    L.call("moe_route_permute", L.ptr(idx), L.ptr(w.contiguous() if w is not None else None), T, k, E,
+           L.ptr(out["offsets"]), L.ptr(out["src_token"]), L.ptr(out["row_expert"]), L.ptr(out["row_weight"]),
+           L.ptr(out["token_pos"]), L.ptr(ws), wsb, _s())
+    return out
+
+
+def combine(y: torch.Tensor, token_pos: torch.Tensor, T: int, k: int, out_dtype=torch.bfloat16,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    y = _rowmajor(y, "y")
+    d = y.shape[1]
+    o = out if out is not None else torch.empty((T, d), dtype=out_dtype, device=y.device)
+    L.call("moe_combine", L.ptr(y), _dt(y), L.ptr(token_pos), T, k, d, L.ptr(o), _dt(o), _s())
+    return o
+
+
+def expert_histogram(idx: torch.Tensor, E: int, layer: int, counts: torch.Tensor,
+                     path_codes: torch.Tensor | None = None) -> None:
+    T, k = idx.shape
+    L.call("moe_expert_histogram", L.ptr(idx.contiguous()), T, k, E, layer, L.ptr(counts), L.ptr(path_codes), _s())
+
+
+# ── K7 / K8 ───────────────────────────────────────────────────────────────
+def hessian(x_tokens: torch.Tensor, smooth: torch.Tensor | None = None, damping_fraction: float = 0.01,
+            H: torch.Tensor | None = None, finalize: bool = True, nonzero: torch.Tensor | None = None):
+    """H = 2 xs^T xs (+ damping) from tokens-major x [T, n]."""
+    x = _rowmajor(x_tokens, "x")
+    T, n = x.shape
+    if H is None:
+        H = torch.zeros((n, n), dtype=torch.float64, device=x.device)
+    if nonzero is None:
+        nonzero = torch.zeros(1, dtype=torch.int64, device=x.device)
+    srec = reciprocal(smooth) if smooth is not None else None
+    L.call("moe_hessian_accum", L.ptr(x), _dt(x), T, n, x.stride(0), L.ptr(smooth), L.ptr(srec), L.ptr(H),
+           L.ptr(nonzero), _s())
+    if finalize:
+        L.call("moe_hessian_finalize", L.ptr(H), n, float(damping_fraction), L.ptr(nonzero), _s())
+    return H
+
+
+def gptq_columns(w: torch.Tensor, U: torch.Tensor, scale: torch.Tensor, zp: torch.Tensor, bits: int,
+                 order: torch.Tensor | None = None) -> torch.Tensor:
+    w = _rowmajor(w, "w")
+    R, n = w.shape
+    codes = torch.empty((R, n), dtype=torch.uint8, device=w.device)
+    lib = L.load()
+    wsb = lib.moe_gptq_workspace(R, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=w.device)
+    o32 = order.to(torch.int32).contiguous() if order is not None else None
+    L.call("moe_gptq_columns", L.ptr(w), R, n, w.stride(0), L.ptr(o32), L.ptr(U.contiguous()),
+           L.ptr(scale.contiguous()), L.ptr(zp.contiguous()), bits, L.ptr(codes), codes.stride(0), L.ptr(ws), wsb,
+           _s())
+    return codes

@@ -1,0 +1,270 @@
+"""GPU parity of each kernel against the CPU oracle on identical inputs.
+
+Bar (north star): INT8 codes, zero points, scales (float64), expert
+assignments, permutations and INT32 accumulators are BIT-EXACT; dequantised
+float outputs are within rtol 1e-5 (float32 epilogue vs float64 oracle on
+the same exact accumulators), well inside the stated 1e-3.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref as M
+from oracle import quant_ref as Q
+from paper_2508_07329_b200 import _lib as L
+from paper_2508_07329_b200 import ops
+
+from .conftest import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+RTOL_DEQ = 1e-5
+
+
+def _acts(rng, T, d, outlier_frac=0.01, scale=100.0):
+    x = rng.normal(size=(T, d)).astype(np.float32)
+    cols = rng.choice(d, max(1, int(d * outlier_frac)), replace=False)
+    x[:, cols] *= scale
+    return bf16_round(x)
+
+
+def _smooth(rng, G, d):
+    return np.exp(rng.normal(size=(G, d)) * 0.7)
+
+
+# ── K1 ───────────────────────────────────────────────────────────────────
+@pytest.mark.parametrize("T,d", [(64, 96), (257, 1024), (1024, 4096), (33, 14336)])
+def test_act_quant_per_token_bitexact(cuda, T, d):
+    rng = np.random.default_rng(T + d)
+    x = _acts(rng, T, d)
+    s = _smooth(rng, 1, d)
+    xd = torch.from_numpy(x).to(cuda).to(torch.bfloat16)
+    r = ops.act_quant(xd, smooth=torch.from_numpy(s).to(cuda))
+    codes, scale, zp, rs = M.quantize_rows(x.astype(np.float64), s[0])
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), scale)
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+    np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
+
+
+def test_act_quant_gather_grouped_bitexact(cuda):
+    rng = np.random.default_rng(5)
+    T, d, G = 300, 512, 8
+    x = _acts(rng, T, d)
+    s = _smooth(rng, G, d)
+    gather = rng.integers(0, T, size=2 * T).astype(np.int32)
+    group = rng.integers(0, G, size=2 * T).astype(np.int32)
+    r = ops.act_quant(torch.from_numpy(x).to(cuda).bfloat16(), smooth=torch.from_numpy(s).to(cuda),
+                      gather=torch.from_numpy(gather).to(cuda), row_group=torch.from_numpy(group).to(cuda))
+    codes, scale, zp, rs = M.quantize_rows_grouped(x.astype(np.float64)[gather], group, s)
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), scale)
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+    np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
+
+
+def test_act_quant_golden_k1(cuda, golden):
+    x = golden["k1_x_bf16"]
+    r = ops.act_quant(torch.from_numpy(x.astype(np.float32)).to(cuda).bfloat16(),
+                      smooth=torch.from_numpy(golden["k1_smooth"]).to(cuda))
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), golden["k1_codes"])
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), golden["k1_scales"])
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), golden["k1_zps"])
+
+
+def test_act_quant_edge_values(cuda):
+    # constant rows (scale floor), all-zero rows, exact ties at .5 of the grid,
+    # negative zero
+    x = np.zeros((6, 64))
+    x[1] = 5.0
+    x[2] = np.linspace(-1, 3, 64)
+    x[3, :] = -0.0
+    x[4] = np.arange(64) * 0.5 - 7.25
+    x[5] = np.r_[np.full(32, 0.49999999999999994), np.full(32, -0.5)]
+    for gran in ("per_token", "per_tensor"):
+        for bits in (2, 4, 8):
+            for sym in (False, True):
+                c = Q.cfg(bits, sym, gran)
+                r = ops.act_quant(torch.from_numpy(x).to(cuda), bits=bits, symmetric=sym, granularity=gran)
+                codes, sc, zp = Q.rtn(x, c)
+                np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+                np.testing.assert_array_equal(r["scale"].cpu().numpy(), sc)
+                np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+
+
+# ── K2 / K5 ──────────────────────────────────────────────────────────────
+def _rand_operand(rng, rows, K, zp_lo=0, zp_hi=255):
+    codes = rng.integers(0, 256, size=(rows, K)).astype(np.uint8)
+    zp = rng.integers(zp_lo, zp_hi + 1, size=rows).astype(np.int32)
+    scale = np.exp(rng.normal(size=rows) - 4)
+    return codes, zp, scale
+
+
+def _dev_operand(cuda, codes, zp, scale):
+    c = torch.from_numpy(codes).to(cuda)
+    sc = torch.from_numpy(scale).to(cuda)
+    return {"codes": c, "zp": torch.from_numpy(zp).to(cuda), "scale": sc, "scale_f32": sc.float(),
+            "rowsum": c.sum(dim=1, dtype=torch.int32)}
+
+
+@pytest.mark.parametrize("M_,N,K", [(300, 512, 512), (128, 256, 4096), (1000, 768, 272), (77, 40, 48),
+                                    (513, 1024, 14336)])
+def test_gemm_accumulators_bitexact(cuda, M_, N, K):
+    rng = np.random.default_rng(M_ * 7 + N + K)
+    a = _rand_operand(rng, M_, K)
+    w = _rand_operand(rng, N, K)
+    acc = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), epilogue=L.EPI_ACC_I32)
+    want = M.int_acc(a[0], a[1], w[0], w[1])
+    np.testing.assert_array_equal(acc.cpu().numpy().astype(np.int64), want)
+
+
+def test_gemm_extreme_zero_points(cuda):
+    # all-255 codes with zp 0 vs all-0 codes with zp 255: |acc| = K*255^2
+    K = 33024
+    a = (np.full((128, K), 255, np.uint8), np.zeros(128, np.int32), np.ones(128))
+    w = (np.zeros((256, K), np.uint8), np.full(256, 255, np.int32), np.ones(256))
+    acc = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), epilogue=L.EPI_ACC_I32)
+    assert (acc.cpu().numpy() == -K * 255 * 255).all()
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_gemm_dequant_epilogue(cuda, out_dtype):
+    rng = np.random.default_rng(11)
+    M_, N, K = 333, 512, 1024
+    a, w = _rand_operand(rng, M_, K), _rand_operand(rng, N, K)
+    bias = rng.normal(size=N).astype(np.float32)
+    y = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), out_dtype=out_dtype,
+                      bias=torch.from_numpy(bias).to(cuda))
+    want, _ = M.w8a8_linear(a[0], a[2], a[1], w[0], w[2], w[1], bias)
+    tol = RTOL_DEQ if out_dtype == torch.float32 else 2.0 ** -8
+    np.testing.assert_allclose(y.float().cpu().numpy(), want, rtol=tol, atol=tol * np.abs(want).max() * 1e-3)
+
+
+def test_grouped_gemm_ragged(cuda):
+    rng = np.random.default_rng(12)
+    E, N, K = 5, 256, 512
+    counts = np.array([0, 129, 1, 300, 77])
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    Mt = int(offs[-1])
+    a = _rand_operand(rng, Mt, K)
+    w = _rand_operand(rng, E * N, K)
+    rw = rng.random(Mt).astype(np.float32)
+    od = torch.from_numpy(offs).to(cuda)
+    acc = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), epilogue=L.EPI_ACC_I32,
+                        group_offsets=od, num_groups=E, n_per_group=N).cpu().numpy()
+    y = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), row_weight=torch.from_numpy(rw).to(cuda),
+                      group_offsets=od, num_groups=E, n_per_group=N).cpu().numpy()
+    for e in range(E):
+        lo, hi = offs[e], offs[e + 1]
+        if hi == lo:
+            continue
+        sl = slice(e * N, (e + 1) * N)
+        want_acc = M.int_acc(a[0][lo:hi], a[1][lo:hi], w[0][sl], w[1][sl])
+        np.testing.assert_array_equal(acc[lo:hi].astype(np.int64), want_acc)
+        want_y = (a[2][lo:hi, None] * w[2][None, sl]) * want_acc * rw[lo:hi, None]
+        np.testing.assert_allclose(y[lo:hi], want_y, rtol=RTOL_DEQ, atol=1e-12)
+
+
+def test_swiglu_epilogue(cuda):
+    rng = np.random.default_rng(13)
+    M_, F, K = 200, 384, 512
+    a = _rand_operand(rng, M_, K)
+    w = _rand_operand(rng, 2 * F, K)             # interleaved blocks of 128 (gate, up)
+    h = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), epilogue=L.EPI_SWIGLU,
+                      out_dtype=torch.float32).cpu().numpy()
+    y, _ = M.w8a8_linear(a[0], a[2], a[1], w[0], w[2], w[1])
+    blk = y.reshape(M_, F // 128, 2, 128)
+    want = (M.silu(blk[:, :, 0]) * blk[:, :, 1]).reshape(M_, F)
+    np.testing.assert_allclose(h, want, rtol=1e-4, atol=1e-6 * np.abs(want).max())
+
+
+# ── K3 / K4 / K6 ─────────────────────────────────────────────────────────
+@pytest.mark.parametrize("E,k", [(8, 2), (16, 4), (5, 1)])
+def test_router_gate_topk(cuda, E, k):
+    rng = np.random.default_rng(E * 10 + k)
+    T, d = 2048, 1024
+    x = _acts(rng, T, d, scale=3.0)
+    wg = (rng.normal(size=(E, d)) / np.sqrt(d)).astype(np.float32)
+    logits, idx, w = ops.router_gate(torch.from_numpy(x).to(cuda).bfloat16(), torch.from_numpy(wg).to(cuda), k)
+    lg = logits.cpu().numpy()
+    np.testing.assert_allclose(lg, x.astype(np.float64) @ wg.T.astype(np.float64), rtol=1e-4, atol=1e-4)
+    oidx, ow, _ = M.router_topk(lg, k)               # identical float32 logits
+    np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
+    np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-6)
+
+
+def test_router_topk_ties(cuda):
+    lg = np.array([[1, 1, 1, 1], [0, 2, 2, 0], [3, 3, 1, 3], [-1, -1, -1, -2]], dtype=np.float32)
+    idx, w = ops.router_topk(torch.from_numpy(lg).to(cuda), 2)
+    np.testing.assert_array_equal(idx.cpu().numpy(), [[0, 1], [1, 2], [0, 1], [0, 1]])
+    np.testing.assert_allclose(w.cpu().numpy(), 0.5, rtol=1e-7)
+
+
+@pytest.mark.parametrize("T,k,E", [(4096, 2, 8), (1, 2, 8), (5000, 4, 16), (777, 1, 3)])
+def test_route_permute(cuda, T, k, E):
+    rng = np.random.default_rng(T + k + E)
+    idx = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    w = rng.random((T, k)).astype(np.float32)
+    p = ops.route_permute(torch.from_numpy(idx).to(cuda), torch.from_numpy(w).to(cuda), E)
+    offs, tok, slot, pos = M.permute(idx, E)
+    np.testing.assert_array_equal(p["offsets"].cpu().numpy(), offs)
+    np.testing.assert_array_equal(p["src_token"].cpu().numpy(), tok)
+    np.testing.assert_array_equal(p["token_pos"].cpu().numpy(), pos.ravel())
+    np.testing.assert_array_equal(p["row_expert"].cpu().numpy(), idx[tok, slot])
+    np.testing.assert_array_equal(p["row_weight"].cpu().numpy(), w[tok, slot])
+
+
+def test_combine(cuda):
+    rng = np.random.default_rng(3)
+    T, k, d = 500, 2, 1024
+    y = rng.normal(size=(T * k, d)).astype(np.float32)
+    pos = rng.permutation(T * k).astype(np.int32)
+    out = ops.combine(torch.from_numpy(y).to(cuda), torch.from_numpy(pos).to(cuda), T, k,
+                      out_dtype=torch.float32).cpu().numpy()
+    want = y[pos.reshape(T, k)].sum(axis=1)
+    np.testing.assert_allclose(out, want, rtol=1e-6, atol=1e-6)
+
+
+def test_expert_histogram(cuda):
+    rng = np.random.default_rng(4)
+    T, k, E = 3000, 2, 8
+    idx = np.stack([np.sort(rng.permutation(E)[:k]) for _ in range(T)]).astype(np.int32)
+    counts = torch.zeros((2, E), dtype=torch.int64, device=cuda)
+    masks = torch.empty(T, dtype=torch.int32, device=cuda)
+    ops.expert_histogram(torch.from_numpy(idx).to(cuda), E, 1, counts, masks)
+    np.testing.assert_array_equal(counts.cpu().numpy()[1], np.bincount(idx.ravel(), minlength=E))
+    np.testing.assert_array_equal(masks.cpu().numpy(), (1 << idx).sum(axis=1))
+
+
+# ── K7 / K8 ──────────────────────────────────────────────────────────────
+def test_hessian_matches_oracle(cuda):
+    rng = np.random.default_rng(6)
+    n, T = 200, 333
+    x = rng.normal(size=(n, T))
+    x[3] *= 40
+    s = np.exp(rng.normal(size=n) * 0.5)
+    H = ops.hessian(torch.from_numpy((x / s[:, None]).T.copy()).to(cuda)).cpu().numpy()
+    np.testing.assert_allclose(H, Q.build_hessian(x / s[:, None]), rtol=1e-12, atol=1e-9)
+    Hs = ops.hessian(torch.from_numpy(x.T.copy()).to(cuda), smooth=torch.from_numpy(s).to(cuda)).cpu().numpy()
+    np.testing.assert_allclose(Hs, Q.build_hessian(x / s[:, None]), rtol=1e-12, atol=1e-9)
+    assert np.array_equal(Hs, Hs.T)
+
+
+@pytest.mark.parametrize("R,n,bits,permute", [(10, 24, 4, False), (130, 256, 8, True), (64, 300, 3, False)])
+def test_gptq_columns_bitexact_given_u(cuda, R, n, bits, permute):
+    rng = np.random.default_rng(R + n)
+    x = rng.normal(size=(n, 4 * n // 3 + 8))
+    w = rng.normal(size=(R, n))
+    h = Q.build_hessian(x)
+    order = rng.permutation(n) if permute else np.arange(n)
+    U = Q.inverse_upper_factor(h[np.ix_(order, order)])
+    c = Q.cfg(bits)
+    sc, zp = Q.affine(w.min(axis=1), w.max(axis=1), c)
+    want_p = Q.gptq_columns(w[:, order], U, sc, zp, (1 << bits) - 1)
+    want = np.empty_like(want_p)
+    want[:, order] = want_p
+    got = ops.gptq_columns(torch.from_numpy(w).to(cuda), torch.from_numpy(U).to(cuda),
+                           torch.from_numpy(sc).to(cuda), torch.from_numpy(zp).to(cuda), bits,
+                           torch.from_numpy(order).to(cuda) if permute else None)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)

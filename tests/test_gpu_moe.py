@@ -1,0 +1,129 @@
+"""GPU: the full MoE layer forward, checked stage by stage against the oracle
+on the GPU's own inputs (identical bytes), at the C2 toy-MoE configuration
+(d=1024, 8 experts, top-2, 4096 tokens, ffn=3584) and a small C4-shape
+slice; plus W8A8Linear (C1 / C3 shapes)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref as M
+from paper_2508_07329_b200 import _lib as L
+from paper_2508_07329_b200.linear import W8A8Linear
+from paper_2508_07329_b200.moe import MoELayer
+
+from .conftest import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+
+def _x(rng, T, d):
+    x = rng.normal(size=(T, d)).astype(np.float32)
+    x[:, rng.choice(d, max(1, d // 100), replace=False)] *= 100.0
+    return bf16_round(x)
+
+
+def _stagewise(cuda, T, d, F, E=8, k=2, seed=0):
+    layer = MoELayer.random(E, d, F, top_k=k, seed=seed + 1, out_dtype=torch.float32)
+    rng = np.random.default_rng(seed)
+    x = _x(rng, T, d)
+    xd = torch.from_numpy(x).to(cuda).bfloat16()
+    out, aux = layer.forward(xd, out_dtype=torch.float32, return_aux=True)
+    lg = aux["logits"].cpu().numpy()
+    # router on identical logits
+    oidx, ow, _ = M.router_topk(lg, k)
+    np.testing.assert_array_equal(aux["idx"].cpu().numpy(), oidx)
+    np.testing.assert_allclose(aux["w"].cpu().numpy(), ow, rtol=1e-6)
+    # permutation
+    offs, tok, slot, pos = M.permute(oidx, E)
+    p = aux["perm"]
+    np.testing.assert_array_equal(p["offsets"].cpu().numpy(), offs)
+    np.testing.assert_array_equal(p["src_token"].cpu().numpy(), tok)
+    rexp = oidx[tok, slot]
+    experts = [layer.expert_host(e) for e in range(E)]
+    s13 = np.stack([e["s13"] for e in experts])
+    s2 = np.stack([e["s2"] for e in experts])
+    # K1 on x (gather + per-expert smoothing): bit-exact
+    c1, sc1, z1, rs1 = M.quantize_rows_grouped(x.astype(np.float64)[tok], rexp, s13)
+    np.testing.assert_array_equal(aux["a1"]["codes"].cpu().numpy(), c1)
+    np.testing.assert_array_equal(aux["a1"]["scale"].cpu().numpy(), sc1)
+    np.testing.assert_array_equal(aux["a1"]["zp"].cpu().numpy(), z1)
+    # GEMM1 + SwiGLU vs exact accumulators (h stored bf16: 1 bf16 ulp)
+    h = aux["h"].float().cpu().numpy()
+    h_codes = aux["a2"]["codes"].cpu().numpy()
+    y = aux["y"].cpu().numpy()
+    for e in range(E):
+        lo, hi = offs[e], offs[e + 1]
+        if hi == lo:
+            continue
+        ex = experts[e]
+        g, _ = M.w8a8_linear(c1[lo:hi], sc1[lo:hi], z1[lo:hi], ex["w1_codes"], ex["w1_scale"], ex["w1_zp"])
+        u, _ = M.w8a8_linear(c1[lo:hi], sc1[lo:hi], z1[lo:hi], ex["w3_codes"], ex["w3_scale"], ex["w3_zp"])
+        hw = M.silu(g) * u
+        np.testing.assert_allclose(h[lo:hi], hw, rtol=2.0 ** -7, atol=1e-3 * np.abs(hw).max())
+    # K1 on the GPU's own h: bit-exact
+    c2, sc2, z2, _ = M.quantize_rows_grouped(h.astype(np.float64), rexp, s2)
+    np.testing.assert_array_equal(h_codes, c2)
+    np.testing.assert_array_equal(aux["a2"]["scale"].cpu().numpy(), sc2)
+    # GEMM2 (dequant * routing weight) vs exact accumulators
+    rw = ow[tok, slot]
+    for e in range(E):
+        lo, hi = offs[e], offs[e + 1]
+        if hi == lo:
+            continue
+        ex = experts[e]
+        yw, _ = M.w8a8_linear(c2[lo:hi], sc2[lo:hi], z2[lo:hi], ex["w2_codes"], ex["w2_scale"], ex["w2_zp"])
+        yw = yw * rw[lo:hi, None]
+        np.testing.assert_allclose(y[lo:hi], yw, rtol=1e-5, atol=1e-6 * np.abs(yw).max())
+    # combine
+    np.testing.assert_allclose(out.cpu().numpy(), y[pos].sum(axis=1), rtol=1e-6, atol=1e-7)
+    return layer, x, out
+
+
+def test_moe_c2_stagewise(cuda):
+    _stagewise(cuda, T=4096, d=1024, F=3584)
+
+
+def test_moe_mixtral_shape_slice_stagewise(cuda):
+    _stagewise(cuda, T=512, d=4096, F=14336, seed=3)
+
+
+def test_moe_end_to_end_vs_oracle(cuda):
+    """Whole-layer output vs the float64 oracle run from x alone (routing on
+    the GPU's logits); differences come only from bf16 storage of h
+    flipping rare codes, so the check is normwise."""
+    layer = MoELayer.random(8, 1024, 1024, seed=5, out_dtype=torch.float32)
+    rng = np.random.default_rng(9)
+    x = _x(rng, 1024, 1024)
+    out, aux = layer.forward(torch.from_numpy(x).to(cuda).bfloat16(), out_dtype=torch.float32, return_aux=True)
+    ref, _, _ = M.moe_forward(x.astype(np.float64), None, [layer.expert_host(e) for e in range(8)],
+                              logits=aux["logits"].cpu().numpy())
+    o = out.cpu().numpy()
+    assert np.linalg.norm(o - ref) / np.linalg.norm(ref) < 1e-2
+
+
+def test_moe_bf16_output_matches_f32(cuda):
+    layer = MoELayer.random(8, 512, 1024, seed=2)
+    x = torch.from_numpy(_x(np.random.default_rng(1), 700, 512)).to(cuda).bfloat16()
+    a = layer.forward(x, out_dtype=torch.float32)
+    b = layer.forward(x)
+    assert b.dtype == torch.bfloat16
+    torch.testing.assert_close(b.float(), a, rtol=2e-2, atol=2e-2 * a.abs().max().item())
+
+
+@pytest.mark.parametrize("T,din,dout", [(512, 256, 1024), (8192, 4096, 16384)])
+def test_w8a8_linear(cuda, T, din, dout):
+    rng = np.random.default_rng(din)
+    w = torch.randn(dout, din, device=cuda) * 0.02
+    s = np.exp(rng.normal(size=din) * 0.5)
+    bias = rng.normal(size=dout).astype(np.float32)
+    lin = W8A8Linear.from_rtn(w, smooth=s, bias=bias, out_dtype=torch.float32)
+    x = _x(rng, T, din)
+    y = lin(torch.from_numpy(x).to(cuda).bfloat16()).cpu().numpy()
+    xq = lin.quantize_input(torch.from_numpy(x).to(cuda).bfloat16())
+    cx, sx, zx, _ = M.quantize_rows(x.astype(np.float64), s)
+    np.testing.assert_array_equal(xq["codes"].cpu().numpy(), cx)
+    want, _ = M.w8a8_linear(cx, sx, zx, lin.w["codes"].cpu().numpy(), lin.w["scale"].cpu().numpy(),
+                            lin.w["zp"].cpu().numpy(), bias)
+    np.testing.assert_allclose(y, want, rtol=1e-5, atol=1e-5 * np.abs(want).max())
+    assert L.EPI_DEQUANT == 0
