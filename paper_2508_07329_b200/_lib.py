@@ -128,7 +128,12 @@ def call(name: str, *args, what: str | None = None):
     lib = load()
     st = getattr(lib, name)(*args)
     check(st, what or name)
+    if _SYNC:
+        import torch
+        try:
+            torch.cuda.synchronize()
+        except RuntimeError as exc:
+            raise RuntimeError(f"{name}: device error after launch: {exc}") from None
 
 
-def debug_sync() -> bool:
-    return os.environ.get("MOE_B200_SYNC", "0") == "1"
+_SYNC = os.environ.get("MOE_B200_SYNC", "0") == "1"   # debug: synchronize after every entry point

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int
   const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
   const int64_t hi = min(n, lo + kPermChunk);
   for (int64_t base = lo; base < hi; base += kPermThreads) {
-    for (int i = threadIdx.x; i < (kPermThreads / 32) * E; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < (kPermThreads / 32) * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
     __syncthreads();
     const int64_t i = base + threadIdx.x;
     const bool valid = i < hi;

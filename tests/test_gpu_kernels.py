@@ -191,7 +191,7 @@ def test_router_gate_topk(cuda, E, k):
     np.testing.assert_allclose(lg, x.astype(np.float64) @ wg.T.astype(np.float64), rtol=1e-4, atol=1e-4)
     oidx, ow, _ = M.router_topk(lg, k)               # identical float32 logits
     np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
-    np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-6)
+    np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-5, atol=1e-9)  # float32 expf
 
 
 def test_router_topk_ties(cuda):

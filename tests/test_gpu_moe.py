@@ -33,7 +33,7 @@ def _stagewise(cuda, T, d, F, E=8, k=2, seed=0):
     # router on identical logits
     oidx, ow, _ = M.router_topk(lg, k)
     np.testing.assert_array_equal(aux["idx"].cpu().numpy(), oidx)
-    np.testing.assert_allclose(aux["w"].cpu().numpy(), ow, rtol=1e-6)
+    np.testing.assert_allclose(aux["w"].cpu().numpy(), ow, rtol=1e-5, atol=1e-9)  # float32 expf
     # permutation
     offs, tok, slot, pos = M.permute(oidx, E)
     p = aux["perm"]
