@@ -78,7 +78,10 @@ moe_status moe_device_check(int dev);
  * with table row row_group[r] (or 0) of `smooth` [G, cols] (with its
  * correctly-rounded reciprocal table `smooth_recip`, used for an exact
  * reciprocal-and-correct division; NULL -> plain IEEE division), then
- * quantizes with float64 semantics bit-identical to the reference:
+ * quantizes with float64 semantics bit-identical to the reference. For bf16
+ * input with per-row groups, `smooth_recip_f32` (RN32 of smooth_recip)
+ * enables the float32-filtered kernel (exact float64 only where the float32
+ * error interval could change the result; identical output):
  * scale = max((max-min)/qmax, 1e-12), zp = clip(rha(-min/scale)),
  * code = clip(rha(xs/scale)+zp), rha(v) = sign(v)*floor(|v|+0.5).
  * per_token / per_output_row: one group per output row. per_tensor: one
@@ -90,13 +93,15 @@ moe_status moe_device_check(int dev);
 int64_t moe_act_quant_workspace(int64_t rows, int64_t cols, int granularity);
 moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
                          const int32_t* gather_rows, const double* smooth, const double* smooth_recip,
-                         int smooth_mode, const int32_t* row_group, int bits, int symmetric,
+                         const float* smooth_recip_f32, int smooth_mode, const int32_t* row_group,
+                         int bits, int symmetric,
                          int granularity, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                          int32_t* zp, int32_t* rowsum, void* workspace, int64_t workspace_bytes,
                          moe_stream_t stream);
 
-/* out[i] = RN(1 / s[i]) (float64); feeds smooth_recip. */
-moe_status moe_reciprocal_f64(const double* s, int64_t n, double* out, moe_stream_t stream);
+/* out[i] = RN(1 / s[i]) (float64) and optionally out_f32[i] = RN32(out[i]);
+ * feed smooth_recip / smooth_recip_f32. */
+moe_status moe_reciprocal_f64(const double* s, int64_t n, double* out, float* out_f32, moe_stream_t stream);
 
 /* dequantize (quant.py:234-240): out = (code - zp) * scale, float64. */
 moe_status moe_dequantize(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ldc,

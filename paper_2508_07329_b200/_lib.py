@@ -30,9 +30,9 @@ _SIGS = {
     "moe_launch_count": (C.c_uint64, []),
     "moe_device_check": (_I, [_I]),
     "moe_act_quant_workspace": (_I64, [_I64, _I64, _I]),
-    "moe_act_quant": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _I, _P, _I, _I, _I, _P, _I64, _P, _P, _P,
-                           _P, _P, _I64, _P]),
-    "moe_reciprocal_f64": (_I, [_P, _I64, _P, _P]),
+    "moe_act_quant": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _I64, _P, _P,
+                           _P, _P, _P, _I64, _P]),
+    "moe_reciprocal_f64": (_I, [_P, _I64, _P, _P, _P]),
     "moe_dequantize": (_I, [_P, _I64, _I64, _I64, _P, _P, _I, _P, _P]),
     "moe_apply_smoothing": (_I, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "moe_channel_stats": (_I, [_P, _I64, _I64, _I, _P, _P]),

@@ -1,0 +1,90 @@
+// Shared pieces of the K1 (smoothing + RTN) kernels: row addressing with
+// gather / per-row smoothing groups and block-level reductions.
+#pragma once
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace moe {
+
+struct SmoothArgs {
+  const double* s;    // [G, cols] smoothing factors
+  const double* rs;   // [G, cols] RN(1/s) (optional)
+  int mode;           // MOE_SMOOTH_*
+  int64_t cols;
+};
+
+struct RowArgs {
+  const void* x;
+  int dt;
+  int64_t rows, cols, ldx;
+  const int32_t* gather;  // output row -> input row (optional)
+  const int32_t* group;   // output row -> smoothing table row (optional)
+  SmoothArgs sm;
+};
+
+struct RowView {
+  int64_t off;    // element offset of the source row
+  int64_t gbase;  // element offset of the smoothing table row
+};
+
+__device__ __forceinline__ RowView row_view(const RowArgs& a, int64_t r) {
+  const int64_t src = a.gather ? (int64_t)a.gather[r] : r;
+  const int64_t g = a.group ? (int64_t)a.group[r] : 0;
+  return RowView{src * a.ldx, g * a.sm.cols};
+}
+
+// x (already float64) smoothed exactly as apply_smoothing does (quant.py:324):
+// RN(x / s) for activations, RN(w * s) for weights.
+__device__ __forceinline__ double smooth_value(double x, const SmoothArgs& sa, int64_t gbase, int64_t j) {
+  if (sa.mode == MOE_SMOOTH_DIVIDE) {
+    const double s = sa.s[gbase + j];
+    return sa.rs ? div_rcp(x, s, sa.rs[gbase + j]) : __ddiv_rn(x, s);
+  }
+  if (sa.mode == MOE_SMOOTH_MULTIPLY) return __dmul_rn(x, sa.s[gbase + j]);
+  return x;
+}
+
+// Block reductions (any blockDim multiple of 32, <= 1024). All threads get
+// the result. `sh` needs blockDim/32 slots.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, T* sh, Op op) {
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  T t = sh[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) t = op(t, sh[i]);
+  return t;
+}
+
+struct OpMin {
+  __device__ double operator()(double a, double b) const { return fmin(a, b); }
+  __device__ float operator()(float a, float b) const { return fminf(a, b); }
+};
+struct OpMax {
+  __device__ double operator()(double a, double b) const { return fmax(a, b); }
+  __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
+};
+struct OpAdd {
+  __device__ int64_t operator()(int64_t a, int64_t b) const { return a + b; }
+};
+
+// order-preserving int64 key of a double (atomic min/max of doubles)
+__device__ __forceinline__ long long dkey(double d) {
+  const long long i = __double_as_longlong(d);
+  return i >= 0 ? i : (i ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+__device__ __forceinline__ double dunkey(long long k) {
+  return __longlong_as_double(k >= 0 ? k : (k ^ 0x7FFFFFFFFFFFFFFFLL));
+}
+
+// Host launcher of the TMA-staged bf16 fast path (act_quant_fast.cu).
+// Returns false when the shape is outside its envelope.
+bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sym, uint8_t* codes, int64_t ldc,
+                           double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum, cudaStream_t s,
+                           cudaError_t* err);
+
+}  // namespace moe

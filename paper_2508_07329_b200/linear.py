@@ -26,12 +26,14 @@ class W8A8Linear:
         self.out_features, self.in_features = self.w["codes"].shape
         self.smooth = None
         self.smooth_recip = None
+        self.smooth_recip_f32 = None
         if smooth is not None:
             s = torch.as_tensor(np.asarray(smooth.cpu() if isinstance(smooth, torch.Tensor) else smooth),
                                 dtype=torch.float64).reshape(1, -1).cuda()
             if s.shape[1] != self.in_features:
                 raise ValueError(f"expected {self.in_features} smoothing factors, got {s.shape[1]}")
-            self.smooth, self.smooth_recip = s, ops.reciprocal(s)
+            self.smooth = s
+            self.smooth_recip, self.smooth_recip_f32 = ops.reciprocal(s, with_f32=True)
         self.bias = None if bias is None else torch.as_tensor(bias, dtype=torch.float32).reshape(-1).cuda()
         self.act_bits, self.act_symmetric, self.out_dtype = act_bits, act_symmetric, out_dtype
 
@@ -56,7 +58,8 @@ class W8A8Linear:
         return cls(qm, smooth, bias, bits, False, out_dtype)
 
     def quantize_input(self, x: torch.Tensor) -> dict:
-        return ops.act_quant(x, smooth=self.smooth, smooth_recip=self.smooth_recip, bits=self.act_bits,
+        return ops.act_quant(x, smooth=self.smooth, smooth_recip=self.smooth_recip,
+                             smooth_recip_f32=self.smooth_recip_f32, bits=self.act_bits,
                              symmetric=self.act_symmetric, granularity=PER_TOKEN)
 
     def forward(self, x: torch.Tensor, out_dtype=None) -> torch.Tensor:

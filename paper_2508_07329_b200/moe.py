@@ -74,7 +74,8 @@ class MoELayer:
                                 for e in experts]).cuda().contiguous()
         self.s2 = torch.stack([torch.as_tensor(np.asarray(_np(e["s2"])), dtype=torch.float64)
                                for e in experts]).cuda().contiguous()
-        self.s13_recip, self.s2_recip = ops.reciprocal(self.s13), ops.reciprocal(self.s2)
+        self.s13_recip, self.s13_recip32 = ops.reciprocal(self.s13, with_f32=True)
+        self.s2_recip, self.s2_recip32 = ops.reciprocal(self.s2, with_f32=True)
         self.out_dtype = out_dtype
         self.host_experts = experts
 
@@ -136,13 +137,15 @@ class MoELayer:
             stats.record(idx)
         perm = ops.route_permute(idx, w, self.E)
         mark("permute")
-        a1 = ops.act_quant(x, smooth=self.s13, smooth_recip=self.s13_recip, row_group=perm["row_expert"],
+        a1 = ops.act_quant(x, smooth=self.s13, smooth_recip=self.s13_recip, smooth_recip_f32=self.s13_recip32,
+                           row_group=perm["row_expert"],
                            gather=perm["src_token"], rows=T * self.k)
         mark("quant_x")
         h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F)
         mark("gemm13_swiglu")
-        a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, row_group=perm["row_expert"])
+        a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
+                           row_group=perm["row_expert"])
         mark("quant_h")
         y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)

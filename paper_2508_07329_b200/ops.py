@@ -41,14 +41,17 @@ def _s():
 
 
 # ── K1 ────────────────────────────────────────────────────────────────────
-def reciprocal(s: torch.Tensor) -> torch.Tensor:
+def reciprocal(s: torch.Tensor, with_f32: bool = False):
+    """RN(1/s) in float64 (and its RN32 copy when with_f32)."""
     s = _cuda(s, "s").contiguous().to(torch.float64)
     out = torch.empty_like(s)
-    L.call("moe_reciprocal_f64", L.ptr(s), s.numel(), L.ptr(out), _s())
-    return out
+    out32 = torch.empty(s.shape, dtype=torch.float32, device=s.device) if with_f32 else None
+    L.call("moe_reciprocal_f64", L.ptr(s), s.numel(), L.ptr(out), L.ptr(out32), _s())
+    return (out, out32) if with_f32 else out
 
 
 def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_recip: torch.Tensor | None = None,
+              smooth_recip_f32: torch.Tensor | None = None,
               smooth_mode: int = L.SMOOTH_DIVIDE, row_group: torch.Tensor | None = None,
               gather: torch.Tensor | None = None, rows: int | None = None, bits: int = 8,
               symmetric: bool = False, granularity: str = "per_token", rowsum: bool = True,
@@ -74,9 +77,11 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
         if smooth.dtype != torch.float64:
             raise ValueError("smoothing table must be float64")
         if smooth_recip is None and mode == L.SMOOTH_DIVIDE:
-            smooth_recip = reciprocal(smooth)
+            smooth_recip, smooth_recip_f32 = reciprocal(smooth, with_f32=True)
+    div = mode == L.SMOOTH_DIVIDE
     L.call("moe_act_quant", L.ptr(x), _dt(x), n_rows, cols, x.stride(0), L.ptr(gather), L.ptr(smooth),
-           L.ptr(smooth_recip) if mode == L.SMOOTH_DIVIDE else None, mode, L.ptr(row_group), bits,
+           L.ptr(smooth_recip) if div else None, L.ptr(smooth_recip_f32) if div else None, mode,
+           L.ptr(row_group), bits,
            int(bool(symmetric)), gran, L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp),
            L.ptr(rs), L.ptr(ws), wsb, _s())
     return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,

@@ -73,6 +73,30 @@ def test_act_quant_golden_k1(cuda, golden):
     np.testing.assert_array_equal(r["zp"].cpu().numpy(), golden["k1_zps"])
 
 
+def test_act_quant_bf16_fast_path_ties(cuda):
+    """bf16 rows whose quotients land exactly on k + 0.5 (and next to it), plus
+    all-positive rows far from zero (clip saturation) — the cases where the
+    float32 filter must defer to the exact float64 path."""
+    rows = []
+    k = np.arange(0, 128)
+    rows.append(np.r_[0.0, 255 / 8, (k + 0.5) / 8, np.zeros(6)])   # scale = 1/8 exactly -> ties
+    rows.append(-np.r_[0.0, 255 / 8, (k + 0.5) / 8, np.zeros(6)])
+    rows.append(100.0 + np.arange(136) / 64)                         # all positive, zp = 0, clipped
+    rows.append(np.r_[np.full(68, 3.0), np.full(68, -1.0)])
+    rng = np.random.default_rng(0)
+    rows.append(rng.normal(size=136) * 1e-30)                        # tiny values
+    rows.append(rng.normal(size=136) * 3e4)
+    x = bf16_round(np.array(rows, dtype=np.float32))
+    for s in (None, np.ones((1, 136)), np.exp(rng.normal(size=(1, 136)))):
+        r = ops.act_quant(torch.from_numpy(x).to(cuda).bfloat16(),
+                          smooth=None if s is None else torch.from_numpy(s).to(cuda))
+        codes, sc, zp, rs = M.quantize_rows(x.astype(np.float64), None if s is None else s[0])
+        np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+        np.testing.assert_array_equal(r["scale"].cpu().numpy(), sc)
+        np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+        np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
+
+
 def test_act_quant_edge_values(cuda):
     # constant rows (scale floor), all-zero rows, exact ties at .5 of the grid,
     # negative zero
