@@ -40,8 +40,8 @@ WORKLOAD = "C4: Mixtral-8x7B-shape single MoE layer (8 experts, top-2, d=4096, f
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU per step")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-tokens", type=int, default=256, help="tokens per CPU-baseline step")
@@ -61,36 +61,51 @@ def synth_tokens(T: int, d: int, seed: int) -> np.ndarray:
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler (100 ms) started before the warm-up; stop(t0, t1)
+    keeps the samples whose timestamps fall inside the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device_index: int):
-        self.dev = device_index
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={device_index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.5)
         except OSError:
             self.p = None
 
-    def stop(self) -> dict:
+    def stop(self, t_start: float, t_end: float) -> dict:
+        import datetime
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         rows = [r.split(", ") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
         os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        good = []
+        for r in rows:
+            if len(r) < 10:
+                continue
+            try:
+                ts = datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                float(r[2])
+            except ValueError:
+                continue
+            good.append((ts, r))
+        inside = [r for ts, r in good if t_start - 0.05 <= ts <= t_end + 0.05]
+        use = inside or [r for _, r in good]
+        sm = [float(r[2]) for r in use]
+        mx = [float(r[3]) for r in use]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({n for r in rows if len(r) >= 9 for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        reasons = sorted({n for r in use for n, v in zip(names, r[6:10]) if v.strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples_in_timed_region": len(inside), "samples_total": len(good)}
 
 
 class StageTimer:
@@ -208,12 +223,13 @@ def main() -> None:
             dist.barrier()
 
     # ---- device-resident timing --------------------------------------------
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         layer.forward(x_dev)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(local)
+    wall0 = time.time()
     timer = StageTimer()
     launches0 = lib.moe_launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -224,9 +240,10 @@ def main() -> None:
     t1.record()
     torch.cuda.synchronize()
     launches = lib.moe_launch_count() - launches0
+    wall1 = time.time()
     barrier()
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop(wall0, wall1)
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
@@ -251,8 +268,18 @@ def main() -> None:
             tt = torch.tensor([e2e_ms], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
+        # diagnostic: raw pinned copy rates of the same buffers (not part of the metric)
+        c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        c0.record()
+        x_dev.copy_(x_host, non_blocking=True)
+        c1.record()
+        out_host.copy_(x_dev, non_blocking=True)
+        c2.record()
+        torch.cuda.synchronize()
+        nbytes = T * D * 2
         e2e = {"value": T * world / (e2e_ms / 1000.0), "unit": "tokens/s",
-               "h2d_bytes_per_step": T * D * 2, "d2h_bytes_per_step": T * D * 2, "ms_per_step": e2e_ms}
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms,
+               "h2d_gbs_raw": nbytes / c0.elapsed_time(c1) / 1e6, "d2h_gbs_raw": nbytes / c1.elapsed_time(c2) / 1e6}
 
     # ---- roofline of the dominant kernel (grouped W8A8 GEMMs) --------------
     peaks = measured_peaks()

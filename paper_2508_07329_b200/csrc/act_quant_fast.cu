@@ -56,9 +56,40 @@ __device__ __forceinline__ void smooth8(const uint4& u, const float* __restrict_
   if (tab) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c);
     const float4 b = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c + 1);
-    xs[0] *= a.x; xs[1] *= a.y; xs[2] *= a.z; xs[3] *= a.w;
-    xs[4] *= b.x; xs[5] *= b.y; xs[6] *= b.z; xs[7] *= b.w;
+    float2 p;
+    p = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(a.x, a.y)); xs[0] = p.x; xs[1] = p.y;
+    p = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(a.z, a.w)); xs[2] = p.x; xs[3] = p.y;
+    p = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(b.x, b.y)); xs[4] = p.x; xs[5] = p.y;
+    p = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(b.z, b.w)); xs[6] = p.x; xs[7] = p.y;
   }
+}
+
+// ── packed 8-bit encode (sm_100 FFMA2/FADD2 + I2IP saturating pack) ───────
+// For |v| < 2^21: t = v + 1.5*2^23 rounds v to the nearest integer in its
+// low mantissa bits (exact: rr = t - 1.5*2^23, d = v - rr). The element is
+// "safe" when |d| + eb(v) < 0.5, i.e. the exact float64 quotient rounds to
+// the same integer (round-half-away only differs from round-to-nearest-even
+// at .5, which is never safe). code = clamp(R + zp, 0, 255) via I2IP.
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+
+__device__ __forceinline__ uint32_t pack_sat_u8(int lo, int hi, uint32_t rest) {
+  uint32_t d;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(hi), "r"(lo), "r"(rest));
+  return d;
+}
+
+// 2 elements: returns codes (as ints, unclamped) and accumulates "unsafe".
+__device__ __forceinline__ void enc2(float2 xs, float2 rsc2, int zpm, int& c0, int& c1, bool& unsafe) {
+  const float2 v = __fmul2_rn(xs, rsc2);
+  const float2 t = __fadd2_rn(v, make_float2(kMagic, kMagic));
+  const float2 rr = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+  const float2 d = __fadd2_rn(v, make_float2(-rr.x, -rr.y));
+  const float2 s = __ffma2_rn(make_float2(fabsf(v.x), fabsf(v.y)), make_float2(kRelErr, kRelErr),
+                              __fadd2_rn(make_float2(fabsf(d.x), fabsf(d.y)), make_float2(kAbsErr, kAbsErr)));
+  unsafe |= (s.x >= 0.5f) | (s.y >= 0.5f);
+  c0 = __float_as_int(t.x) + zpm;
+  c1 = __float_as_int(t.y) + zpm;
 }
 
 // ── rare float64 paths, out of line ───────────────────────────────────────
@@ -214,6 +245,26 @@ __global__ void __launch_bounds__(W * G * 32, 1)
     // pass C: encode (float32 decision; float64 out of line near a boundary)
     int sum = 0;
     uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+    const bool packed_ok = bits == 8 && !exact_all && fmax(fabs(mn), fabs(mx)) * p.rscale < 2097152.0;
+    if (packed_ok) {
+      const float2 rsc2 = make_float2(rsc32, rsc32);
+      const int zpm = p.zp - kMagicBits;
+#pragma unroll 2
+      for (int64_t c = glane; c < nvec; c += 32 * W) {
+        float xs[8];
+        smooth8(xr[c], tab, c, xs);
+        int q[8];
+        bool unsafe = false;
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) enc2(make_float2(xs[e], xs[e + 1]), rsc2, zpm, q[e], q[e + 1], unsafe);
+        uint2 out = make_uint2(pack_sat_u8(q[0], q[1], pack_sat_u8(q[2], q[3], 0u)),
+                               pack_sat_u8(q[4], q[5], pack_sat_u8(q[6], q[7], 0u)));
+        sum = (int)__dp4a(out.x, 0x01010101u, (unsigned)sum);
+        sum = (int)__dp4a(out.y, 0x01010101u, (unsigned)sum);
+        if (unsafe) out = exact_encode8(xr[c], srow, rrow, c, 0xFFu, out, ExactParams{p.scale, p.rscale, p.zp, qmax}, &sum);
+        __stcs(dst + c, out);
+      }
+    } else
 #pragma unroll 2
     for (int64_t c = glane; c < nvec; c += 32 * W) {
       float xs[8];

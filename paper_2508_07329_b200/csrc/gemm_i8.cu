@@ -29,7 +29,7 @@ constexpr int kBM = 128;          // UMMA M
 constexpr int kBK = 128;          // bytes of K per stage = one SW128 atom row
 constexpr int kUmmaK = 32;        // K per tcgen05.mma for 8-bit inputs
 constexpr int kMaxGroups = 64;
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
 
 struct GemmArgs {
   int M, N, K, G;
@@ -76,7 +76,7 @@ __device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start
   return TileInfo{g, off[g] + m_tile * kBM, off[g + 1], n_tile * BN};
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 template <bool BF16>
 __device__ __forceinline__ void store32(void* out, int64_t idx, const float (&v)[32], int nvalid, bool vec) {
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 256);
     }
     fence_mbar_init();
   }
@@ -226,7 +226,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ===== epilogue =====
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;  // which half of the tile columns
     uint32_t tile_it = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_it) {
       const TileInfo ti = map_tile(t, p.G, tile_start, off, n_tiles, BN);
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (EPI == MOE_EPI_SWIGLU) {
         // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
 #pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
+        for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
           uint32_t vg[32], vu[32];
           tmem_ld32(tbase + c * 32, vg);
           tmem_ld32(tbase + BN / 2 + c * 32, vu);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
           uint32_t v[32];
           tmem_ld32(tbase + c * 32, v);
           tmem_ld_wait();
