@@ -168,27 +168,31 @@ class MoELayer:
         if out_host is None:
             out_host = torch.empty((T, self.d), dtype=self.out_dtype, pin_memory=True)
         cur = torch.cuda.current_stream()
-        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        # persistent copy streams and device staging buffer: per-call streams
+        # would defeat the caching allocator (fresh cudaMalloc = device sync)
+        if getattr(self, "_io", None) is None or self._io["xbuf"].shape[0] < T:
+            self._io = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+                        "xbuf": torch.empty((T, self.d), dtype=x_host.dtype, device="cuda")}
+        h2d, d2h, xbuf = self._io["h2d"], self._io["d2h"], self._io["xbuf"]
+        h2d.wait_stream(cur)      # previous users of xbuf on the compute stream are done
         bounds = [(s, min(T, s + chunk_tokens)) for s in range(0, T, chunk_tokens)]
-        xs, ys, loaded, done = [], [], [], []
-        for lo, hi in bounds:
-            with torch.cuda.stream(h2d):
-                xs.append(x_host[lo:hi].to("cuda", non_blocking=True))
+        loaded = []
+        with torch.cuda.stream(h2d):
+            for lo, hi in bounds:
+                xbuf[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 loaded.append(ev)
         for i, (lo, hi) in enumerate(bounds):
             cur.wait_event(loaded[i])
-            ys.append(self.forward(xs[i]))
+            y = self.forward(xbuf[lo:hi])
             ev = torch.cuda.Event()
             ev.record(cur)
-            done.append(ev)
+            d2h.wait_event(ev)
             with torch.cuda.stream(d2h):
-                d2h.wait_event(ev)
-                out_host[lo:hi].copy_(ys[i], non_blocking=True)
+                out_host[lo:hi].copy_(y, non_blocking=True)
+            y.record_stream(d2h)
         d2h.synchronize()
-        for t in xs + ys:
-            t.record_stream(cur)
         return out_host
 
     # ------------------------------------------------------------------
