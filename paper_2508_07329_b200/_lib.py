@@ -31,13 +31,13 @@ _SIGS = {
     "moe_device_check": (_I, [_I]),
     "moe_act_quant_workspace": (_I64, [_I64, _I64, _I]),
     "moe_act_quant": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _I64, _P, _P,
-                           _P, _P, _P, _I64, _P]),
+                           _P, _P, _P, _P, _I64, _P]),
     "moe_reciprocal_f64": (_I, [_P, _I64, _P, _P, _P]),
     "moe_dequantize": (_I, [_P, _I64, _I64, _I64, _P, _P, _I, _P, _P]),
     "moe_apply_smoothing": (_I, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "moe_channel_stats": (_I, [_P, _I64, _I64, _I, _P, _P]),
     "moe_w8a8_gemm": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I,
-                           _P, _I, _I64, _P, _I64, _P]),
+                           _P, _I, _I64, _P, _I64, _P, _I64, _P, _P]),
     "moe_quant_sq_error": (_I, [_P, _I64, _I64, _P, _I, _P, _P, _P, _P, _I64, _P]),
     "moe_quant_sq_error_workspace": (_I64, [_I64, _I64]),
     "moe_router_gate": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),

@@ -1,14 +1,15 @@
 // K1 hot path — bf16 rows, smoothing division, per-token RTN, bit-identical
 // to the float64 reference semantics (quant.py:191-231, 314-324).
 //
-// Data movement (B200): a row is owned by a group of W warps (W = 1 for
-// d = 4096, W = 4 for ffn = 14336). Each group streams its contiguous range
-// of rows through a 2-stage shared-memory ring filled by 1-D bulk TMA copies
-// (cp.async.bulk + mbarrier complete_tx): the next row is in flight while the
-// current one is processed, without occupying registers. Rows are gathered
-// through the MoE permutation straight from x. The float32 reciprocal table
-// of the row's expert is read through L1 (a group's consecutive rows share
-// an expert). HBM traffic = one read of x + one write of the codes.
+// Layout: one warp per row, 16 warps per CTA, rows gathered through the MoE
+// permutation straight from x. A row is streamed up to three times — float32
+// extremes (pass A, skipped when the producing GEMM epilogue already
+// supplied them), exact float64 extremes over the few candidates (pass B),
+// encode (pass C) — with 4 x 16-byte loads per lane in flight; the re-reads
+// hit L1/L2 (a warp's row is 8-28 KB), so HBM sees one read of x and one
+// write of the codes. No shared-memory staging and no block barriers: the
+// reductions are warp shuffles. The float32 reciprocal table of the row's
+// expert is read through L1 (a CTA's rows share an expert).
 //
 // Arithmetic: every element is first evaluated in float32 from correctly
 // rounded reciprocals; the float32 value is within |v32| * 2^-21 of the
@@ -28,18 +29,10 @@ namespace moe {
 
 constexpr float kRelErr = 4.76837158203125e-07f;    // 2^-21
 constexpr float kAbsErr = 7.174648137343064e-43f;   // 2^-140
-constexpr int kStages = 2;
-constexpr int64_t kSmemBudget = 220 * 1024;
+constexpr int kWarpsPerCta = 16;
+constexpr int kBatch = 4;                           // 16-byte vectors in flight per lane
 
 __device__ __forceinline__ float err_bound(float v) { return fmaf(fabsf(v), kRelErr, kAbsErr); }
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -79,7 +72,6 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int lo, int hi, uint32_t rest) {
   return d;
 }
 
-// 2 elements: returns codes (as ints, unclamped) and accumulates "unsafe".
 __device__ __forceinline__ void enc2(float2 xs, float2 rsc2, int zpm, int& c0, int& c1, bool& unsafe) {
   const float2 v = __fmul2_rn(xs, rsc2);
   const float2 t = __fadd2_rn(v, make_float2(kMagic, kMagic));
@@ -113,164 +105,63 @@ struct ExactParams {
 };
 
 __device__ __noinline__ uint2 exact_encode8(uint4 u, const double* srow, const double* rrow, int64_t c, uint32_t mask,
-                                            uint2 packed, ExactParams p, int* dsum) {
+                                            uint2 packed, ExactParams p) {
   float f[8];
   unpack8(u, f);
   uint32_t w[2] = {packed.x, packed.y};
-  int delta = 0;
   for (int e = 0; e < 8; ++e) {
     if (!(mask >> e & 1u)) continue;
     const double xd = srow ? div_rcp((double)f[e], srow[c * 8 + e], rrow[c * 8 + e]) : (double)f[e];
     const uint32_t code = (uint32_t)encode_code(xd, p.scale, p.rscale, p.zp, p.qmax);
     const int sh = 8 * (e & 3);
-    delta += (int)code - (int)((w[e >> 2] >> sh) & 0xFFu);
     w[e >> 2] = (w[e >> 2] & ~(0xFFu << sh)) | (code << sh);
   }
-  *dsum += delta;
   return make_uint2(w[0], w[1]);
 }
 
-// Reduction across the W warps of a row group: warp shuffle, then smem +
-// named barrier (id 1 + group) when W > 1.
-template <int W, typename T, typename Op>
-__device__ __forceinline__ T group_reduce(T v, T* slots, int gid, int wig, Op op) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if constexpr (W > 1) {
-    if ((threadIdx.x & 31) == 0) slots[gid * W + wig] = v;
-    named_bar_sync(1 + gid, W * 32);
-    T t = slots[gid * W];
-#pragma unroll
-    for (int i = 1; i < W; ++i) t = op(t, slots[gid * W + i]);
-    named_bar_sync(1 + gid, W * 32);
-    return t;
-  } else {
-    return v;
-  }
+__device__ __forceinline__ int bytesum(uint2 v) {
+  return (int)__dp4a(v.y, 0x01010101u, __dp4a(v.x, 0x01010101u, 0u));
 }
 
-struct IntAdd {
-  __device__ int operator()(int a, int b) const { return a + b; }
-};
+// Encoder of one row once its exact extremes (hence scale / zero point) are
+// known: 8 elements per call, packed f32x2 path for 8-bit codes when the
+// row's quotients stay below 2^21, general float32 path otherwise; either
+// way elements whose float32 interval straddles a rounding boundary are
+// re-encoded exactly (out of line).
+struct RowEncoder {
+  double scale, rscale;
+  int zp, qmax;
+  float rsc32, big;
+  int zpm;
+  bool packed, exact_all;
 
-template <int W, int G>
-__global__ void __launch_bounds__(W * G * 32, 1)
-    act_quant_fast_kernel(RowArgs a, const float* __restrict__ rs32_tab, int bits, int sym, uint8_t* codes,
-                          int64_t ldc, double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum,
-                          int64_t rows_per_group) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ float sf[G * W];
-  __shared__ double sd[G * W];
-  __shared__ int si[G * W];
-  __shared__ __align__(8) uint64_t bars[G][kStages];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = warp / W, wig = warp % W;   // row group, warp in group
-  const int glane = wig * 32 + lane;          // lane within the row group
-  const int64_t cols = a.cols, nvec = cols / 8;
-  const uint32_t row_bytes = (uint32_t)(cols * 2);
-  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
-  const int qmax = (1 << bits) - 1;
-  uint4* ring = reinterpret_cast<uint4*>(sm) + (int64_t)gid * kStages * nvec;
-  const int64_t r_lo = ((int64_t)blockIdx.x * G + gid) * rows_per_group;
-  const int64_t r_hi = min(a.rows, r_lo + rows_per_group);
-  const bool leader = glane == 0;
-
-  auto issue = [&](int64_t r, int st) {
-    const int64_t src = a.gather ? (int64_t)a.gather[r] : r;
-    mbar_expect_tx(&bars[gid][st], row_bytes);
-    bulk_g2s(ring + st * nvec, static_cast<const __nv_bfloat16*>(a.x) + src * a.ldx, row_bytes, &bars[gid][st]);
-  };
-  if (leader) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&bars[gid][st], 1);
-    fence_mbar_init();
-    for (int st = 0; st < kStages && r_lo + st < r_hi; ++st) issue(r_lo + st, st);
+  __device__ __forceinline__ RowEncoder(const AffineParams& p, double mn, double mx, int bits, bool exact)
+      : scale(p.scale), rscale(p.rscale), zp(p.zp), qmax((1 << bits) - 1) {
+    rsc32 = __double2float_rn(p.rscale);
+    big = (float)(qmax + zp + 2) * 1.001f;
+    zpm = zp - kMagicBits;
+    exact_all = exact;
+    packed = bits == 8 && !exact && fmax(fabs(mn), fabs(mx)) * p.rscale < 2097152.0;
   }
-  __syncthreads();
-  if (r_lo >= r_hi) return;
 
-  for (int64_t r = r_lo, it = 0; r < r_hi; ++r, ++it) {
-    const int st = (int)(it & 1);
-    const RowView rv = row_view(a, r);
-    const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
-    const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
-    const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
-    mbar_wait(&bars[gid][st], (uint32_t)((it >> 1) & 1));
-    const uint4* xr = ring + st * nvec;
-
-    // pass A: float32 extremes of the smoothed row
-    float tmax = -FLT_MAX, tmin = FLT_MAX;
-#pragma unroll 2
-    for (int64_t c = glane; c < nvec; c += 32 * W) {
-      float xs[8];
-      smooth8(xr[c], tab, c, xs);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        tmax = fmaxf(tmax, xs[e]);
-        tmin = fminf(tmin, xs[e]);
-      }
-    }
-    const float M = group_reduce<W>(tmax, sf, gid, wig, OpMax());
-    const float m = group_reduce<W>(tmin, sf, gid, wig, OpMin());
-    const bool exact_all = !(isfinite(M) && isfinite(m));
-    const float lb_max = M - err_bound(M);   // the exact max is >= this
-    const float ub_min = m + err_bound(m);   // the exact min is <= this
-
-    // pass B: exact float64 extremes over the elements that can reach them
-    double mn = DBL_MAX, mx = -DBL_MAX;
-    const bool scan_max = exact_all || tmax + err_bound(tmax) >= lb_max;
-    const bool scan_min = exact_all || tmin - err_bound(tmin) <= ub_min;
-    if (scan_max || scan_min) {
-      for (int64_t c = glane; c < nvec; c += 32 * W) {
-        float xs[8];
-        smooth8(xr[c], tab, c, xs);
-        uint32_t mmax = 0, mmin = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          mmax |= (uint32_t)(scan_max && (exact_all || xs[e] + err_bound(xs[e]) >= lb_max)) << e;
-          mmin |= (uint32_t)(scan_min && (exact_all || xs[e] - err_bound(xs[e]) <= ub_min)) << e;
-        }
-        if (mmax | mmin) {
-          const double2 ext = exact_extremes8(xr[c], srow, rrow, c, mmax, mmin);
-          mn = fmin(mn, ext.x);
-          mx = fmax(mx, ext.y);
-        }
-      }
-    }
-    mn = group_reduce<W>(mn, sd, gid, wig, OpMin());
-    mx = group_reduce<W>(mx, sd, gid, wig, OpMax());
-    const AffineParams p = affine_params(mn, mx, bits, sym);
-    const float rsc32 = __double2float_rn(p.rscale);
-    const float big = (float)(qmax + p.zp + 2) * 1.001f;
-
-    // pass C: encode (float32 decision; float64 out of line near a boundary)
-    int sum = 0;
-    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
-    const bool packed_ok = bits == 8 && !exact_all && fmax(fabs(mn), fabs(mx)) * p.rscale < 2097152.0;
-    if (packed_ok) {
+  __device__ __forceinline__ uint2 encode8(const uint4& u, const float* tab, int64_t c, const double* srow,
+                                           const double* rrow, int& sum) const {
+    float xs[8];
+    smooth8(u, tab, c, xs);
+    uint2 out;
+    uint32_t redo = 0;
+    if (packed) {
       const float2 rsc2 = make_float2(rsc32, rsc32);
-      const int zpm = p.zp - kMagicBits;
-#pragma unroll 2
-      for (int64_t c = glane; c < nvec; c += 32 * W) {
-        float xs[8];
-        smooth8(xr[c], tab, c, xs);
-        int q[8];
-        bool unsafe = false;
+      int q[8];
+      bool unsafe = false;
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) enc2(make_float2(xs[e], xs[e + 1]), rsc2, zpm, q[e], q[e + 1], unsafe);
-        uint2 out = make_uint2(pack_sat_u8(q[0], q[1], pack_sat_u8(q[2], q[3], 0u)),
-                               pack_sat_u8(q[4], q[5], pack_sat_u8(q[6], q[7], 0u)));
-        sum = (int)__dp4a(out.x, 0x01010101u, (unsigned)sum);
-        sum = (int)__dp4a(out.y, 0x01010101u, (unsigned)sum);
-        if (unsafe) out = exact_encode8(xr[c], srow, rrow, c, 0xFFu, out, ExactParams{p.scale, p.rscale, p.zp, qmax}, &sum);
-        __stcs(dst + c, out);
-      }
-    } else
-#pragma unroll 2
-    for (int64_t c = glane; c < nvec; c += 32 * W) {
-      float xs[8];
-      smooth8(xr[c], tab, c, xs);
-      uint32_t packed[2] = {0u, 0u};
-      uint32_t redo = 0;
+      for (int e = 0; e < 8; e += 2) enc2(make_float2(xs[e], xs[e + 1]), rsc2, zpm, q[e], q[e + 1], unsafe);
+      out = make_uint2(pack_sat_u8(q[0], q[1], pack_sat_u8(q[2], q[3], 0u)),
+                       pack_sat_u8(q[4], q[5], pack_sat_u8(q[6], q[7], 0u)));
+      sum += bytesum(out);
+      redo = unsafe ? 0xFFu : 0u;
+    } else {
+      uint32_t packedw[2] = {0u, 0u};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float v32 = xs[e] * rsc32;
@@ -278,73 +169,166 @@ __global__ void __launch_bounds__(W * G * 32, 1)
         const float rr = rintf(av);
         const bool safe = 0.5f - fabsf(av - rr) > err_bound(av);
         const int R = (int)rr;
-        int code = min(max((v32 < 0.f ? -R : R) + p.zp, 0), qmax);
+        int code = min(max((v32 < 0.f ? -R : R) + zp, 0), qmax);
         if (!safe) code = v32 < 0.f ? 0 : qmax;   // exact whenever av > big
         redo |= (uint32_t)(exact_all || (!safe && !(av > big))) << e;
         sum += code;
-        packed[e >> 2] |= (uint32_t)code << (8 * (e & 3));
+        packedw[e >> 2] |= (uint32_t)code << (8 * (e & 3));
       }
-      uint2 out = make_uint2(packed[0], packed[1]);
-      if (redo) out = exact_encode8(xr[c], srow, rrow, c, redo, out, ExactParams{p.scale, p.rscale, p.zp, qmax}, &sum);
-      __stcs(dst + c, out);
+      out = make_uint2(packedw[0], packedw[1]);
     }
-    if (rowsum) sum = group_reduce<W>(sum, si, gid, wig, IntAdd());
-    if (leader) {
+    if (redo) {
+      const uint2 fixed = exact_encode8(u, srow, rrow, c, redo, out, ExactParams{scale, rscale, zp, qmax});
+      sum += bytesum(fixed) - bytesum(out);
+      out = fixed;
+    }
+    return out;
+  }
+};
+
+// order-preserving int32 key of a float (atomic min/max of floats)
+__device__ __forceinline__ float funkey(int k) { return __int_as_float(k >= 0 ? k : (k ^ 0x7FFFFFFF)); }
+
+template <typename F>
+__device__ __forceinline__ void for_row_batches(const uint4* src, int64_t nvec, int lane, F&& body) {
+  for (int64_t c0 = lane; c0 < nvec; c0 += 32 * kBatch) {
+    uint4 u[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int64_t c = c0 + 32 * b;
+      u[b] = c < nvec ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int64_t c = c0 + 32 * b;
+      if (c < nvec) body(u[b], c);
+    }
+  }
+}
+
+template <bool GIVEN>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+    act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const int* __restrict__ bounds, int bits,
+                          int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                          int32_t* rowsum, int64_t rows_per_cta) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t nvec = a.cols / 8;
+  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
+  // each CTA owns a contiguous range of rows (shared expert tables in L1)
+  const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
+  for (int64_t r = r_lo + warp; r < r_hi; r += kWarpsPerCta) {
+    const RowView rv = row_view(a, r);
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x) + rv.off);
+    const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
+    const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
+    const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
+
+    // pass A: float32 extremes (given by the producing epilogue, or computed)
+    float M, m;
+    if (GIVEN) {
+      m = funkey(bounds[2 * r]);
+      M = funkey(bounds[2 * r + 1]);
+    } else {
+      float tmax = -FLT_MAX, tmin = FLT_MAX;
+      for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+        float xs[8];
+        smooth8(u, tab, c, xs);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          tmax = fmaxf(tmax, xs[e]);
+          tmin = fminf(tmin, xs[e]);
+        }
+      });
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+      }
+      M = tmax;
+      m = tmin;
+    }
+    const bool exact_all = !(isfinite(M) && isfinite(m));
+    const float lb_max = exact_all ? -FLT_MAX : M - err_bound(M);   // the exact max is >= this
+    const float ub_min = exact_all ? FLT_MAX : m + err_bound(m);    // the exact min is <= this
+
+    // pass B: exact float64 extremes over the elements that can reach them
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+      float xs[8];
+      smooth8(u, tab, c, xs);
+      uint32_t mmax = 0, mmin = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        mmax |= (uint32_t)(xs[e] + err_bound(xs[e]) >= lb_max) << e;
+        mmin |= (uint32_t)(xs[e] - err_bound(xs[e]) <= ub_min) << e;
+      }
+      if (mmax | mmin) {
+        const double2 ext = exact_extremes8(u, srow, rrow, c, mmax, mmin);
+        mn = fmin(mn, ext.x);
+        mx = fmax(mx, ext.y);
+      }
+    });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const AffineParams p = affine_params(mn, mx, bits, sym);
+    const RowEncoder enc(p, mn, mx, bits, exact_all);
+
+    // pass C: encode
+    int sum = 0;
+    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+    for_row_batches(src, nvec, lane,
+                    [&](const uint4& u, int64_t c) { __stcs(dst + c, enc.encode8(u, tab, c, srow, rrow, sum)); });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
       if (rowsum) rowsum[r] = sum;
       scale[r] = p.scale;
       if (scale_f32) scale_f32[r] = (float)p.scale;
       zp[r] = p.zp;
     }
-    // refill this stage with row r + 2 once every lane of the group is done with it
-    if constexpr (W > 1) named_bar_sync(1 + gid, W * 32);
-    else __syncwarp();
-    if (leader && r + kStages < r_hi) {
-      fence_proxy_async_smem();
-      issue(r + kStages, st);
-    }
   }
 }
 
-template <int W, int G>
-static cudaError_t launch_wg(const RowArgs& a, const float* rs32, int bits, int sym, uint8_t* codes, int64_t ldc,
-                             double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum, cudaStream_t s) {
-  const int64_t smem = (int64_t)G * kStages * a.cols * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(act_quant_fast_kernel<W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmemBudget);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  // persistent: one CTA per SM; every row group walks a contiguous row range
-  const int64_t groups = std::min<int64_t>(a.rows, (int64_t)num_sms() * G);
-  const int64_t rows_per_group = (a.rows + groups - 1) / groups;
-  const int64_t used = (a.rows + rows_per_group - 1) / rows_per_group;
-  const int64_t blocks = (used + G - 1) / G;
-  act_quant_fast_kernel<W, G><<<(unsigned)blocks, W * G * 32, (size_t)smem, s>>>(
-      a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_group);
+static bool eligible(const RowArgs& a, const float* rs32, uint8_t* codes, int64_t ldc) {
+  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
+  return a.dt == MOE_DT_BF16 && a.cols % 8 == 0 && a.ldx % 8 == 0 && ldc % 8 == 0 &&
+         (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (reinterpret_cast<uintptr_t>(codes) & 7) == 0 &&
+         (a.sm.mode == MOE_SMOOTH_NONE || (smooth && a.sm.rs && rs32));
+}
+
+template <bool GIVEN>
+static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const int* bounds, int bits, int sym,
+                              uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                              int32_t* rowsum, cudaStream_t s) {
+  // contiguous row ranges, ~4 CTAs (64 warps) per SM
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + kWarpsPerCta - 1) / kWarpsPerCta,
+                                                              4 * (int64_t)num_sms()));
+  const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
+  const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
+  act_quant_warp_kernel<GIVEN><<<(unsigned)nblk, kWarpsPerCta * 32, 0, s>>>(
+      a, rs32, bounds, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
   count_launch();
   return cudaGetLastError();
+}
+
+bool launch_act_quant_given(const RowArgs& a, const float* rs32, const int* bounds, int bits, int sym,
+                            uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                            int32_t* rowsum, cudaStream_t s, cudaError_t* err) {
+  if (!bounds || !eligible(a, rs32, codes, ldc)) return false;
+  *err = launch_warp<true>(a, rs32, bounds, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+  return true;
 }
 
 bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sym, uint8_t* codes, int64_t ldc,
                            double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum, cudaStream_t s,
                            cudaError_t* err) {
-  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
-  const int64_t row_bytes = a.cols * 2;
-  if (a.dt != MOE_DT_BF16 || a.cols % 8 || a.ldx % 8 || ldc % 8 ||
-      (reinterpret_cast<uintptr_t>(a.x) & 15) || (reinterpret_cast<uintptr_t>(codes) & 7) ||
-      !(a.sm.mode == MOE_SMOOTH_NONE || (smooth && a.sm.rs && rs32)))
-    return false;
-  // W warps per row (>= ~28 vectors per lane keeps the loop efficient),
-  // G row groups per CTA so that G * 2 stages of rows fit in shared memory.
-  auto fits = [&](int G) { return (int64_t)G * kStages * row_bytes <= kSmemBudget; };
-  if (row_bytes <= 4096 && fits(16)) *err = launch_wg<1, 16>(a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  else if (row_bytes <= 12 * 1024 && fits(8)) *err = launch_wg<1, 8>(a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  else if (fits(4)) *err = launch_wg<4, 4>(a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  else if (fits(2)) *err = launch_wg<8, 2>(a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  else if (fits(1)) *err = launch_wg<16, 1>(a, rs32, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  else return false;
+  if (!eligible(a, rs32, codes, ldc)) return false;
+  *err = launch_warp<false>(a, rs32, nullptr, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   return true;
 }
 

@@ -8,26 +8,32 @@
 //   acc = sum a*w  - zw*rowsum_a - za*(rowsum_w - K*zw)    (wrapping int32,
 //   exact because the true value satisfies |acc| <= K*255^2 < 2^31).
 //
-// Structure (one CTA per SM, persistent, warp-specialised):
-//   warp 0 lane 0 : TMA producer  — A tile 128x128 B, W tile BNx128 B per
-//                   stage, 128-byte swizzle, mbarrier complete_tx
-//   warp 1 lane 0 : UMMA issuer   — tcgen05.mma.cta_group::1.kind::i8,
-//                   M=128 N=BN K=32, accumulator in TMEM (2 stages x BN cols)
+// Structure (persistent, warp-specialised, 384 threads per CTA):
+//   warp 0 lane 0 : TMA producer — A tile 128 x 128 B, W tile (256/CG) x 128 B
+//                   per stage, 128-byte swizzle, mbarrier complete_tx
+//   warp 1 lane 0 : UMMA issuer — tcgen05.mma.kind::i8, N=256 K=32, int32
+//                   accumulators in TMEM (2 x 256 columns, double-buffered)
 //   warp 2        : TMEM allocator
-//   warps 4..7    : epilogue      — tcgen05.ld 32x32b, zero-point
-//                   correction, dequant / SwiGLU / raw int32, global stores
+//   warps 4..11   : epilogue — tcgen05.ld 32x32b, zero-point correction,
+//                   dequant / SwiGLU / raw int32, global stores
+// CG = 2 (the MoE hot path): a CTA pair on one TPC computes a 256 x 256 tile
+// with tcgen05.mma.cta_group::2 issued by the leader; each CTA stages its own
+// 128 A rows and half of the W tile, so per-SM shared-memory traffic per MMA
+// drops from 12 KB to 8 KB and the W tile crosses L2 once per pair.
 // Grouped mode (MoE): the tile scheduler walks experts from the device-side
 // offsets, so routing never syncs with the host.
-#include "common.cuh"
+#include <algorithm>
+
+#include "k1_common.cuh"
 #include "ptx.cuh"
 
 #include <cudaTypedefs.h>
 
 namespace moe {
 
-constexpr int kBM = 128;          // UMMA M
-constexpr int kBK = 128;          // bytes of K per stage = one SW128 atom row
-constexpr int kUmmaK = 32;        // K per tcgen05.mma for 8-bit inputs
+constexpr int kBM = 128;           // rows per CTA (UMMA M per CTA)
+constexpr int kBK = 128;           // bytes of K per stage = one SW128 atom row
+constexpr int kUmmaK = 32;         // K per tcgen05.mma for 8-bit inputs
 constexpr int kMaxGroups = 64;
 constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
 
@@ -47,12 +53,16 @@ struct GemmArgs {
   int32_t* acc_out;
   int64_t ld_acc;
   int vec_ok;  // output pointer / ldo allow 16-byte vector stores
+  // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
+  const float* ns_rs32;
+  int64_t ns_ld;
+  int* row_bounds;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 struct Smem {
   static constexpr int kA = kBM * kBK;
-  static constexpr int kB = BN * kBK;
+  static constexpr int kB = (BN / CG) * kBK;
   static constexpr int kStage = kA + kB;
   static constexpr int kBarOff = STAGES * kStage;
   static constexpr int kNumBars = 2 * STAGES + 4;
@@ -65,15 +75,15 @@ struct TileInfo {
   int g, m0, m_end, n0;
 };
 
-__device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start, const int* off, int n_tiles,
-                                             int BN) {
+// tile t -> (group, first row, group end, first column); tiles of TM rows,
+// m fastest within an N block so a group's weight block is reused in L2.
+__device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start, const int* off, int TM, int BN) {
   int g = 0;
   while (g + 1 < G && t >= tile_start[g + 1]) ++g;
   const int local = t - tile_start[g];
-  const int mt = (off[g + 1] - off[g] + kBM - 1) / kBM;
+  const int mt = (off[g + 1] - off[g] + TM - 1) / TM;
   const int n_tile = local / mt, m_tile = local - n_tile * mt;
-  (void)n_tiles;
-  return TileInfo{g, off[g] + m_tile * kBM, off[g + 1], n_tile * BN};
+  return TileInfo{g, off[g] + m_tile * TM, off[g + 1], n_tile * BN};
 }
 
 __device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
@@ -110,6 +120,35 @@ __device__ __forceinline__ void store32(void* out, int64_t idx, const float (&v)
   }
 }
 
+// ── float32 per-row bounds of the stored outputs * RN32(1/s_next) ─────────
+// Feeds the next K1 (act_quant row_bounds): the same float32 products K1
+// forms, reduced to a per-thread (min, max) and merged per row with one
+// order-preserving int32 atomic each per tile. Exactness stays in K1.
+__device__ __forceinline__ int fkey(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : (i ^ 0x7FFFFFFF);
+}
+
+__device__ __forceinline__ void chunk_bounds(const float (&hv)[32], const float* __restrict__ t32, float& m,
+                                             float& M) {
+  const float4* t = reinterpret_cast<const float4*>(t32);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 tt = __ldg(t + q);
+    const float2 a = __fmul2_rn(make_float2(hv[4 * q], hv[4 * q + 1]), make_float2(tt.x, tt.y));
+    const float2 b = __fmul2_rn(make_float2(hv[4 * q + 2], hv[4 * q + 3]), make_float2(tt.z, tt.w));
+    M = fmaxf(fmaxf(M, a.x), fmaxf(a.y, fmaxf(b.x, b.y)));
+    m = fminf(fminf(m, a.x), fminf(a.y, fminf(b.x, b.y)));
+  }
+}
+
+__global__ void rowbounds_init_kernel(int* rb, int64_t M) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+    rb[2 * i] = 0x7FFFFFFF;
+    rb[2 * i + 1] = (int)0x80000000;
+  }
+}
+
 // zero-point corrected exact accumulator (wrapping int32 arithmetic)
 __device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t rsw, int32_t za, int32_t rsa,
                                               int32_t K) {
@@ -117,12 +156,94 @@ __device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t 
   return (int32_t)(acc - (uint32_t)zw * (uint32_t)rsa - (uint32_t)za * t);
 }
 
-template <int BN, int STAGES, int EPI, bool BF16>
+// Epilogue of one tile for one thread: TMEM lane quarter q, column half
+// `half` (8 epilogue warps split the 256 columns), output row `row`.
+template <int BN, int EPI, bool BF16>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase,
+                                              int half, float& bmn, float& bmx) {
+  const bool rvalid = row < ti.m_end;
+  float sa = 0.f, rw = 1.f;
+  int32_t za = 0, rsa = 0;
+  if (rvalid) {
+    za = p.a_zp[row];
+    rsa = p.a_rowsum[row];
+    if (EPI != MOE_EPI_ACC_I32) {
+      sa = p.a_scale[row];
+      if (p.row_weight) rw = p.row_weight[row];
+    }
+  }
+  const int wbase = ti.g * p.N;
+  if (EPI == MOE_EPI_SWIGLU) {
+    // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
+#pragma unroll 1
+    for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
+      uint32_t vg[32], vu[32];
+      tmem_ld32(tbase + c * 32, vg);
+      tmem_ld32(tbase + BN / 2 + c * 32, vu);
+      tmem_ld_wait();
+      float h[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int ng = wbase + ti.n0 + c * 32 + j;
+        const int nu = ng + BN / 2;
+        const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
+        const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
+        float g = (float)ag * (sa * p.w_scale[ng]);
+        float u = (float)au * (sa * p.w_scale[nu]);
+        if (p.bias) {
+          g += p.bias[ng];
+          u += p.bias[nu];
+        }
+        h[j] = silu_f(g) * u * rw;
+        if (BF16) h[j] = __bfloat162float(__float2bfloat16_rn(h[j]));   // the value K1 will read
+      }
+      if (rvalid) {
+        store32<BF16>(p.out, (int64_t)row * p.ldo + ti.n0 / 2 + c * 32, h, 32, p.vec_ok);
+        if (p.row_bounds) chunk_bounds(h, p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + c * 32, bmn, bmx);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      uint32_t v[32];
+      tmem_ld32(tbase + c * 32, v);
+      tmem_ld_wait();
+      const int n_lo = ti.n0 + c * 32;
+      int nvalid = p.N - n_lo;
+      nvalid = nvalid > 32 ? 32 : nvalid;
+      if (!rvalid || nvalid <= 0) continue;
+      if (EPI == MOE_EPI_ACC_I32) {
+        int32_t* o = p.acc_out + (int64_t)row * p.ld_acc + n_lo;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < nvalid) {
+            const int n = wbase + n_lo + j;
+            o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+          }
+        }
+      } else {
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
+          const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+          float val = (float)a * (sa * p.w_scale[n]);
+          if (p.bias) val += p.bias[n];
+          y[j] = val * rw;
+        }
+        store32<BF16>(p.out, (int64_t)row * p.ldo + n_lo, y, nvalid, p.vec_ok);
+      }
+    }
+  }
+}
+
+template <int BN, int STAGES, int EPI, bool BF16, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
-  using L = Smem<BN, STAGES>;
+  using L = Smem<BN, STAGES, CG>;
+  constexpr int TM = kBM * CG;  // tile rows (a CTA pair shares one 256-row tile)
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte alignment for the 128B-swizzled TMA / UMMA tiles
+  // 1024-byte alignment for the 128B-swizzled TMA / UMMA tiles (same offset in both CTAs of a pair)
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -137,6 +258,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (p.N + BN - 1) / BN;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = (int)blockIdx.x / CG;         // scheduling unit: a CTA or a CTA pair
+  const int n_units = (int)gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     if (p.offsets) {
@@ -148,16 +273,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     for (int g = 0; g < p.G; ++g) {
       tile_start[g] = acc;
-      acc += ((off[g + 1] - off[g] + kBM - 1) / kBM) * n_tiles;
+      acc += ((off[g + 1] - off[g] + TM - 1) / TM) * n_tiles;
     }
     tile_start[p.G] = acc;
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CG);        // leader: its own expect_tx arrive + the peer's arrive
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 256);
+      mbar_init(&tempty[s], 256 * CG);  // all epilogue threads of the pair (leader's copy)
     }
     fence_mbar_init();
   }
@@ -166,41 +291,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     prefetch_tmap(&tmB);
   }
   if (warp == 2) {
-    tmem_alloc(tmem_ptr, 2 * BN);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_pair(tmem_ptr, 2 * BN);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_ptr, 2 * BN);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
   const int total_tiles = tile_start[p.G];
 
   if (warp == 0 && lane == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs of a pair load their own halves) =====
     const uint64_t pol_a = policy_evict_last();
     const uint64_t pol_b = policy_evict_last();
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileInfo ti = map_tile(t, p.G, tile_start, off, n_tiles, BN);
-      const int wrow = ti.g * p.N + ti.n0;
+    for (int t = unit; t < total_tiles; t += n_units) {
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN);
+      const int arow = ti.m0 + (int)rank * kBM;
+      const int wrow = ti.g * p.N + ti.n0 + (int)rank * (BN / CG);
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* sa = smem + s * L::kStage;
         uint8_t* sb = sa + L::kA;
-        mbar_expect_tx(&full[s], L::kStage);
-        tma_load_2d(sa, &tmA, &full[s], kb * kBK, ti.m0, pol_a);
-        tma_load_2d(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+        if (CG == 2) {
+          if (leader) mbar_expect_tx(&full[s], 2 * L::kStage);
+          tma_load_2d_pair(sa, &tmA, &full[s], kb * kBK, arow, pol_a);
+          tma_load_2d_pair(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+          if (!leader) mbar_arrive_leader(&full[s]);
+        } else {
+          mbar_expect_tx(&full[s], L::kStage);
+          tma_load_2d(sa, &tmA, &full[s], kb * kBK, arow, pol_a);
+          tma_load_2d(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+        }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ===== UMMA issuer =====
-    constexpr uint32_t idesc = idesc_i8(kBM, BN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===== UMMA issuer (the leader issues for the whole pair) =====
+    constexpr uint32_t idesc = idesc_i8(TM, BN);
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0, tile_it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_it) {
+    for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
       mbar_wait(&tempty[as], aph ^ 1);
       tc_fence_after();
@@ -217,104 +356,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int k = 0; k < kBK / kUmmaK; ++k) {
           // advance the start address by k*32 bytes inside the swizzle atom
-          umma_i8(d_tmem, adesc + (uint64_t)(k * kUmmaK / 16), bdesc + (uint64_t)(k * kUmmaK / 16), idesc,
-                  (kb | k) != 0);
+          const uint64_t da = adesc + (uint64_t)(k * kUmmaK / 16), db = bdesc + (uint64_t)(k * kUmmaK / 16);
+          if (CG == 2) umma_i8_pair(d_tmem, da, db, idesc, (kb | k) != 0);
+          else umma_i8(d_tmem, da, db, idesc, (kb | k) != 0);
         }
-        umma_commit(&empty[s]);
+        if (CG == 2) umma_commit_pair(&empty[s]);
+        else umma_commit(&empty[s]);
       }
-      umma_commit(&tfull[as]);
+      if (CG == 2) umma_commit_pair(&tfull[as]);
+      else umma_commit(&tfull[as]);
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
-    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int half = (warp - 4) >> 2;  // which half of the tile columns
     uint32_t tile_it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_it) {
-      const TileInfo ti = map_tile(t, p.G, tile_start, off, n_tiles, BN);
+    for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN);
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
-      const int row = ti.m0 + q * 32 + lane;
-      const bool rvalid = row < ti.m_end;
-      float sa = 0.f, rw = 1.f;
-      int32_t za = 0, rsa = 0;
-      if (rvalid) {
-        za = p.a_zp[row];
-        rsa = p.a_rowsum[row];
-        if (EPI != MOE_EPI_ACC_I32) {
-          sa = p.a_scale[row];
-          if (p.row_weight) rw = p.row_weight[row];
-        }
-      }
+      const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
-      const int wbase = ti.g * p.N;
-      if (EPI == MOE_EPI_SWIGLU) {
-        // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
-#pragma unroll 1
-        for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
-          uint32_t vg[32], vu[32];
-          tmem_ld32(tbase + c * 32, vg);
-          tmem_ld32(tbase + BN / 2 + c * 32, vu);
-          tmem_ld_wait();
-          float h[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int ng = wbase + ti.n0 + c * 32 + j;
-            const int nu = ng + BN / 2;
-            const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
-            const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
-            float g = (float)ag * (sa * p.w_scale[ng]);
-            float u = (float)au * (sa * p.w_scale[nu]);
-            if (p.bias) {
-              g += p.bias[ng];
-              u += p.bias[nu];
-            }
-            h[j] = silu_f(g) * u * rw;
-          }
-          if (rvalid) store32<BF16>(p.out, (int64_t)row * p.ldo + ti.n0 / 2 + c * 32, h, 32, p.vec_ok);
-        }
-      } else {
-#pragma unroll 1
-        for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
-          uint32_t v[32];
-          tmem_ld32(tbase + c * 32, v);
-          tmem_ld_wait();
-          const int n_lo = ti.n0 + c * 32;
-          int nvalid = p.N - n_lo;
-          nvalid = nvalid > 32 ? 32 : nvalid;
-          if (!rvalid || nvalid <= 0) continue;
-          if (EPI == MOE_EPI_ACC_I32) {
-            int32_t* o = p.acc_out + (int64_t)row * p.ld_acc + n_lo;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < nvalid) {
-                const int n = wbase + n_lo + j;
-                o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
-              }
-            }
-          } else {
-            float y[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
-              const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
-              float val = (float)a * (sa * p.w_scale[n]);
-              if (p.bias) val += p.bias[n];
-              y[j] = val * rw;
-            }
-            store32<BF16>(p.out, (int64_t)row * p.ldo + n_lo, y, nvalid, p.vec_ok);
-          }
-        }
-      }
+      float bmn = FLT_MAX, bmx = -FLT_MAX;
+      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, bmn, bmx);
       tc_fence_before();
-      mbar_arrive(&tempty[as]);
+      if (CG == 2) mbar_arrive_leader(&tempty[as]);
+      else mbar_arrive(&tempty[as]);
+      if (EPI == MOE_EPI_SWIGLU && p.row_bounds && row < ti.m_end) {
+        atomicMin(&p.row_bounds[2 * (int64_t)row], fkey(bmn));
+        atomicMax(&p.row_bounds[2 * (int64_t)row + 1], fkey(bmx));
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * BN);
+    if (CG == 2) tmem_dealloc_pair(tmem_base, 2 * BN);
+    else tmem_dealloc(tmem_base, 2 * BN);
   }
 }
 
@@ -392,19 +473,65 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, int EPI, bool BF16>
+template <int BN, int STAGES, int EPI, bool BF16, int CG>
 static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& p, int grid,
                             cudaStream_t s) {
-  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16>;
-  constexpr int bytes = Smem<BN, STAGES>::kBytes;
+  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG>;
+  constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
   static bool attr_set = false;
   if (!attr_set) {
     MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr_set = true;
   }
-  kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, p); ::moe::count_launch();
+  if (CG == 1) {
+    kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  }
+  ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
+}
+
+template <int CG>
+static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const uint8_t* w, int64_t N,
+                              int64_t ldw, int num_groups, int epilogue, bool bf16, const GemmArgs& p,
+                              cudaStream_t s) {
+  constexpr int BN = 256;
+  constexpr int ST = CG == 2 ? 6 : 4;
+  CUtensorMap ta, tb;
+  if (!make_map_u8(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBM) ||
+      !make_map_u8(&tb, w, (uint64_t)N * num_groups, (uint64_t)K, (uint64_t)ldw, BN / CG)) {
+    set_error("w8a8_gemm: cuTensorMapEncodeTiled failed");
+    return MOE_ECUDA;
+  }
+  const int64_t TM = kBM * CG;
+  const int64_t n_tiles = (N + BN - 1) / BN;
+  const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
+  const int64_t max_units = num_sms() / CG;
+  const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
+  switch (epilogue) {
+    case MOE_EPI_DEQUANT:
+      return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG>(ta, tb, p, grid, s)
+                  : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG>(ta, tb, p, grid, s);
+    case MOE_EPI_SWIGLU:
+      return bf16 ? launch_tc<BN, ST, MOE_EPI_SWIGLU, true, CG>(ta, tb, p, grid, s)
+                  : launch_tc<BN, ST, MOE_EPI_SWIGLU, false, CG>(ta, tb, p, grid, s);
+    default:
+      return launch_tc<BN, ST, MOE_EPI_ACC_I32, false, CG>(ta, tb, p, grid, s);
+  }
 }
 
 }  // namespace moe
@@ -417,8 +544,14 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
                                     const int32_t* w_rowsum, const float* bias, const float* row_weight,
                                     const int32_t* group_offsets, int num_groups, int epilogue, void* out,
                                     int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
+                                    const float* next_smooth_recip_f32, int64_t next_ld, int32_t* row_bounds,
                                     moe_stream_t stream) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
+  if (row_bounds) {
+    MOE_REQUIRE(epilogue == MOE_EPI_SWIGLU, "w8a8_gemm: row_bounds is produced by the SwiGLU epilogue");
+    MOE_REQUIRE(next_smooth_recip_f32 && next_ld >= N / 2 && next_ld % 4 == 0,
+                "w8a8_gemm: row_bounds needs the next float32 reciprocal smoothing table");
+  }
   MOE_REQUIRE(M >= 1 && N >= 1 && K >= 1, "w8a8_gemm: empty problem");
   MOE_REQUIRE(lda >= K && ldw >= K, "w8a8_gemm: bad leading dimension");
   MOE_REQUIRE(M < (1LL << 31) && N < (1LL << 31) && K <= 33025, "w8a8_gemm: K too large for exact int32");
@@ -452,35 +585,26 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   p.ldo = ldo;
   p.acc_out = acc_out;
   p.ld_acc = ld_acc;
+  p.ns_rs32 = next_smooth_recip_f32;
+  p.ns_ld = next_ld;
+  p.row_bounds = row_bounds;
   const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
   p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
   cudaStream_t s = as_stream(stream);
+  if (row_bounds) {
+    rowbounds_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_bounds, M);
+    ::moe::count_launch();
+  }
   const bool bf16 = out_dtype == MOE_DT_BF16;
 
   const bool tc_ok = (K % 16 == 0) && K >= kBK && (lda % 16 == 0) && (ldw % 16 == 0) &&
                      ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+  MOE_REQUIRE(tc_ok || !row_bounds, "w8a8_gemm: row_bounds needs the tensor-core path (K % 16 == 0, K >= 128)");
   if (tc_ok) {
-    constexpr int BN = 256;
-    CUtensorMap ta, tb;
-    if (!make_map_u8(&ta, a, (uint64_t)M, (uint64_t)K, (uint64_t)lda, kBM) ||
-        !make_map_u8(&tb, w, (uint64_t)N * num_groups, (uint64_t)K, (uint64_t)ldw, BN)) {
-      set_error("w8a8_gemm: cuTensorMapEncodeTiled failed");
-      return MOE_ECUDA;
-    }
-    const int64_t n_tiles = (N + BN - 1) / BN;
-    const int64_t tiles_bound = ((M + kBM - 1) / kBM + num_groups) * n_tiles;
-    const int grid = (int)(tiles_bound < num_sms() ? tiles_bound : num_sms());
-    constexpr int ST = 4;
-    switch (epilogue) {
-      case MOE_EPI_DEQUANT:
-        return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true>(ta, tb, p, grid, s)
-                    : launch_tc<BN, ST, MOE_EPI_DEQUANT, false>(ta, tb, p, grid, s);
-      case MOE_EPI_SWIGLU:
-        return bf16 ? launch_tc<BN, ST, MOE_EPI_SWIGLU, true>(ta, tb, p, grid, s)
-                    : launch_tc<BN, ST, MOE_EPI_SWIGLU, false>(ta, tb, p, grid, s);
-      default:
-        return launch_tc<BN, ST, MOE_EPI_ACC_I32, false>(ta, tb, p, grid, s);
-    }
+    // CTA pairs once there are enough 256-row tiles to fill the machine
+    const bool pair = M >= 256 * 8 && getenv("MOE_B200_NO_PAIR") == nullptr;
+    return pair ? dispatch_tc<2>(a, M, K, lda, w, N, ldw, num_groups, epilogue, bf16, p, s)
+                : dispatch_tc<1>(a, M, K, lda, w, N, ldw, num_groups, epilogue, bf16, p, s);
   }
   const int64_t total = M * (epilogue == MOE_EPI_SWIGLU ? N / 2 : N);
   int64_t blocks = (total + 255) / 256;

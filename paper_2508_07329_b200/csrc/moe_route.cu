@@ -2,6 +2,8 @@
 // statistics feeding placement. None of these exist in the reference; they
 // implement the MoE forward around its quantizer (SURVEY.md §8a a'1, a'2)
 // and emit statistics in the reference's trace semantics (trace.py:207-225).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace moe {
@@ -92,6 +94,61 @@ __global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt,
     if (logits)
       for (int e = 0; e < E; ++e) logits[(int64_t)warp * E + e] = l[e];
     topk_select(l, E, k, idx + (int64_t)warp * k, w + (int64_t)warp * k);
+  }
+}
+
+// Persistent variant: the gate matrix (E x d float32) is staged once per CTA
+// in shared memory, each warp then streams tokens (x read exactly once from
+// HBM, weights from smem instead of E*d*4 bytes of L2 per token). Same
+// per-lane accumulation order as router_gate_kernel.
+template <int E_T>
+__global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat16* __restrict__ x, int64_t T,
+                                                               int64_t d, const float* __restrict__ gw,
+                                                               const float* gb, int E, int k, float* logits,
+                                                               int32_t* idx, float* w) {
+  extern __shared__ __align__(16) float sgw[];
+  for (int64_t i = threadIdx.x; i < (int64_t)E * d / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(sgw)[i] = reinterpret_cast<const float4*>(gw)[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int64_t t = (int64_t)blockIdx.x * nw + (threadIdx.x >> 5); t < T; t += (int64_t)gridDim.x * nw) {
+    float acc[E_T];
+#pragma unroll
+    for (int e = 0; e < E_T; ++e) acc[e] = 0.f;
+    const uint4* xp = reinterpret_cast<const uint4*>(x + t * d);
+    for (int64_t c = lane; c < d / 8; c += 32) {
+      const uint4 u = __ldcs(xp + c);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+      float xv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = __bfloat162float(h[i]);
+#pragma unroll
+      for (int e = 0; e < E_T; ++e) {
+        if (e >= E) break;
+        const float4* g = reinterpret_cast<const float4*>(sgw + (int64_t)e * d + c * 8);
+        const float4 g0 = g[0], g1 = g[1];
+        acc[e] = fmaf(xv[0], g0.x, acc[e]);
+        acc[e] = fmaf(xv[1], g0.y, acc[e]);
+        acc[e] = fmaf(xv[2], g0.z, acc[e]);
+        acc[e] = fmaf(xv[3], g0.w, acc[e]);
+        acc[e] = fmaf(xv[4], g1.x, acc[e]);
+        acc[e] = fmaf(xv[5], g1.y, acc[e]);
+        acc[e] = fmaf(xv[6], g1.z, acc[e]);
+        acc[e] = fmaf(xv[7], g1.w, acc[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E_T; ++e)
+      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (lane == 0) {
+      float l[E_T];
+#pragma unroll
+      for (int e = 0; e < E_T; ++e) l[e] = (gb && e < E) ? acc[e] + gb[e] : acc[e];
+      if (logits)
+        for (int e = 0; e < E; ++e) logits[t * E + e] = l[e];
+      topk_select(l, E, k, idx + t * k, w + t * k);
+    }
   }
 }
 
@@ -254,7 +311,20 @@ extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int
   const int64_t threads = T * 32;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   cudaStream_t s = as_stream(stream);
-  if (E <= 8) {
+  const int64_t gw_bytes = (int64_t)E * d * 4;
+  if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
+    static bool attr = false;
+    if (!attr) {
+      MOE_CUDA_TRY(cudaFuncSetAttribute(router_gate_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+      attr = true;
+    }
+    const int64_t grid = std::min<int64_t>((T + 15) / 16, num_sms());
+    router_gate_smem_kernel<8><<<(unsigned)grid, 512, (size_t)gw_bytes, s>>>(
+        static_cast<const __nv_bfloat16*>(x), T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
+    ::moe::count_launch();
+  } else if (E <= 8) {
     router_gate_kernel<8><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
   } else if (E <= 16) {
     router_gate_kernel<16><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();

@@ -141,11 +141,16 @@ class MoELayer:
                            row_group=perm["row_expert"],
                            gather=perm["src_token"], rows=T * self.k)
         mark("quant_x")
+        # the SwiGLU epilogue also emits each h row's float32 bounds of
+        # h * RN32(1/s2), so the second K1 skips a pass over h
+        fuse = self.d % 16 == 0 and self.d >= 128
+        bounds = torch.empty((T * self.k, 2), dtype=torch.int32, device=x.device) if fuse else None
         h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
-                          group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F)
+                          group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,
+                          next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_bounds=bounds)
         mark("gemm13_swiglu")
         a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
-                           row_group=perm["row_expert"])
+                           row_group=perm["row_expert"], row_bounds=bounds)
         mark("quant_h")
         y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)

@@ -55,7 +55,7 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
               smooth_mode: int = L.SMOOTH_DIVIDE, row_group: torch.Tensor | None = None,
               gather: torch.Tensor | None = None, rows: int | None = None, bits: int = 8,
               symmetric: bool = False, granularity: str = "per_token", rowsum: bool = True,
-              out_codes: torch.Tensor | None = None) -> dict:
+              out_codes: torch.Tensor | None = None, row_bounds: torch.Tensor | None = None) -> dict:
     """K1: codes/scales/zero points of (x[gather] (/ or *) smooth[row_group])."""
     x = _rowmajor(x, "x")
     n_rows = rows if rows is not None else (gather.numel() if gather is not None else x.shape[0])
@@ -83,7 +83,7 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
            L.ptr(smooth_recip) if div else None, L.ptr(smooth_recip_f32) if div else None, mode,
            L.ptr(row_group), bits,
            int(bool(symmetric)), gran, L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp),
-           L.ptr(rs), L.ptr(ws), wsb, _s())
+           L.ptr(rs), L.ptr(row_bounds), L.ptr(ws), wsb, _s())
     return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
             "granularity": granularity, "bits": bits}
 
@@ -117,7 +117,8 @@ def channel_stats(x: torch.Tensor, strategy: int) -> torch.Tensor:
 def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torch.float32,
               bias: torch.Tensor | None = None, row_weight: torch.Tensor | None = None,
               group_offsets: torch.Tensor | None = None, num_groups: int = 1, n_per_group: int | None = None,
-              out: torch.Tensor | None = None) -> torch.Tensor:
+              out: torch.Tensor | None = None, next_smooth_recip_f32: torch.Tensor | None = None,
+              row_bounds: torch.Tensor | None = None) -> torch.Tensor:
     """a: dict from act_quant (codes [M, K], scale_f32, zp, rowsum per row).
     w: dict with codes [G*N, K], scale_f32, zp, rowsum per row."""
     ac, wc = a["codes"], w["codes"]
@@ -144,7 +145,9 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
     L.call("moe_w8a8_gemm", L.ptr(ac), M, K, ac.stride(0), L.ptr(a_scale), L.ptr(a_zp), L.ptr(a["rowsum"]),
            L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w["rowsum"]),
            L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue, L.ptr(o), odt, ldo,
-           L.ptr(acc), acc.stride(0) if acc is not None else 0, _s())
+           L.ptr(acc), acc.stride(0) if acc is not None else 0,
+           L.ptr(next_smooth_recip_f32),
+           next_smooth_recip_f32.shape[-1] if next_smooth_recip_f32 is not None else 0, L.ptr(row_bounds), _s())
     return acc if epilogue == L.EPI_ACC_I32 else o
 
 

@@ -133,7 +133,9 @@ def _dev_operand(cuda, codes, zp, scale):
 
 
 @pytest.mark.parametrize("M_,N,K", [(300, 512, 512), (128, 256, 4096), (1000, 768, 272), (77, 40, 48),
-                                    (513, 1024, 14336)])
+                                    (513, 1024, 14336),
+                                    # CTA-pair (cta_group::2) path: M >= 2048, ragged last tile
+                                    (2500, 768, 4096), (4096, 512, 1024), (2049, 256, 14336)])
 def test_gemm_accumulators_bitexact(cuda, M_, N, K):
     rng = np.random.default_rng(M_ * 7 + N + K)
     a = _rand_operand(rng, M_, K)
@@ -165,10 +167,11 @@ def test_gemm_dequant_epilogue(cuda, out_dtype):
     np.testing.assert_allclose(y.float().cpu().numpy(), want, rtol=tol, atol=tol * np.abs(want).max() * 1e-3)
 
 
-def test_grouped_gemm_ragged(cuda):
+@pytest.mark.parametrize("counts", [[0, 129, 1, 300, 77], [0, 1029, 1, 1300, 777], [2048, 0, 256, 513, 3]])
+def test_grouped_gemm_ragged(cuda, counts):
     rng = np.random.default_rng(12)
     E, N, K = 5, 256, 512
-    counts = np.array([0, 129, 1, 300, 77])
+    counts = np.array(counts)
     offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
     Mt = int(offs[-1])
     a = _rand_operand(rng, Mt, K)
