@@ -88,11 +88,13 @@ moe_status moe_device_check(int dev);
  * group (workspace >= moe_act_quant_workspace()). Outputs: codes [rows,
  * ldc], scale f64 [groups], scale_f32 (optional) [groups], zp [groups],
  * rowsum (optional) [rows] = sum of the row's codes (for the GEMM's
- * zero-point correction). row_bounds (optional, per-row modes, bf16 input):
- * float32 (min, max) of each smoothed row (x * RN32(1/s)) as
- * order-preserving int32 keys [rows, 2], as produced by moe_w8a8_gemm's
- * SwiGLU epilogue — the kernel then skips its float32 pass; exactness is
- * unaffected (the float64 extremes are still resolved here).
+ * zero-point correction). row_ext (optional, per-row modes, bf16 input):
+ * records [rows, 2] (min, max) of the float32 smoothed row (x * RN32(1/s)),
+ * each (order-preserving key of the value << 32) | column, as produced by
+ * moe_w8a8_gemm's SwiGLU epilogue — the kernel then speculates that the two
+ * recorded elements are the exact extremes and streams the row once,
+ * verifying the speculation while encoding (a failed check re-encodes the
+ * row exactly); results are identical either way.
  */
 int64_t moe_act_quant_workspace(int64_t rows, int64_t cols, int granularity);
 moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
@@ -100,7 +102,7 @@ moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols,
                          const float* smooth_recip_f32, int smooth_mode, const int32_t* row_group,
                          int bits, int symmetric,
                          int granularity, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
-                         int32_t* zp, int32_t* rowsum, const int32_t* row_bounds, void* workspace,
+                         int32_t* zp, int32_t* rowsum, const unsigned long long* row_ext, void* workspace,
                          int64_t workspace_bytes, moe_stream_t stream);
 
 /* out[i] = RN(1 / s[i]) (float64) and optionally out_f32[i] = RN32(out[i]);
@@ -138,17 +140,17 @@ moe_status moe_channel_stats(const double* x, int64_t n, int64_t T, int strategy
  * of M rows. K must be a multiple of 16; other shapes use a SIMT path with
  * identical integer results.
  * Fusion with the next K1 (SwiGLU epilogue, tensor-core path): when
- * row_bounds [M, 2] is given, the epilogue also emits the float32 (min, max)
- * of each stored output row times the next layer's RN32 reciprocal
- * smoothing (table [G, next_ld]) as order-preserving int32 keys, so that
- * moe_act_quant(row_bounds=...) skips one pass over h. */
+ * row_ext [M, 2] is given, the epilogue also emits the (value, column)
+ * records of the float32 min and max of each stored output row times the
+ * next layer's RN32 reciprocal smoothing (table [G, next_ld]), so that
+ * moe_act_quant(row_ext=...) reads h once. */
 moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
                          const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
                          int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,
                          const float* bias, const float* row_weight, const int32_t* group_offsets,
                          int num_groups, int epilogue, void* out, int out_dtype, int64_t ldo,
                          int32_t* acc_out, int64_t ld_acc, const float* next_smooth_recip_f32,
-                         int64_t next_ld, int32_t* row_bounds, moe_stream_t stream);
+                         int64_t next_ld, unsigned long long* row_ext, moe_stream_t stream);
 
 /* Frobenius-loss reduction for quant_loss (quant.py:283) on the exact
  * accumulators: out = sum_{m,n} (a_scale[m]*w_scale[n]*acc[m,n] - ref[m,n])^2

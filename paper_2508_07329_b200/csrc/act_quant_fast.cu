@@ -144,10 +144,8 @@ struct RowEncoder {
     packed = bits == 8 && !exact && fmax(fabs(mn), fabs(mx)) * p.rscale < 2097152.0;
   }
 
-  __device__ __forceinline__ uint2 encode8(const uint4& u, const float* tab, int64_t c, const double* srow,
+  __device__ __forceinline__ uint2 encode8(const uint4& u, const float (&xs)[8], int64_t c, const double* srow,
                                            const double* rrow, int& sum) const {
-    float xs[8];
-    smooth8(u, tab, c, xs);
     uint2 out;
     uint32_t redo = 0;
     if (packed) {
@@ -186,8 +184,19 @@ struct RowEncoder {
   }
 };
 
-// order-preserving int32 key of a float (atomic min/max of floats)
-__device__ __forceinline__ float funkey(int k) { return __int_as_float(k >= 0 ? k : (k ^ 0x7FFFFFFF)); }
+// ── per-row extreme records ────────────────────────────────────────────────
+// (float32 value, column) of the max and of the min of the smoothed row, as
+// produced by the grouped GEMM's SwiGLU epilogue ((order key << 32) | col)
+// or by pass A here.
+struct RowExt {
+  float M, m;
+  int64_t cM, cm;
+};
+
+__device__ __forceinline__ float key_to_float(uint32_t k) {
+  const int i = (int)(k ^ 0x80000000u);
+  return __int_as_float(i >= 0 ? i : (i ^ 0x7FFFFFFF));
+}
 
 template <typename F>
 __device__ __forceinline__ void for_row_batches(const uint4* src, int64_t nvec, int lane, F&& body) {
@@ -206,11 +215,45 @@ __device__ __forceinline__ void for_row_batches(const uint4* src, int64_t nvec, 
   }
 }
 
+// warp arg-reduce: larger value wins, ties to the lower column
+__device__ __forceinline__ void warp_argmax(float& v, int64_t& col) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int64_t c2 = __shfl_xor_sync(0xffffffffu, col, o);
+    if (v2 > v || (v2 == v && c2 < col)) {
+      v = v2;
+      col = c2;
+    }
+  }
+}
+__device__ __forceinline__ void warp_argmin(float& v, int64_t& col) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int64_t c2 = __shfl_xor_sync(0xffffffffu, col, o);
+    if (v2 < v || (v2 == v && c2 < col)) {
+      v = v2;
+      col = c2;
+    }
+  }
+}
+
+// exact float64 value of element j of the row, and whether its float32
+// evaluation matches the recorded extreme (record consistency check)
+__device__ __forceinline__ double exact_at(const __nv_bfloat16* row, const float* tab, const double* srow,
+                                           const double* rrow, int64_t j, float expect, bool& ok) {
+  const float xf = __bfloat162float(row[j]);
+  const float xs = tab ? __fmul_rn(xf, tab[j]) : xf;
+  ok = ok && xs == expect;
+  return srow ? div_rcp((double)xf, srow[j], rrow[j]) : (double)xf;
+}
+
 template <bool GIVEN>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
-    act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const int* __restrict__ bounds, int bits,
-                          int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
-                          int32_t* rowsum, int64_t rows_per_cta) {
+    act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
+                          int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                          int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t nvec = a.cols / 8;
@@ -220,76 +263,117 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
   const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
   for (int64_t r = r_lo + warp; r < r_hi; r += kWarpsPerCta) {
     const RowView rv = row_view(a, r);
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x) + rv.off);
+    const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + rv.off;
+    const uint4* src = reinterpret_cast<const uint4*>(row);
     const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
     const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
     const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
 
-    // pass A: float32 extremes (given by the producing epilogue, or computed)
-    float M, m;
+    // records of the float32 extremes: from the producer, or pass A
+    RowExt rec;
     if (GIVEN) {
-      m = funkey(bounds[2 * r]);
-      M = funkey(bounds[2 * r + 1]);
+      const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
+      rec = RowExt{key_to_float((uint32_t)(kmax >> 32)), key_to_float((uint32_t)(kmin >> 32)),
+                   (int64_t)(kmax & 0xFFFFFFFFu), (int64_t)(kmin & 0xFFFFFFFFu)};
     } else {
       float tmax = -FLT_MAX, tmin = FLT_MAX;
+      int64_t imax = 0, imin = 0;
       for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
         float xs[8];
         smooth8(u, tab, c, xs);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          tmax = fmaxf(tmax, xs[e]);
-          tmin = fminf(tmin, xs[e]);
+          if (xs[e] > tmax) { tmax = xs[e]; imax = c * 8 + e; }
+          if (xs[e] < tmin) { tmin = xs[e]; imin = c * 8 + e; }
         }
       });
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-        tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-      }
-      M = tmax;
-      m = tmin;
+      warp_argmax(tmax, imax);
+      warp_argmin(tmin, imin);
+      rec = RowExt{tmax, tmin, imax, imin};
     }
-    const bool exact_all = !(isfinite(M) && isfinite(m));
-    const float lb_max = exact_all ? -FLT_MAX : M - err_bound(M);   // the exact max is >= this
-    const float ub_min = exact_all ? FLT_MAX : m + err_bound(m);    // the exact min is <= this
-
-    // pass B: exact float64 extremes over the elements that can reach them
+    const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m)) || rec.cM >= a.cols || rec.cm >= a.cols;
+    // speculative exact extremes: the recorded elements (verified below)
+    bool spec = !exact_all;
     double mn = DBL_MAX, mx = -DBL_MAX;
-    for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
-      float xs[8];
-      smooth8(u, tab, c, xs);
-      uint32_t mmax = 0, mmin = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        mmax |= (uint32_t)(xs[e] + err_bound(xs[e]) >= lb_max) << e;
-        mmin |= (uint32_t)(xs[e] - err_bound(xs[e]) <= ub_min) << e;
-      }
-      if (mmax | mmin) {
-        const double2 ext = exact_extremes8(u, srow, rrow, c, mmax, mmin);
-        mn = fmin(mn, ext.x);
-        mx = fmax(mx, ext.y);
-      }
-    });
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (spec) {
+      mx = exact_at(row, tab, srow, rrow, rec.cM, rec.M, spec);
+      mn = exact_at(row, tab, srow, rrow, rec.cm, rec.m, spec);
     }
-    const AffineParams p = affine_params(mn, mx, bits, sym);
-    const RowEncoder enc(p, mn, mx, bits, exact_all);
-
-    // pass C: encode
+    // a record that names an element of the row bounds the exact extreme
+    // (the max is >= lb_max, the min <= ub_min); an inconsistent one bounds nothing
+    const float lb_max = spec ? rec.M - err_bound(rec.M) : -FLT_MAX;
+    const float ub_min = spec ? rec.m + err_bound(rec.m) : FLT_MAX;
     int sum = 0;
-    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
-    for_row_batches(src, nvec, lane,
-                    [&](const uint4& u, int64_t c) { __stcs(dst + c, enc.encode8(u, tab, c, srow, rrow, sum)); });
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (!spec) {
+        // pass B: exact float64 extremes over every element that can reach them
+        mn = DBL_MAX;
+        mx = -DBL_MAX;
+        for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+          float xs[8];
+          smooth8(u, tab, c, xs);
+          uint32_t mmax = 0, mmin = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) {
-      if (rowsum) rowsum[r] = sum;
-      scale[r] = p.scale;
-      if (scale_f32) scale_f32[r] = (float)p.scale;
-      zp[r] = p.zp;
+          for (int e = 0; e < 8; ++e) {
+            mmax |= (uint32_t)(xs[e] + err_bound(xs[e]) >= lb_max) << e;
+            mmin |= (uint32_t)(xs[e] - err_bound(xs[e]) <= ub_min) << e;
+          }
+          if (mmax | mmin) {
+            const double2 e2 = exact_extremes8(u, srow, rrow, c, mmax, mmin);
+            mn = fmin(mn, e2.x);
+            mx = fmax(mx, e2.y);
+          }
+        });
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+      }
+      const AffineParams p = affine_params(mn, mx, bits, sym);
+      const RowEncoder enc(p, mn, mx, bits, exact_all);
+      // pass C: encode; while speculating also count the elements that could
+      // be extremes (must be exactly the two recorded ones)
+      sum = 0;
+      int cnt_max = 0, cnt_min = 0;
+      uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+      const bool count = spec;
+      const float2 K2 = make_float2(kRelErr, kRelErr), A2 = make_float2(kAbsErr, kAbsErr);
+      for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+        float xs[8];
+        smooth8(u, tab, c, xs);
+        if (count) {
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float2 eb = __ffma2_rn(make_float2(fabsf(xs[e]), fabsf(xs[e + 1])), K2, A2);
+            const float2 hi = __fadd2_rn(make_float2(xs[e], xs[e + 1]), eb);
+            const float2 lo = __fadd2_rn(make_float2(xs[e], xs[e + 1]), make_float2(-eb.x, -eb.y));
+            cnt_max += (hi.x >= lb_max) + (hi.y >= lb_max);
+            cnt_min += (lo.x <= ub_min) + (lo.y <= ub_min);
+          }
+        }
+        __stcs(dst + c, enc.encode8(u, xs, c, srow, rrow, sum));
+      });
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (count) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          cnt_max += __shfl_xor_sync(0xffffffffu, cnt_max, o);
+          cnt_min += __shfl_xor_sync(0xffffffffu, cnt_min, o);
+        }
+        if (cnt_max != 1 || cnt_min != 1) {  // another element could be an extreme: redo exactly
+          spec = false;
+          continue;
+        }
+      }
+      if (lane == 0) {
+        if (rowsum) rowsum[r] = sum;
+        scale[r] = p.scale;
+        if (scale_f32) scale_f32[r] = (float)p.scale;
+        zp[r] = p.zp;
+      }
+      break;
     }
   }
 }
@@ -302,7 +386,7 @@ static bool eligible(const RowArgs& a, const float* rs32, uint8_t* codes, int64_
 }
 
 template <bool GIVEN>
-static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const int* bounds, int bits, int sym,
+static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                               int32_t* rowsum, cudaStream_t s) {
   // contiguous row ranges, ~4 CTAs (64 warps) per SM
@@ -311,16 +395,16 @@ static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const int* b
   const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
   const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
   act_quant_warp_kernel<GIVEN><<<(unsigned)nblk, kWarpsPerCta * 32, 0, s>>>(
-      a, rs32, bounds, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
   count_launch();
   return cudaGetLastError();
 }
 
-bool launch_act_quant_given(const RowArgs& a, const float* rs32, const int* bounds, int bits, int sym,
+bool launch_act_quant_given(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                             uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                             int32_t* rowsum, cudaStream_t s, cudaError_t* err) {
-  if (!bounds || !eligible(a, rs32, codes, ldc)) return false;
-  *err = launch_warp<true>(a, rs32, bounds, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+  if (!ext || !eligible(a, rs32, codes, ldc)) return false;
+  *err = launch_warp<true>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   return true;
 }
 

@@ -56,7 +56,7 @@ struct GemmArgs {
   // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
   const float* ns_rs32;
   int64_t ns_ld;
-  int* row_bounds;
+  unsigned long long* row_ext;  // [M, 2] (min, max) records
 };
 
 template <int BN, int STAGES, int CG>
@@ -120,32 +120,63 @@ __device__ __forceinline__ void store32(void* out, int64_t idx, const float (&v)
   }
 }
 
-// ── float32 per-row bounds of the stored outputs * RN32(1/s_next) ─────────
-// Feeds the next K1 (act_quant row_bounds): the same float32 products K1
-// forms, reduced to a per-thread (min, max) and merged per row with one
-// order-preserving int32 atomic each per tile. Exactness stays in K1.
-__device__ __forceinline__ int fkey(float f) {
-  const int i = __float_as_int(f);
-  return i >= 0 ? i : (i ^ 0x7FFFFFFF);
-}
+// ── per-row float32 extreme records of stored output * RN32(1/s_next) ─────
+// Feeds the next K1 (act_quant row_ext): the same float32 products K1 forms,
+// reduced per thread to (value, column) of the max and of the min and merged
+// per row with one 64-bit atomic each per tile: (order-preserving key << 32)
+// | column. K1 then only divides those two elements exactly and verifies
+// during its single encode pass that no other element could be an extreme.
+struct ExtRec {
+  float M, m;
+  int cM, cm;
+};
 
-__device__ __forceinline__ void chunk_bounds(const float (&hv)[32], const float* __restrict__ t32, float& m,
-                                             float& M) {
+__device__ __forceinline__ void chunk_ext(const float (&hv)[32], const float* __restrict__ t32, int col0,
+                                          ExtRec& r) {
   const float4* t = reinterpret_cast<const float4*>(t32);
+  float xs[32];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float4 tt = __ldg(t + q);
     const float2 a = __fmul2_rn(make_float2(hv[4 * q], hv[4 * q + 1]), make_float2(tt.x, tt.y));
     const float2 b = __fmul2_rn(make_float2(hv[4 * q + 2], hv[4 * q + 3]), make_float2(tt.z, tt.w));
-    M = fmaxf(fmaxf(M, a.x), fmaxf(a.y, fmaxf(b.x, b.y)));
-    m = fminf(fminf(m, a.x), fminf(a.y, fminf(b.x, b.y)));
+    xs[4 * q] = a.x;
+    xs[4 * q + 1] = a.y;
+    xs[4 * q + 2] = b.x;
+    xs[4 * q + 3] = b.y;
+  }
+  float M = xs[0], m = xs[0];
+#pragma unroll
+  for (int j = 1; j < 32; ++j) {
+    M = fmaxf(M, xs[j]);
+    m = fminf(m, xs[j]);
+  }
+  if (M > r.M) {  // rare after the first chunk: locate the column
+    int j0 = 0;
+#pragma unroll
+    for (int j = 31; j >= 0; --j) j0 = xs[j] == M ? j : j0;
+    r.M = M;
+    r.cM = col0 + j0;
+  }
+  if (m < r.m) {
+    int j0 = 0;
+#pragma unroll
+    for (int j = 31; j >= 0; --j) j0 = xs[j] == m ? j : j0;
+    r.m = m;
+    r.cm = col0 + j0;
   }
 }
 
-__global__ void rowbounds_init_kernel(int* rb, int64_t M) {
+__device__ __forceinline__ unsigned long long ext_key(float v, int col) {
+  const int i = __float_as_int(v);
+  const uint32_t k = (uint32_t)(i >= 0 ? i : (i ^ 0x7FFFFFFF)) ^ 0x80000000u;  // unsigned float order
+  return ((unsigned long long)k << 32) | (uint32_t)col;
+}
+
+__global__ void rowext_init_kernel(unsigned long long* re, int64_t M) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
-    rb[2 * i] = 0x7FFFFFFF;
-    rb[2 * i + 1] = (int)0x80000000;
+    re[2 * i] = ~0ull;     // min record
+    re[2 * i + 1] = 0ull;  // max record
   }
 }
 
@@ -160,7 +191,7 @@ __device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t 
 // `half` (8 epilogue warps split the 256 columns), output row `row`.
 template <int BN, int EPI, bool BF16>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase,
-                                              int half, float& bmn, float& bmx) {
+                                              int half, ExtRec& ext) {
   const bool rvalid = row < ti.m_end;
   float sa = 0.f, rw = 1.f;
   int32_t za = 0, rsa = 0;
@@ -199,7 +230,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
       }
       if (rvalid) {
         store32<BF16>(p.out, (int64_t)row * p.ldo + ti.n0 / 2 + c * 32, h, 32, p.vec_ok);
-        if (p.row_bounds) chunk_bounds(h, p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + c * 32, bmn, bmx);
+        if (p.row_ext) chunk_ext(h, p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + c * 32, ti.n0 / 2 + c * 32, ext);
       }
     }
   } else {
@@ -378,14 +409,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
-      float bmn = FLT_MAX, bmx = -FLT_MAX;
-      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, bmn, bmx);
+      ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
+      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext);
       tc_fence_before();
       if (CG == 2) mbar_arrive_leader(&tempty[as]);
       else mbar_arrive(&tempty[as]);
-      if (EPI == MOE_EPI_SWIGLU && p.row_bounds && row < ti.m_end) {
-        atomicMin(&p.row_bounds[2 * (int64_t)row], fkey(bmn));
-        atomicMax(&p.row_bounds[2 * (int64_t)row + 1], fkey(bmx));
+      if (EPI == MOE_EPI_SWIGLU && p.row_ext && row < ti.m_end) {
+        atomicMin(&p.row_ext[2 * (int64_t)row], ext_key(ext.m, ext.cm));
+        atomicMax(&p.row_ext[2 * (int64_t)row + 1], ext_key(ext.M, ext.cM));
       }
     }
   }
@@ -544,13 +575,13 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
                                     const int32_t* w_rowsum, const float* bias, const float* row_weight,
                                     const int32_t* group_offsets, int num_groups, int epilogue, void* out,
                                     int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                                    const float* next_smooth_recip_f32, int64_t next_ld, int32_t* row_bounds,
+                                    const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
                                     moe_stream_t stream) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
-  if (row_bounds) {
-    MOE_REQUIRE(epilogue == MOE_EPI_SWIGLU, "w8a8_gemm: row_bounds is produced by the SwiGLU epilogue");
+  if (row_ext) {
+    MOE_REQUIRE(epilogue == MOE_EPI_SWIGLU, "w8a8_gemm: row_ext is produced by the SwiGLU epilogue");
     MOE_REQUIRE(next_smooth_recip_f32 && next_ld >= N / 2 && next_ld % 4 == 0,
-                "w8a8_gemm: row_bounds needs the next float32 reciprocal smoothing table");
+                "w8a8_gemm: row_ext needs the next float32 reciprocal smoothing table");
   }
   MOE_REQUIRE(M >= 1 && N >= 1 && K >= 1, "w8a8_gemm: empty problem");
   MOE_REQUIRE(lda >= K && ldw >= K, "w8a8_gemm: bad leading dimension");
@@ -587,19 +618,19 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   p.ld_acc = ld_acc;
   p.ns_rs32 = next_smooth_recip_f32;
   p.ns_ld = next_ld;
-  p.row_bounds = row_bounds;
+  p.row_ext = row_ext;
   const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
   p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
   cudaStream_t s = as_stream(stream);
-  if (row_bounds) {
-    rowbounds_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_bounds, M);
+  if (row_ext) {
+    rowext_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_ext, M);
     ::moe::count_launch();
   }
   const bool bf16 = out_dtype == MOE_DT_BF16;
 
   const bool tc_ok = (K % 16 == 0) && K >= kBK && (lda % 16 == 0) && (ldw % 16 == 0) &&
                      ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
-  MOE_REQUIRE(tc_ok || !row_bounds, "w8a8_gemm: row_bounds needs the tensor-core path (K % 16 == 0, K >= 128)");
+  MOE_REQUIRE(tc_ok || !row_ext, "w8a8_gemm: row_ext needs the tensor-core path (K % 16 == 0, K >= 128)");
   if (tc_ok) {
     // CTA pairs once there are enough 256-row tiles to fill the machine
     const bool pair = M >= 256 * 8 && getenv("MOE_B200_NO_PAIR") == nullptr;

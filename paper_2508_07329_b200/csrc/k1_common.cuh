@@ -87,10 +87,10 @@ bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sy
                            double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum, cudaStream_t s,
                            cudaError_t* err);
 
-// K1 for rows whose float32 (min, max) of the smoothed values were produced
-// upstream (grouped GEMM SwiGLU epilogue) as order-preserving int32 keys
-// `bounds` [rows, 2]: skips the float32 pass. False if not eligible.
-bool launch_act_quant_given(const RowArgs& a, const float* rs32, const int* bounds, int bits, int sym,
+// K1 for rows whose float32 (min, max) records of the smoothed values were
+// produced upstream (grouped GEMM SwiGLU epilogue) as (order key << 32 | col)
+// `ext` [rows, 2]: a single speculative encode pass. False if not eligible.
+bool launch_act_quant_given(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                             uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                             int32_t* rowsum, cudaStream_t s, cudaError_t* err);
 

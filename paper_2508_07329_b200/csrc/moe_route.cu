@@ -116,26 +116,23 @@ __global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat
     float acc[E_T];
 #pragma unroll
     for (int e = 0; e < E_T; ++e) acc[e] = 0.f;
-    const uint4* xp = reinterpret_cast<const uint4*>(x + t * d);
-    for (int64_t c = lane; c < d / 8; c += 32) {
-      const uint4 u = __ldcs(xp + c);
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
-      float xv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) xv[i] = __bfloat162float(h[i]);
+    // 4 elements (8 B of x, one conflict-free float4 of each gate row) per
+    // lane and step; 4 steps in flight
+    const uint2* xp = reinterpret_cast<const uint2*>(x + t * d);
+    const int64_t n4 = d / 4;
+#pragma unroll 4
+    for (int64_t c = lane; c < n4; c += 32) {
+      const uint2 u = __ldcs(xp + c);
+      const float xv[4] = {__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                           __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u)};
 #pragma unroll
       for (int e = 0; e < E_T; ++e) {
         if (e >= E) break;
-        const float4* g = reinterpret_cast<const float4*>(sgw + (int64_t)e * d + c * 8);
-        const float4 g0 = g[0], g1 = g[1];
-        acc[e] = fmaf(xv[0], g0.x, acc[e]);
-        acc[e] = fmaf(xv[1], g0.y, acc[e]);
-        acc[e] = fmaf(xv[2], g0.z, acc[e]);
-        acc[e] = fmaf(xv[3], g0.w, acc[e]);
-        acc[e] = fmaf(xv[4], g1.x, acc[e]);
-        acc[e] = fmaf(xv[5], g1.y, acc[e]);
-        acc[e] = fmaf(xv[6], g1.z, acc[e]);
-        acc[e] = fmaf(xv[7], g1.w, acc[e]);
+        const float4 g = reinterpret_cast<const float4*>(sgw + (int64_t)e * d)[c];
+        acc[e] = fmaf(xv[0], g.x, acc[e]);
+        acc[e] = fmaf(xv[1], g.y, acc[e]);
+        acc[e] = fmaf(xv[2], g.z, acc[e]);
+        acc[e] = fmaf(xv[3], g.w, acc[e]);
       }
     }
 #pragma unroll

@@ -174,7 +174,7 @@ extern "C" moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, in
                                     const float* smooth_recip_f32, int smooth_mode, const int32_t* row_group,
                                     int bits, int symmetric, int granularity, uint8_t* codes, int64_t ldc,
                                     double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum,
-                                    const int32_t* row_bounds, void* workspace, int64_t workspace_bytes,
+                                    const unsigned long long* row_ext, void* workspace, int64_t workspace_bytes,
                                     moe_stream_t stream) {
   MOE_REQUIRE(x && codes && scale && zp, "act_quant: null pointer");
   MOE_REQUIRE(rows >= 1 && cols >= 1, "act_quant: matrix must be non-empty");
@@ -194,11 +194,11 @@ extern "C" moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, in
     tensor_minmax_kernel<<<(unsigned)rows, kQuantThreads, 0, s>>>(a, ws); ::moe::count_launch();
     tensor_encode_kernel<<<(unsigned)rows, kQuantThreads, 0, s>>>(a, ws, bits, symmetric, codes, ldc, scale,
                                                                    scale_f32, zp, rowsum); ::moe::count_launch();
-  } else if (row_bounds) {
+  } else if (row_ext) {
     cudaError_t err = cudaSuccess;
-    MOE_REQUIRE(launch_act_quant_given(a, smooth_recip_f32, row_bounds, bits, symmetric, codes, ldc, scale,
+    MOE_REQUIRE(launch_act_quant_given(a, smooth_recip_f32, row_ext, bits, symmetric, codes, ldc, scale,
                                        scale_f32, zp, rowsum, s, &err),
-                "act_quant: row_bounds needs bf16 rows (cols % 8 == 0) and float32 reciprocals");
+                "act_quant: row_ext needs bf16 rows (cols % 8 == 0) and float32 reciprocals");
     MOE_CUDA_TRY(err);
   } else {
     cudaError_t err = cudaSuccess;

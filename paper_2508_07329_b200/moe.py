@@ -141,16 +141,16 @@ class MoELayer:
                            row_group=perm["row_expert"],
                            gather=perm["src_token"], rows=T * self.k)
         mark("quant_x")
-        # the SwiGLU epilogue also emits each h row's float32 bounds of
-        # h * RN32(1/s2), so the second K1 skips a pass over h
+        # the SwiGLU epilogue also emits each h row's (value, column) records
+        # of the float32 min/max of h * RN32(1/s2), so the second K1 streams h once
         fuse = self.d % 16 == 0 and self.d >= 128
-        bounds = torch.empty((T * self.k, 2), dtype=torch.int32, device=x.device) if fuse else None
+        ext = torch.empty((T * self.k, 2), dtype=torch.int64, device=x.device) if fuse else None
         h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,
-                          next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_bounds=bounds)
+                          next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_ext=ext)
         mark("gemm13_swiglu")
         a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
-                           row_group=perm["row_expert"], row_bounds=bounds)
+                           row_group=perm["row_expert"], row_ext=ext)
         mark("quant_h")
         y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)

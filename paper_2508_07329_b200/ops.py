@@ -55,7 +55,7 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
               smooth_mode: int = L.SMOOTH_DIVIDE, row_group: torch.Tensor | None = None,
               gather: torch.Tensor | None = None, rows: int | None = None, bits: int = 8,
               symmetric: bool = False, granularity: str = "per_token", rowsum: bool = True,
-              out_codes: torch.Tensor | None = None, row_bounds: torch.Tensor | None = None) -> dict:
+              out_codes: torch.Tensor | None = None, row_ext: torch.Tensor | None = None) -> dict:
     """K1: codes/scales/zero points of (x[gather] (/ or *) smooth[row_group])."""
     x = _rowmajor(x, "x")
     n_rows = rows if rows is not None else (gather.numel() if gather is not None else x.shape[0])
@@ -83,7 +83,7 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
            L.ptr(smooth_recip) if div else None, L.ptr(smooth_recip_f32) if div else None, mode,
            L.ptr(row_group), bits,
            int(bool(symmetric)), gran, L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp),
-           L.ptr(rs), L.ptr(row_bounds), L.ptr(ws), wsb, _s())
+           L.ptr(rs), L.ptr(row_ext), L.ptr(ws), wsb, _s())
     return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
             "granularity": granularity, "bits": bits}
 
@@ -118,7 +118,7 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
               bias: torch.Tensor | None = None, row_weight: torch.Tensor | None = None,
               group_offsets: torch.Tensor | None = None, num_groups: int = 1, n_per_group: int | None = None,
               out: torch.Tensor | None = None, next_smooth_recip_f32: torch.Tensor | None = None,
-              row_bounds: torch.Tensor | None = None) -> torch.Tensor:
+              row_ext: torch.Tensor | None = None) -> torch.Tensor:
     """a: dict from act_quant (codes [M, K], scale_f32, zp, rowsum per row).
     w: dict with codes [G*N, K], scale_f32, zp, rowsum per row."""
     ac, wc = a["codes"], w["codes"]
@@ -147,7 +147,7 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
            L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue, L.ptr(o), odt, ldo,
            L.ptr(acc), acc.stride(0) if acc is not None else 0,
            L.ptr(next_smooth_recip_f32),
-           next_smooth_recip_f32.shape[-1] if next_smooth_recip_f32 is not None else 0, L.ptr(row_bounds), _s())
+           next_smooth_recip_f32.shape[-1] if next_smooth_recip_f32 is not None else 0, L.ptr(row_ext), _s())
     return acc if epilogue == L.EPI_ACC_I32 else o
 
 

@@ -117,6 +117,87 @@ def test_act_quant_edge_values(cuda):
                 np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
 
 
+def _ext_key(v32, col):
+    """(order-preserving key of a float32 << 32) | column, as int64 bits."""
+    i = np.asarray(v32, np.float32).view(np.int32).astype(np.int64)
+    u = np.where(i >= 0, i, i ^ 0x7FFFFFFF) & 0xFFFFFFFF
+    k = u ^ 0x80000000
+    return ((k << 32) | np.asarray(col, np.int64)).astype(np.uint64).view(np.int64)
+
+
+def _true_records(x32, recip32):
+    xs = x32 * recip32
+    cM, cm = xs.argmax(1), xs.argmin(1)
+    r = np.arange(len(xs))
+    return np.stack([_ext_key(xs[r, cm], cm), _ext_key(xs[r, cM], cM)], 1)
+
+
+def test_act_quant_row_ext_speculation(cuda):
+    """K1 fed (value, column) extreme records: correct records, records that
+    point at the wrong element, stale values, duplicated extremes, empty
+    (never-written) records and out-of-range columns all give the exact
+    result — the kernel verifies the speculation and re-encodes on failure."""
+    rng = np.random.default_rng(21)
+    T, d, G = 96, 1024, 4
+    x = _acts(rng, T, d)
+    x[5, 7] = x[5, 900] = 50.0                                   # duplicated maximum
+    x[6, 3] = x[6, 4] = -70.0                                    # duplicated minimum (same column scale below)
+    s = _smooth(rng, G, d)
+    s[:, 4] = s[:, 3]
+    group = rng.integers(0, G, size=T).astype(np.int32)
+    recip32 = (1.0 / s).astype(np.float32)
+    rec = _true_records(x.astype(np.float32), recip32[group])
+    bad = rec.copy()
+    bad[10, 1] = _ext_key(np.float32(1e9), 3)                     # stale value
+    bad[11, 0] = _ext_key(np.float32(-1e9), 5)
+    bad[12, 1] = (bad[12, 1] & ~np.int64(0xFFFFFFFF)) | 17       # right value, wrong column
+    bad[13] = [-1, 0]                                            # never written (init records)
+    bad[14, 1] = (bad[14, 1] & ~np.int64(0xFFFFFFFF)) | (d + 5)  # column out of range
+    xd = torch.from_numpy(x).to(cuda).bfloat16()
+    sd = torch.from_numpy(s).to(cuda)
+    gd = torch.from_numpy(group).to(cuda)
+    want = M.quantize_rows_grouped(x.astype(np.float64), group, s)
+    for records in (rec, bad):
+        r = ops.act_quant(xd, smooth=sd, row_group=gd, row_ext=torch.from_numpy(records).to(cuda))
+        for got, exp in zip((r["codes"], r["scale"], r["zp"], r["rowsum"]), want):
+            np.testing.assert_array_equal(got.cpu().numpy(), exp)
+
+
+def test_swiglu_row_ext_feeds_k1(cuda):
+    """The grouped SwiGLU epilogue's extreme records of h * RN32(1/s2) match
+    the stored bf16 h, and K1 fed those records equals K1 without them."""
+    rng = np.random.default_rng(22)
+    E, F, K = 3, 512, 256
+    counts = np.array([300, 0, 211])
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    Mt = int(offs[-1])
+    a = _rand_operand(rng, Mt, K)
+    w = _rand_operand(rng, E * 2 * F, K)
+    s2 = _smooth(rng, E, F)
+    s2d = torch.from_numpy(s2).to(cuda)
+    recip, recip32 = ops.reciprocal(s2d, with_f32=True)
+    od = torch.from_numpy(offs).to(cuda)
+    ext = torch.empty((Mt, 2), dtype=torch.int64, device=cuda)
+    h = ops.w8a8_gemm(_dev_operand(cuda, *a), _dev_operand(cuda, *w), epilogue=L.EPI_SWIGLU,
+                      out_dtype=torch.bfloat16, group_offsets=od, num_groups=E, n_per_group=2 * F,
+                      next_smooth_recip_f32=recip32, row_ext=ext)
+    group = np.repeat(np.arange(E), counts).astype(np.int32)
+    xs = h.float().cpu().numpy() * recip32.cpu().numpy()[group]
+    e = ext.cpu().numpy().view(np.uint64)
+    r = np.arange(Mt)
+    want = _true_records(h.float().cpu().numpy(), recip32.cpu().numpy()[group]).view(np.uint64)
+    np.testing.assert_array_equal(e >> np.uint64(32), want >> np.uint64(32))     # extreme values
+    cols = (e & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    np.testing.assert_array_equal(xs[r, cols[:, 0]], xs.min(1))                  # columns hold them
+    np.testing.assert_array_equal(xs[r, cols[:, 1]], xs.max(1))
+    gd = torch.from_numpy(group).to(cuda)
+    with_ext = ops.act_quant(h, smooth=s2d, smooth_recip=recip, smooth_recip_f32=recip32, row_group=gd,
+                             row_ext=ext)
+    plain = ops.act_quant(h, smooth=s2d, row_group=gd)
+    for k in ("codes", "scale", "zp", "rowsum"):
+        assert torch.equal(with_ext[k], plain[k]), k
+
+
 # ── K2 / K5 ──────────────────────────────────────────────────────────────
 def _rand_operand(rng, rows, K, zp_lo=0, zp_hi=255):
     codes = rng.integers(0, 256, size=(rows, K)).astype(np.uint8)
