@@ -249,8 +249,117 @@ __device__ __forceinline__ double exact_at(const __nv_bfloat16* row, const float
   return srow ? div_rcp((double)xf, srow[j], rrow[j]) : (double)xf;
 }
 
-template <bool GIVEN>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+
+// ── 3-input min/max (FMNMX3) ───────────────────────────────────────────────
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// NaN-propagating max of |a|, |b|, |c|
+__device__ __forceinline__ float fmax3_abs_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(fabsf(a)), "f"(fabsf(b)), "f"(fabsf(c)));
+  return d;
+}
+__device__ __forceinline__ float max8(const float (&v)[8]) {
+  return fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
+}
+__device__ __forceinline__ float min8(const float (&v)[8]) {
+  return fmin3(fmin3(v[0], v[1], v[2]), fmin3(v[3], v[4], v[5]), fminf(v[6], v[7]));
+}
+
+// ── fast 8-bit encode of one row (asymmetric, extremes at codes <= 0 / >= 255)
+// t = RN(xs * rsc + (1.5*2^23 + zp)) holds round(p) + zp in its low mantissa
+// bits (p = xs * rsc exact inside the FMA); d = RN(p - round(p)). A vector
+// of 8 takes the fast path when every code is in [2, 253] and every |d| is
+// below 0.5 - 2^-12: those codes equal the float64 reference's (|p| <= 256
+// there, so p is within 2^-14 of the reference quotient). Everything else —
+// clipping, rounding-boundary cases, non-finite values and the elements
+// that could be row extremes (codes <= 1 / >= 254) — goes out of line.
+constexpr float kMagicF = 12582912.0f;
+constexpr float kFastTlo = 12582914.0f;          // code 2
+constexpr float kFastThi = 12583165.0f;          // code 253
+constexpr float kFastThr = 0.499755859375f;      // 0.5 - 2^-12
+
+struct FastRow {
+  double scale, rscale;
+  float rsc, magic;
+  float cand_max, cand_min;  // xs >= cand_max (<= cand_min) may be an exact extreme
+  int zp;
+};
+
+// Rare vectors: generic float32 encode (clip, exact float64 redo) plus the
+// count of possible-extreme elements. Returns (codes, cnt_max | cnt_min << 16).
+__device__ __noinline__ uint4 slow_vec8(uint4 u, const float* tab, int64_t c, const double* srow, const double* rrow,
+                                        FastRow f) {
+  float xs[8];
+  smooth8(u, tab, c, xs);
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) cnt += (uint32_t)(xs[e] >= f.cand_max) + ((uint32_t)(xs[e] <= f.cand_min) << 16);
+  RowEncoder enc(AffineParams{f.scale, f.rscale, f.zp}, 0.0, 0.0, 8, false);
+  enc.packed = false;
+  int sum = 0;
+  const uint2 out = enc.encode8(u, xs, c, srow, rrow, sum);
+  return make_uint4(out.x, out.y, cnt, 0u);
+}
+
+__device__ __forceinline__ uint32_t low_bytes4(float a, float b, float c, float d) {
+  const uint32_t ab = __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040);
+  const uint32_t cd = __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040);
+  return __byte_perm(ab, cd, 0x5410);
+}
+
+// Fallback for a whole row: float64 extremes over every element that can
+// reach them (pass B), then the generic encode (pass C). Used when the
+// speculative extremes fail their check, for symmetric / non-8-bit codes
+// and for rows outside the fast envelope.
+__device__ __noinline__ int fallback_row(const uint4* src, int64_t nvec, int lane, const float* tab,
+                                         const double* srow, const double* rrow, float lb_max, float ub_min,
+                                         bool exact_all, int bits, int sym, uint2* dst, AffineParams* out) {
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+    float xs[8];
+    smooth8(u, tab, c, xs);
+    uint32_t mmax = 0, mmin = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      mmax |= (uint32_t)(!(xs[e] + err_bound(xs[e]) < lb_max)) << e;
+      mmin |= (uint32_t)(!(xs[e] - err_bound(xs[e]) > ub_min)) << e;
+    }
+    if (mmax | mmin) {
+      const double2 e2 = exact_extremes8(u, srow, rrow, c, mmax, mmin);
+      mn = fmin(mn, e2.x);
+      mx = fmax(mx, e2.y);
+    }
+  });
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const AffineParams p = affine_params(mn, mx, bits, sym);
+  const RowEncoder enc(p, mn, mx, bits, exact_all);
+  int sum = 0;
+  for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+    float xs[8];
+    smooth8(u, tab, c, xs);
+    __stcs(dst + c, enc.encode8(u, xs, c, srow, rrow, sum));
+  });
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  *out = p;
+  return sum;
+}
+
+template <bool GIVEN, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
     act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
                           int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                           int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
@@ -261,15 +370,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
   const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
-  for (int64_t r = r_lo + warp; r < r_hi; r += kWarpsPerCta) {
+  for (int64_t r = r_lo + warp; r < r_hi; r += WARPS) {
     const RowView rv = row_view(a, r);
     const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + rv.off;
     const uint4* src = reinterpret_cast<const uint4*>(row);
     const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
     const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
     const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
+    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
 
-    // records of the float32 extremes: from the producer, or pass A
+    // (value, column) records of the float32 extremes: producer's, or pass A
     RowExt rec;
     if (GIVEN) {
       const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
@@ -281,10 +391,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
       for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
         float xs[8];
         smooth8(u, tab, c, xs);
+        const float vmax = max8(xs), vmin = min8(xs);
+        if (vmax > tmax) {
+          int j = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (xs[e] > tmax) { tmax = xs[e]; imax = c * 8 + e; }
-          if (xs[e] < tmin) { tmin = xs[e]; imin = c * 8 + e; }
+          for (int e = 7; e >= 0; --e) j = xs[e] == vmax ? e : j;
+          tmax = vmax;
+          imax = c * 8 + j;
+        }
+        if (vmin < tmin) {
+          int j = 0;
+#pragma unroll
+          for (int e = 7; e >= 0; --e) j = xs[e] == vmin ? e : j;
+          tmin = vmin;
+          imin = c * 8 + j;
         }
       });
       warp_argmax(tmax, imax);
@@ -292,6 +412,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
       rec = RowExt{tmax, tmin, imax, imin};
     }
     const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m)) || rec.cM >= a.cols || rec.cm >= a.cols;
+
     // speculative exact extremes: the recorded elements (verified below)
     bool spec = !exact_all;
     double mn = DBL_MAX, mx = -DBL_MAX;
@@ -303,77 +424,69 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
     // (the max is >= lb_max, the min <= ub_min); an inconsistent one bounds nothing
     const float lb_max = spec ? rec.M - err_bound(rec.M) : -FLT_MAX;
     const float ub_min = spec ? rec.m + err_bound(rec.m) : FLT_MAX;
+
+    AffineParams p{};
     int sum = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      if (!spec) {
-        // pass B: exact float64 extremes over every element that can reach them
-        mn = DBL_MAX;
-        mx = -DBL_MAX;
+    bool done = false;
+    if (spec && bits == 8 && !sym) {
+      p = affine_params(mn, mx, bits, sym);
+      const double hc = __dadd_rn(rha(div_rcp(mx, p.scale, p.rscale)), (double)p.zp);
+      const double lc = __dadd_rn(rha(div_rcp(mn, p.scale, p.rscale)), (double)p.zp);
+      if (hc >= 255.0 && lc <= 0.0) {
+        FastRow f;
+        f.scale = p.scale;
+        f.rscale = p.rscale;
+        f.zp = p.zp;
+        f.rsc = __double2float_rn(p.rscale);
+        f.magic = kMagicF + (float)p.zp;
+        f.cand_max = rec.M - 3.f * fabsf(rec.M) * kRelErr - 2.350988701644575e-38f;
+        f.cand_min = rec.m + 3.f * fabsf(rec.m) * kRelErr + 2.350988701644575e-38f;
+        const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
+        uint32_t cnt = 0;
         for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
           float xs[8];
           smooth8(u, tab, c, xs);
-          uint32_t mmax = 0, mmin = 0;
+          float t[8], d[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            mmax |= (uint32_t)(xs[e] + err_bound(xs[e]) >= lb_max) << e;
-            mmin |= (uint32_t)(xs[e] - err_bound(xs[e]) <= ub_min) << e;
+          for (int e = 0; e < 8; e += 2) {
+            const float2 x2 = make_float2(xs[e], xs[e + 1]);
+            const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
+            const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
+            const float2 d2 = __ffma2_rn(x2, rsc2, nr);
+            t[e] = t2.x;
+            t[e + 1] = t2.y;
+            d[e] = d2.x;
+            d[e + 1] = d2.y;
           }
-          if (mmax | mmin) {
-            const double2 e2 = exact_extremes8(u, srow, rrow, c, mmax, mmin);
-            mn = fmin(mn, e2.x);
-            mx = fmax(mx, e2.y);
+          const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
+                                         fmax3_abs_nan(d[6], d[7], 0.f));
+          uint2 out;
+          if (max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr) {
+            out = make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
+          } else {
+            const uint4 s = slow_vec8(u, tab, c, srow, rrow, f);
+            out = make_uint2(s.x, s.y);
+            cnt += s.z;
           }
+          sum += bytesum(out);
+          __stcs(dst + c, out);
         });
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         }
+        // exactly one possible extreme on each side: the recorded elements
+        // are the exact extremes and the codes stand
+        done = cnt == 0x10001u;
       }
-      const AffineParams p = affine_params(mn, mx, bits, sym);
-      const RowEncoder enc(p, mn, mx, bits, exact_all);
-      // pass C: encode; while speculating also count the elements that could
-      // be extremes (must be exactly the two recorded ones)
-      sum = 0;
-      int cnt_max = 0, cnt_min = 0;
-      uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
-      const bool count = spec;
-      const float2 K2 = make_float2(kRelErr, kRelErr), A2 = make_float2(kAbsErr, kAbsErr);
-      for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
-        float xs[8];
-        smooth8(u, tab, c, xs);
-        if (count) {
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float2 eb = __ffma2_rn(make_float2(fabsf(xs[e]), fabsf(xs[e + 1])), K2, A2);
-            const float2 hi = __fadd2_rn(make_float2(xs[e], xs[e + 1]), eb);
-            const float2 lo = __fadd2_rn(make_float2(xs[e], xs[e + 1]), make_float2(-eb.x, -eb.y));
-            cnt_max += (hi.x >= lb_max) + (hi.y >= lb_max);
-            cnt_min += (lo.x <= ub_min) + (lo.y <= ub_min);
-          }
-        }
-        __stcs(dst + c, enc.encode8(u, xs, c, srow, rrow, sum));
-      });
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (count) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          cnt_max += __shfl_xor_sync(0xffffffffu, cnt_max, o);
-          cnt_min += __shfl_xor_sync(0xffffffffu, cnt_min, o);
-        }
-        if (cnt_max != 1 || cnt_min != 1) {  // another element could be an extreme: redo exactly
-          spec = false;
-          continue;
-        }
-      }
-      if (lane == 0) {
-        if (rowsum) rowsum[r] = sum;
-        scale[r] = p.scale;
-        if (scale_f32) scale_f32[r] = (float)p.scale;
-        zp[r] = p.zp;
-      }
-      break;
+    }
+    if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
+    if (lane == 0) {
+      if (rowsum) rowsum[r] = sum;
+      scale[r] = p.scale;
+      if (scale_f32) scale_f32[r] = (float)p.scale;
+      zp[r] = p.zp;
     }
   }
 }
@@ -385,17 +498,31 @@ static bool eligible(const RowArgs& a, const float* rs32, uint8_t* codes, int64_
          (a.sm.mode == MOE_SMOOTH_NONE || (smooth && a.sm.rs && rs32));
 }
 
+template <bool GIVEN, int WARPS, int MINB>
+static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
+                       uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum,
+                       cudaStream_t s) {
+  // contiguous row ranges, MINB+ CTAs per SM
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + WARPS - 1) / WARPS,
+                                                              (MINB + 2) * (int64_t)num_sms()));
+  const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
+  const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
+  act_quant_warp_kernel<GIVEN, WARPS, MINB><<<(unsigned)nblk, WARPS * 32, 0, s>>>(
+      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+}
+
 template <bool GIVEN>
 static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                               int32_t* rowsum, cudaStream_t s) {
-  // contiguous row ranges, ~4 CTAs (64 warps) per SM
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + kWarpsPerCta - 1) / kWarpsPerCta,
-                                                              4 * (int64_t)num_sms()));
-  const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
-  const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
-  act_quant_warp_kernel<GIVEN><<<(unsigned)nblk, kWarpsPerCta * 32, 0, s>>>(
-      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+  const char* env = getenv("MOE_B200_K1_CFG");
+  const int cfg = env ? atoi(env) : 0;
+  switch (cfg) {
+    case 1: launch_cfg<GIVEN, 16, 1>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
+    case 2: launch_cfg<GIVEN, 8, 3>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
+    case 3: launch_cfg<GIVEN, 8, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
+    default: launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+  }
   count_launch();
   return cudaGetLastError();
 }
