@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline time budget")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="use the expert-parallel runtime even at N=1 (validation)")
+    ap.add_argument("--ep-stage1", type=int, default=1, help="EP (N>1): plan_two_stage path residents per layer")
+    ap.add_argument("--ep-stage2", type=int, default=1, help="EP (N>1): frequency supplement per layer")
     return ap.parse_args()
 
 
@@ -217,6 +220,20 @@ def main() -> None:
     x_host = torch.from_numpy(x_np).to(torch.bfloat16).pin_memory()
     x_dev = x_host.cuda()
     torch.cuda.synchronize()
+    ep_info = None
+    model = layer
+    if world > 1 or args.ep:
+        # expert parallelism: plan_two_stage over the GPU-measured routing of
+        # all ranks -> replicated residents, the rest bin-packed (ep.py)
+        from paper_2508_07329_b200.ep import CudaExpertBackend, ExpertParallelMoE, plan_placement
+        placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
+        model = ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank)),
+                                  placement)
+        counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
+        ep_info = {"replicated": list(placement.replicated), "owner": list(placement.owner),
+                   "local_fraction_est": placement.local_fraction(counts)}
+        del layer.w13, layer.w2            # this rank keeps only its local experts' weights
+        torch.cuda.empty_cache()
 
     def barrier():
         if world > 1:
@@ -225,7 +242,7 @@ def main() -> None:
     # ---- device-resident timing --------------------------------------------
     clocks = Clocks(local)
     for _ in range(args.warmup):
-        layer.forward(x_dev)
+        model.forward(x_dev)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -236,7 +253,7 @@ def main() -> None:
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
-        layer.forward(x_dev, timer=timer)
+        model.forward(x_dev, timer=timer)
     t1.record()
     torch.cuda.synchronize()
     launches = lib.moe_launch_count() - launches0
@@ -256,12 +273,12 @@ def main() -> None:
     if not args.no_e2e:
         out_host = torch.empty((T, D), dtype=torch.bfloat16, pin_memory=True)
         for _ in range(max(1, args.warmup)):
-            layer.forward_host(x_host, out_host)
+            model.forward_host(x_host, out_host)
         torch.cuda.synchronize()
         barrier()
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            layer.forward_host(x_host, out_host)
+            model.forward_host(x_host, out_host)
         torch.cuda.synchronize()
         e2e_ms = 1000.0 * (time.perf_counter() - w0) / args.steps
         if world > 1:
@@ -314,12 +331,14 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
-                       "top_k": TOPK, "d": D, "ffn": F, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "top_k": TOPK, "d": D, "ffn": F, "parallelism": f"ep{world}" if ep_info is not None else "1gpu",
                        "l2": "inputs larger than L2 (x 134 MB, expert weights 1.41 GB per layer)"},
             "int8_tops_layer": value / world * OPS_PER_TOKEN / 1e12,
             "stages_ms": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches,
         }
+        if ep_info is not None:
+            line["config"]["expert_placement"] = ep_info
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

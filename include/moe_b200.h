@@ -223,6 +223,25 @@ moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, int64_t ldw, 
                             uint8_t* codes, int64_t ldc, void* err_ws, int64_t err_ws_bytes,
                             moe_stream_t stream);
 
+/* ---- expert-parallel plumbing (no reference counterpart:
+ * the reference has no forward, placement.py:1-256 only plans residency) --
+ * route_keys: keys[i] = dest_rank[topk_idx[i]] * E + topk_idx[i], the sort
+ *   key of moe_route_permute(E' = world * E) that makes each destination's
+ *   rows contiguous and expert-sorted within it.
+ * gather_rows: dst row r = src row index[r] (index NULL -> identity), rows
+ *   of row_bytes bytes (16-byte vectors when aligned).
+ * ep_pack_params: params[n, 4] int32 = (scale_f32 bits, zp, rowsum, weight
+ *   bits; weight NULL -> 1.0f), the per-row sidecar of dispatched codes.
+ * ep_unpack_params: SoA scale_f32/zp/rowsum/weight of params[index[r]]. */
+moe_status moe_route_keys(const int32_t* topk_idx, int64_t n, const int32_t* dest_rank, int E, int32_t* keys,
+                          moe_stream_t stream);
+moe_status moe_gather_rows(const void* src, int64_t src_ld_bytes, const int32_t* index, int64_t n,
+                           int64_t row_bytes, void* dst, int64_t dst_ld_bytes, moe_stream_t stream);
+moe_status moe_ep_pack_params(const float* scale_f32, const int32_t* zp, const int32_t* rowsum,
+                              const float* weight, int64_t n, int32_t* params, moe_stream_t stream);
+moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, float* scale_f32,
+                                int32_t* zp, int32_t* rowsum, float* weight, moe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

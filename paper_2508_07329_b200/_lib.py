@@ -50,6 +50,10 @@ _SIGS = {
     "moe_hessian_finalize": (_I, [_P, _I64, _D, _P, _P]),
     "moe_gptq_workspace": (_I64, [_I64, _I64]),
     "moe_gptq_columns": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P, _I64, _P, _I64, _P]),
+    "moe_route_keys": (_I, [_P, _I64, _P, _I, _P, _P]),
+    "moe_gather_rows": (_I, [_P, _I64, _P, _I64, _I64, _P, _I64, _P]),
+    "moe_ep_pack_params": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
+    "moe_ep_unpack_params": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

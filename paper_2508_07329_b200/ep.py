@@ -1,0 +1,395 @@
+"""Expert-parallel MoE forward: one process per GPU, NCCL all-to-all
+(SURVEY.md §8e).
+
+Tokens are data-parallel (each rank routes its own tokens); experts are
+placed per layer. The reference only *plans* residency (placement.py:125-176,
+evaluate_plan :179-208) for a single device; here the plan's residents become
+experts REPLICATED on every rank (always served locally, no traffic) and the
+remaining experts are SHARDED by greedy bin-packing on routing counts, so
+``evaluate_plan``'s hit rate is exactly the fraction of activations that
+never leave their home GPU.
+
+One forward on rank r:
+
+  1. K3 router on the local tokens -> (idx, w) over all E experts
+  2. route_keys: key = dest_rank[e] * E + e, and route_permute over W*E keys:
+     rows for each destination are contiguous, expert-sorted within it
+  3. K1 on the sender (per-expert smoothing of the destination expert) ->
+     u8 codes [n, d] + an int32 [n, 4] sidecar (scale_f32, zp, rowsum, w):
+     dispatch moves d + 16 bytes per row instead of 2d
+  4. counts [W, E] all-to-all, then the codes / sidecar all_to_all_v
+  5. receiver: gather rows into expert-contiguous order, grouped GEMM13 +
+     SwiGLU (+ extreme records), K1 on h, grouped GEMM2 (x routing weight),
+     gather back into receive order
+  6. bf16 rows all_to_all_v back to their home rank, K6 combine
+
+The per-row arithmetic is the single-GPU path's (same K1 rows, exact int32
+accumulators, same epilogues), so an EP forward is bit-identical to
+``MoELayer.forward`` on the same tokens (tests/test_gpu_ep.py).
+
+The compute is behind a small backend interface (``CudaExpertBackend`` is the
+product; tests plug a float64 CPU backend into the same runtime to check the
+host logic and the gloo exchange at world size 2).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import ops
+from .placement import PlacementPlan
+from .trace import ExpertFreq
+
+
+# ── placement ─────────────────────────────────────────────────────────────
+@dataclass(frozen=True)
+class ExpertPlacement:
+    """Where each expert of one layer lives in a world of ``world`` ranks.
+
+    replicated: experts held by every rank (served where the token is).
+    owner[e]:   rank holding sharded expert e, -1 for replicated experts."""
+    world: int
+    experts: int
+    replicated: tuple
+    owner: tuple
+
+    def __post_init__(self):
+        if self.world < 1 or self.experts < 1:
+            raise ValueError("world and experts must be >= 1")
+        if len(self.owner) != self.experts:
+            raise ValueError(f"owner has {len(self.owner)} entries for {self.experts} experts")
+        rep = set(self.replicated)
+        for e, o in enumerate(self.owner):
+            if e in rep:
+                if o != -1:
+                    raise ValueError(f"replicated expert {e} must have owner -1")
+            elif not 0 <= o < self.world:
+                raise ValueError(f"expert {e} has owner {o} outside [0, {self.world})")
+        if any(not 0 <= e < self.experts for e in rep):
+            raise ValueError("replicated expert id out of range")
+
+    @classmethod
+    def sharded(cls, experts: int, world: int) -> "ExpertPlacement":
+        """Contiguous blocks, no replication (expert e -> rank e * W // E)."""
+        return cls(world, experts, (), tuple(e * world // experts for e in range(experts)))
+
+    @classmethod
+    def from_counts(cls, counts, world: int, replicated=()) -> "ExpertPlacement":
+        """Greedy bin-packing of the non-replicated experts by routed-token
+        counts: hottest first (ties -> lower id) onto the least-loaded rank
+        (ties -> lower rank). Replicated experts load every rank equally
+        (each serves its own tokens), so they do not enter the packing."""
+        counts = np.asarray(counts, dtype=np.int64).reshape(-1)
+        E = counts.size
+        rep = tuple(sorted(set(int(e) for e in replicated)))
+        owner = [-1] * E
+        load = np.zeros(world, dtype=np.int64)
+        order = np.lexsort((np.arange(E), -counts))
+        for e in order:
+            e = int(e)
+            if e in rep:
+                continue
+            r = int(np.argmin(load))          # first minimum -> lowest rank on ties
+            owner[e] = r
+            load[r] += counts[e]
+        return cls(world, E, rep, tuple(owner))
+
+    @classmethod
+    def from_plan(cls, plan: PlacementPlan, layer: int, freq: ExpertFreq, world: int) -> "ExpertPlacement":
+        """Residents of ``plan`` (plan_two_stage / plan_frequency / plan_path)
+        at ``layer`` are replicated; the rest are bin-packed on freq counts."""
+        return cls.from_counts(freq.counts[layer], world, plan.residents[layer])
+
+    def dest_table(self, rank: int) -> np.ndarray:
+        """dest[e] = the rank that serves expert e for tokens of ``rank``."""
+        return np.array([rank if o == -1 else o for o in self.owner], dtype=np.int32)
+
+    def local_experts(self, rank: int) -> tuple:
+        return tuple(e for e in range(self.experts) if self.owner[e] == -1 or self.owner[e] == rank)
+
+    def local_fraction(self, counts) -> float:
+        """Fraction of activations served without leaving the home rank, for
+        tokens spread evenly over ranks: replicated experts always, a sharded
+        expert for the 1/W of tokens that live on its owner."""
+        counts = np.asarray(counts, dtype=np.float64).reshape(-1)
+        tot = counts.sum()
+        if tot == 0:
+            return 1.0
+        rep = np.zeros(self.experts, dtype=bool)
+        rep[list(self.replicated)] = True
+        return float((counts[rep].sum() + counts[~rep].sum() / self.world) / tot)
+
+
+# ── exchange ──────────────────────────────────────────────────────────────
+class TorchDistExchange:
+    """all_to_all over a torch.distributed process group (NCCL on GPUs, gloo
+    on CPU). world == 1 without an initialised group is the identity."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.dist = torch.distributed if torch.distributed.is_initialized() else None
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+
+    def counts(self, send: np.ndarray) -> np.ndarray:
+        """send [W, E] (rows this rank sends to each rank, per expert) ->
+        recv [W, E] (rows each rank sends to this one)."""
+        if self.world == 1:
+            return send.copy()
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        s = torch.as_tensor(send, dtype=torch.int64, device=dev).contiguous()
+        r = torch.empty_like(s)
+        self.dist.all_to_all_single(r, s, group=self.group)
+        return r.cpu().numpy()
+
+    def rows(self, t: torch.Tensor, send_splits: list, recv_splits: list) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        out = t.new_empty((int(sum(recv_splits)),) + tuple(t.shape[1:]))
+        self.dist.all_to_all_single(out, t.contiguous(), [int(v) for v in recv_splits],
+                                    [int(v) for v in send_splits], group=self.group)
+        return out
+
+
+def regroup_index(recv_counts: np.ndarray, local: tuple) -> tuple[np.ndarray, np.ndarray]:
+    """Received rows arrive source-major, expert-sorted within each source
+    block. Returns the gather index that makes them expert-contiguous (local
+    experts ascending, sources ascending within an expert) and the per-local-
+    expert row counts."""
+    recv_counts = np.asarray(recv_counts, dtype=np.int64)
+    W, E = recv_counts.shape
+    stray = np.ones(E, dtype=bool)
+    stray[list(local)] = False
+    if recv_counts[:, stray].any():
+        raise RuntimeError("received rows for an expert this rank does not hold (placement mismatch)")
+    block = np.concatenate([[0], np.cumsum(recv_counts.sum(axis=1))])
+    start = block[:-1, None] + np.concatenate([np.zeros((W, 1), np.int64), np.cumsum(recv_counts, axis=1)[:, :-1]],
+                                              axis=1)
+    pieces = [np.arange(start[s, e], start[s, e] + recv_counts[s, e]) for e in local for s in range(W)]
+    index = np.concatenate(pieces).astype(np.int32) if pieces else np.zeros(0, np.int32)
+    return index, recv_counts[:, list(local)].sum(axis=0)
+
+
+@dataclass
+class DispatchState:
+    T: int
+    perm: dict
+    payload: list
+    send_counts: np.ndarray          # [W, E]
+    send_splits: list = field(default_factory=list)
+
+
+class ExpertParallelMoE:
+    """One rank's view of an expert-parallel MoE layer."""
+
+    def __init__(self, backend, placement: ExpertPlacement, exchange=None, rank: int | None = None):
+        self.be = backend
+        self.pl = placement
+        self.ex = exchange if exchange is not None else TorchDistExchange()
+        self.rank = self.ex.rank if rank is None else rank
+        if getattr(self.ex, "world", placement.world) != placement.world:
+            raise ValueError(f"placement is for {placement.world} ranks, the group has {self.ex.world}")
+        self.local = placement.local_experts(self.rank)
+        if tuple(backend.local_experts) != self.local:
+            raise ValueError(f"backend holds experts {backend.local_experts}, placement gives {self.local}")
+        self.dest = backend.to_index_tensor(placement.dest_table(self.rank))
+
+    # phases (kept separate so a single process can drive several ranks: run_loopback)
+    def dispatch(self, x: torch.Tensor) -> DispatchState:
+        W, E = self.pl.world, self.pl.experts
+        T = x.shape[0]
+        idx, w = self.be.route(x)
+        keys = self.be.route_keys(idx, self.dest, E)
+        perm = self.be.permute(keys, w, W * E)
+        payload = self.be.quantize_pack(x, perm, E)
+        off = self.be.to_host(perm["offsets"]).astype(np.int64)
+        send_counts = np.diff(off).reshape(W, E)
+        return DispatchState(T, perm, payload, send_counts, send_counts.sum(axis=1).tolist())
+
+    def compute(self, recv_payload: list, recv_counts: np.ndarray, mark=None) -> torch.Tensor:
+        index, group_counts = regroup_index(recv_counts, self.local)
+        return self.be.experts(recv_payload, index, group_counts, mark or (lambda _n: None))
+
+    def finish(self, st: DispatchState, y_home: torch.Tensor) -> torch.Tensor:
+        return self.be.combine(y_home, st.perm, st.T)
+
+    def forward(self, x: torch.Tensor, timer=None) -> torch.Tensor:
+        """x [T, d] on this rank's device -> [T, d]. ``timer`` (optional) gets
+        ``mark(stage)`` calls between phases (CUDA events)."""
+        mark = timer.mark if timer is not None else (lambda _n: None)
+        mark("start")
+        st = self.dispatch(x)
+        mark("dispatch_prepare")
+        recv_counts = self.ex.counts(st.send_counts)
+        recv_splits = recv_counts.sum(axis=1).tolist()
+        recv = [self.ex.rows(p, st.send_splits, recv_splits) for p in st.payload]
+        mark("all_to_all_dispatch")
+        y_recv = self.compute(recv, recv_counts, mark)
+        y_home = self.ex.rows(y_recv, recv_splits, st.send_splits)
+        mark("all_to_all_combine")
+        out = self.finish(st, y_home)
+        mark("combine")
+        return out
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        """Pinned host tokens in, host tokens out (the end-to-end call)."""
+        x = x_host.to(self.be.device, non_blocking=True)
+        y = self.forward(x)
+        if out_host is None:
+            out_host = torch.empty(tuple(y.shape), dtype=y.dtype, pin_memory=True)
+        out_host.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out_host
+
+
+def run_loopback(ranks: list, xs: list) -> list:
+    """Drive W ``ExpertParallelMoE`` instances (one per simulated rank) in one
+    process, performing the two all-to-all exchanges by concatenation. Used
+    to exercise the multi-rank data layout (several sources per receiver,
+    remote experts) on a single device; the kernels are the same, only the
+    transport differs. Ranks run one after another, nothing waits on a peer."""
+    W = len(ranks)
+    sts = [m.dispatch(x) for m, x in zip(ranks, xs)]
+    parts = [[list(torch.split(p, s.send_splits)) for p in s.payload] for s in sts]
+    y_parts = []
+    for r, m in enumerate(ranks):
+        recv_counts = np.stack([sts[s].send_counts[r] for s in range(W)])
+        recv = [torch.cat([parts[s][i][r] for s in range(W)]) for i in range(len(sts[0].payload))]
+        y = m.compute(recv, recv_counts)
+        y_parts.append(list(torch.split(y, recv_counts.sum(axis=1).tolist())))
+    return [ranks[s].finish(sts[s], torch.cat([y_parts[r][s] for r in range(W)])) for s in range(W)]
+
+
+# ── the B200 backend ──────────────────────────────────────────────────────
+class CudaExpertBackend:
+    """Expert compute of one rank on its GPU: the same kernels as
+    ``MoELayer.forward`` (K3, K4, K1, K5, K6) plus the EP gather/pack
+    kernels. Holds the full router and the per-expert x-side smoothing of
+    all E experts (the sender quantizes for the destination expert) and the
+    weights of the local experts only."""
+
+    def __init__(self, gate_weight, experts: list[dict], local_experts, top_k: int = 2, gate_bias=None,
+                 out_dtype=torch.bfloat16):
+        from .moe import MoELayer
+
+        self.local_experts = tuple(local_experts)
+        self.E = len(experts)
+        self.k = top_k
+        self.out_dtype = out_dtype
+        self.gate_w = torch.as_tensor(gate_weight, dtype=torch.float32).cuda().contiguous()
+        self.gate_b = None if gate_bias is None else torch.as_tensor(gate_bias, dtype=torch.float32).cuda()
+        s13 = torch.stack([torch.as_tensor(np.asarray(_np(e["s13"])), dtype=torch.float64) for e in experts]).cuda()
+        self.s13 = s13.contiguous()
+        self.s13_recip, self.s13_recip32 = ops.reciprocal(self.s13, with_f32=True)
+        self.bank = (MoELayer(gate_weight, [experts[e] for e in self.local_experts], top_k=1, out_dtype=out_dtype)
+                     if self.local_experts else None)
+        self.d = self.s13.shape[1]
+        self.device = self.s13.device
+        self._tiled = {}
+
+    @classmethod
+    def from_layer_spec(cls, layer, local_experts):
+        """Slice a full single-GPU ``MoELayer`` (its host expert list)."""
+        return cls(layer.gate_w.cpu().numpy(), layer.host_experts, local_experts, top_k=layer.k,
+                   gate_bias=None if layer.gate_b is None else layer.gate_b.cpu().numpy(), out_dtype=layer.out_dtype)
+
+    # host <-> device helpers used by the runtime
+    @staticmethod
+    def to_index_tensor(a: np.ndarray) -> torch.Tensor:
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+    @staticmethod
+    def to_host(t: torch.Tensor) -> np.ndarray:
+        return t.cpu().numpy()
+
+    def _smooth_tables(self, W: int):
+        # row_group of a dispatched row is its sort key dest * E + e: tile the
+        # per-expert tables W times so key indexes them directly
+        if W not in self._tiled:
+            self._tiled[W] = tuple(t.repeat(W, 1).contiguous() for t in (self.s13, self.s13_recip, self.s13_recip32))
+        return self._tiled[W]
+
+    def route(self, x):
+        _, idx, w = ops.router_gate(x, self.gate_w, self.k, gate_bias=self.gate_b)
+        return idx, w
+
+    def route_keys(self, idx, dest, E):
+        return ops.route_keys(idx, dest, E)
+
+    def permute(self, keys, w, G):
+        return ops.route_permute(keys, w, G)
+
+    def quantize_pack(self, x, perm, E):
+        W = perm["offsets"].numel() // E if E else 1
+        s, sr, sr32 = self._smooth_tables(W)
+        n = perm["src_token"].numel()
+        a = ops.act_quant(x, smooth=s, smooth_recip=sr, smooth_recip_f32=sr32, row_group=perm["row_expert"],
+                          gather=perm["src_token"], rows=n)
+        return [a["codes"], ops.ep_pack_params(a, perm["row_weight"])]
+
+    def experts(self, recv: list, index: np.ndarray, group_counts: np.ndarray, mark=lambda _n: None) -> torch.Tensor:
+        codes_r, params_r = recv
+        n = int(index.size)
+        if n == 0:
+            return torch.empty((0, self.d), dtype=torch.bfloat16, device="cuda")
+        b = self.bank
+        G = len(self.local_experts)
+        idx = self.to_index_tensor(index)
+        prm = ops.ep_unpack_params(params_r, idx)
+        a1 = {"codes": ops.gather_rows(codes_r, idx), "scale_f32": prm["scale_f32"], "zp": prm["zp"],
+              "rowsum": prm["rowsum"]}
+        offs = self.to_index_tensor(np.concatenate([[0], np.cumsum(group_counts)]))
+        row_group = self.to_index_tensor(np.repeat(np.arange(G), group_counts))
+        fuse = b.d % 16 == 0 and b.d >= 128
+        ext = torch.empty((n, 2), dtype=torch.int64, device="cuda") if fuse else None
+        h = ops.w8a8_gemm(a1, b.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16, group_offsets=offs,
+                          num_groups=G, n_per_group=2 * b.F, next_smooth_recip_f32=b.s2_recip32 if fuse else None,
+                          row_ext=ext)
+        mark("gemm13_swiglu")
+        a2 = ops.act_quant(h, smooth=b.s2, smooth_recip=b.s2_recip, smooth_recip_f32=b.s2_recip32,
+                           row_group=row_group, row_ext=ext)
+        mark("quant_h")
+        y = ops.w8a8_gemm(a2, b.w2, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16, row_weight=prm["weight"],
+                          group_offsets=offs, num_groups=G, n_per_group=b.d)
+        mark("gemm2")
+        inv = np.empty_like(index)
+        inv[index] = np.arange(n, dtype=np.int32)
+        return ops.gather_rows(y, self.to_index_tensor(inv))
+
+    def combine(self, y_home, perm, T):
+        return ops.combine(y_home, perm["token_pos"], T, self.k, out_dtype=self.out_dtype)
+
+
+def plan_placement(idx: torch.Tensor, experts: int, top_k: int, world: int, top_k_per_layer: int = 1,
+                   supplement_k_per_layer: int = 1, group=None) -> ExpertPlacement:
+    """The paper's placement from GPU-measured routing of one layer: every
+    rank records its router output (RoutingStats, one histogram kernel),
+    the selections of all ranks are gathered, and plan_two_stage
+    (placement.py:125-176) over the global path statistics and expert
+    frequencies picks the replicated residents; the rest are bin-packed."""
+    from .placement import plan_two_stage
+    from .trace import RoutingStats, Trace, expert_freq, path_stats
+
+    st = RoutingStats(1, experts, top_k)
+    st.record(idx, 0)
+    events = st.to_trace().events
+    paths = [ev.path for ev in events]
+    if torch.distributed.is_initialized() and torch.distributed.get_world_size(group) > 1:
+        gathered = [None] * torch.distributed.get_world_size(group)
+        torch.distributed.all_gather_object(gathered, paths, group=group)
+        paths = [p for part in gathered for p in part]
+    from .trace import RoutingEvent, PHASE_PREFILL
+    trace = Trace(1, experts, top_k, [RoutingEvent(t, PHASE_PREFILL, p) for t, p in enumerate(paths)])
+    freq = expert_freq(trace)
+    plan = plan_two_stage(path_stats(trace), freq, top_k_per_layer, supplement_k_per_layer)
+    return ExpertPlacement.from_plan(plan, 0, freq, world)
+
+
+def _np(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)

@@ -254,3 +254,45 @@ def gptq_columns(w: torch.Tensor, U: torch.Tensor, scale: torch.Tensor, zp: torc
            L.ptr(scale.contiguous()), L.ptr(zp.contiguous()), bits, L.ptr(codes), codes.stride(0), L.ptr(ws), wsb,
            _s())
     return codes
+
+
+# ── expert-parallel plumbing ──────────────────────────────────────────────
+def route_keys(idx: torch.Tensor, dest_rank: torch.Tensor, E: int) -> torch.Tensor:
+    """keys = dest_rank[idx] * E + idx (sort keys grouping rows by destination rank, then expert)."""
+    idx = idx.contiguous()
+    keys = torch.empty_like(idx)
+    L.call("moe_route_keys", L.ptr(idx), idx.numel(), L.ptr(dest_rank.contiguous()), E, L.ptr(keys), _s())
+    return keys
+
+
+def gather_rows(src: torch.Tensor, index: torch.Tensor | None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[r] = src[index[r]] for a row-major 2-D tensor (any dtype)."""
+    src = _rowmajor(src, "src")
+    n = index.numel() if index is not None else src.shape[0]
+    o = out if out is not None else torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else o[0].numel() * o.element_size()
+    L.call("moe_gather_rows", L.ptr(src), src.stride(0) * src.element_size(),
+           L.ptr(index.contiguous() if index is not None else None), n, row_bytes, L.ptr(o),
+           o.stride(0) * o.element_size(), _s())
+    return o
+
+
+def ep_pack_params(a: dict, weight: torch.Tensor | None) -> torch.Tensor:
+    """[n, 4] int32 sidecar of dispatched rows: (scale_f32 bits, zp, rowsum, weight bits)."""
+    n = a["codes"].shape[0]
+    params = torch.empty((n, 4), dtype=torch.int32, device=a["codes"].device)
+    L.call("moe_ep_pack_params", L.ptr(a["scale_f32"]), L.ptr(a["zp"]), L.ptr(a["rowsum"]), L.ptr(weight), n,
+           L.ptr(params), _s())
+    return params
+
+
+def ep_unpack_params(params: torch.Tensor, index: torch.Tensor | None) -> dict:
+    n = index.numel() if index is not None else params.shape[0]
+    dev = params.device
+    out = {"scale_f32": torch.empty(n, dtype=torch.float32, device=dev),
+           "zp": torch.empty(n, dtype=torch.int32, device=dev),
+           "rowsum": torch.empty(n, dtype=torch.int32, device=dev),
+           "weight": torch.empty(n, dtype=torch.float32, device=dev)}
+    L.call("moe_ep_unpack_params", L.ptr(params.contiguous()), L.ptr(index), n, L.ptr(out["scale_f32"]),
+           L.ptr(out["zp"]), L.ptr(out["rowsum"]), L.ptr(out["weight"]), _s())
+    return out

@@ -1,0 +1,165 @@
+"""Expert-parallel runtime on CPU: placement, regrouping, the loopback
+driver and a real world-size-2 gloo all-to-all, with the float64 oracle
+backend; every rank's output must equal moe_ref.moe_forward on its tokens
+(bit-exact: the per-row arithmetic is identical and k = 2 sums commute)."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import moe_ref as M
+from paper_2508_07329_b200 import placement as P
+from paper_2508_07329_b200 import trace as TR
+from paper_2508_07329_b200.ep import ExpertParallelMoE, ExpertPlacement, regroup_index, run_loopback
+
+from .ep_oracle_backend import OracleBackend, random_experts
+
+E, D, F, K = 6, 32, 48, 2
+
+
+def _layer(seed=0):
+    rng = np.random.default_rng(seed)
+    experts = random_experts(rng, E, D, F)
+    wg = rng.normal(size=(E, D)) / np.sqrt(D)
+    wg[0] *= 3.0                                   # skewed routing: expert 0 hot
+    return wg, experts
+
+
+def _tokens(rng, T):
+    x = rng.normal(size=(T, D))
+    x[:, 3] *= 50.0
+    return x.astype(np.float32).astype(np.float64)
+
+
+# ── placement ──────────────────────────────────────────────────────────────
+def test_sharded_placement_blocks():
+    p = ExpertPlacement.sharded(8, 4)
+    assert p.owner == (0, 0, 1, 1, 2, 2, 3, 3)
+    assert p.local_experts(2) == (4, 5)
+    np.testing.assert_array_equal(p.dest_table(1), [0, 0, 1, 1, 2, 2, 3, 3])
+
+
+def test_bin_packing_hottest_first_least_loaded():
+    counts = [50, 10, 40, 40, 5, 30]
+    p = ExpertPlacement.from_counts(counts, 2)
+    # hottest first onto the least-loaded rank (ties -> lower rank):
+    # 0(50)->r0, 2(40)->r1, 3(40)->r1, 5(30)->r0, 1(10)->r0 (80 = 80), 4(5)->r1
+    assert p.owner == (0, 0, 1, 1, 1, 0)
+    loads = [sum(c for c, o in zip(counts, p.owner) if o == r) for r in range(2)]
+    assert loads == [90, 85]
+
+
+def test_replicated_experts_are_local_everywhere():
+    p = ExpertPlacement.from_counts([9, 1, 1, 9], 2, replicated=(0, 3))
+    assert p.owner[0] == -1 and p.owner[3] == -1
+    for r in range(2):
+        assert {0, 3} <= set(p.local_experts(r))
+        assert p.dest_table(r)[0] == r and p.dest_table(r)[3] == r
+    assert p.local_fraction([9, 1, 1, 9]) == pytest.approx((18 + 2 / 2) / 20)
+
+
+def test_placement_from_two_stage_plan():
+    cfg = TR.GenConfig(layers=2, experts_per_layer=E, top_k=2, n_prefill_tokens=60, n_decode_tokens=60,
+                      zipf_s=1.2, hot_path_prob=0.3, seed=3)
+    trace = TR.generate_trace(cfg)
+    stats, freq = TR.path_stats(trace), TR.expert_freq(trace)
+    plan = P.plan_two_stage(stats, freq, 1, 1)
+    for layer in range(2):
+        pl = ExpertPlacement.from_plan(plan, layer, freq, world=2)
+        assert set(pl.replicated) == set(plan.residents[layer])
+        rep = set(plan.residents[layer])
+        assert all((o == -1) == (e in rep) for e, o in enumerate(pl.owner))
+        # the local-serve fraction counts replicated activations fully
+        c = freq.counts[layer]
+        want = (c[list(rep)].sum() + (c.sum() - c[list(rep)].sum()) / 2) / c.sum()
+        assert pl.local_fraction(c) == pytest.approx(want)
+
+
+def test_placement_validation():
+    with pytest.raises(ValueError):
+        ExpertPlacement(2, 3, (), (0, 1))
+    with pytest.raises(ValueError):
+        ExpertPlacement(2, 2, (), (0, 2))
+    with pytest.raises(ValueError):
+        ExpertPlacement(2, 2, (0,), (0, 1))
+
+
+def test_regroup_index():
+    # 2 sources x 3 experts, this rank holds experts 0 and 2
+    rc = np.array([[2, 0, 1], [1, 0, 3]])
+    idx, g = regroup_index(rc, (0, 2))
+    # source blocks: s0 rows [0,1 (e0), 2 (e2)], s1 rows [3 (e0), 4,5,6 (e2)]
+    np.testing.assert_array_equal(idx, [0, 1, 3, 2, 4, 5, 6])
+    np.testing.assert_array_equal(g, [3, 4])
+    with pytest.raises(RuntimeError):
+        regroup_index(np.array([[0, 1, 0]]), (0, 2))
+
+
+# ── runtime with the oracle backend ───────────────────────────────────────
+def test_ep_single_rank_matches_moe_forward():
+    wg, experts = _layer(1)
+    x = _tokens(np.random.default_rng(2), 40)
+    pl = ExpertPlacement.sharded(E, 1)
+    m = ExpertParallelMoE(OracleBackend(wg, experts, pl.local_experts(0), K), pl)
+    got = m(torch.from_numpy(x)).numpy()
+    want, _, _ = M.moe_forward(x, wg, experts, K)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("W,replicated,T", [(2, (), (37, 21)), (3, (0,), (16, 1, 25)), (4, (0, 5), (8, 8, 8, 8))])
+def test_ep_loopback_matches_moe_forward(W, replicated, T):
+    wg, experts = _layer(3)
+    rng = np.random.default_rng(4)
+    xs = [_tokens(rng, t) for t in T]
+    counts = np.bincount(M.router_topk(M.gate_logits(np.concatenate(xs), wg).astype(np.float32), K)[0].ravel(),
+                         minlength=E)
+    pl = ExpertPlacement.from_counts(counts, W, replicated)
+    ranks = [ExpertParallelMoE(OracleBackend(wg, experts, pl.local_experts(r), K), pl, rank=r,
+                               exchange=_NoExchange(W, r)) for r in range(W)]
+    outs = run_loopback(ranks, [torch.from_numpy(x) for x in xs])
+    for x, o in zip(xs, outs):
+        want, _, _ = M.moe_forward(x, wg, experts, K)
+        np.testing.assert_array_equal(o.numpy(), want)
+
+
+class _NoExchange:
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+
+
+# ── world size 2 over gloo ─────────────────────────────────────────────────
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wg, experts = _layer(5)
+        rng = np.random.default_rng(100 + rank)
+        x = _tokens(rng, 30 + 7 * rank)
+        pl = ExpertPlacement.from_counts([40, 5, 30, 30, 10, 20], world, replicated=(2,))
+        m = ExpertParallelMoE(OracleBackend(wg, experts, pl.local_experts(rank), K), pl)
+        out = m(torch.from_numpy(x)).numpy()
+        want, _, _ = M.moe_forward(x, wg, experts, K)
+        np.save(os.path.join(outdir, f"r{rank}.npy"), np.stack([out, want]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_gloo_world2_matches_moe_forward():
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        for r in range(2):
+            got, want = np.load(os.path.join(d, f"r{r}.npy"))
+            np.testing.assert_array_equal(got, want)

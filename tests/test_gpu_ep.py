@@ -1,0 +1,109 @@
+"""GPU: the expert-parallel forward equals the single-GPU MoELayer forward
+bit for bit — at world size 1 (identity exchange and a real one-rank NCCL
+group) and with several simulated ranks driven in one process
+(``run_loopback``: remote experts, several sources per receiver, replicated
+experts, an idle rank). Also the EP plumbing kernels on their own."""
+
+import os
+import socket
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2508_07329_b200 import ops
+from paper_2508_07329_b200.ep import CudaExpertBackend, ExpertParallelMoE, ExpertPlacement, run_loopback
+from paper_2508_07329_b200.moe import MoELayer
+
+from .conftest import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+
+def _x(rng, T, d):
+    x = rng.normal(size=(T, d)).astype(np.float32)
+    x[:, rng.choice(d, max(1, d // 100), replace=False)] *= 100.0
+    return torch.from_numpy(bf16_round(x)).cuda().bfloat16()
+
+
+@pytest.fixture(scope="module")
+def layer(cuda):
+    return MoELayer.random(8, 512, 1024, top_k=2, seed=3)
+
+
+class _Local:
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+
+
+def test_gather_rows_and_params(cuda):
+    rng = np.random.default_rng(0)
+    src = torch.from_numpy(rng.integers(0, 256, size=(50, 72), dtype=np.uint8)).cuda()
+    idx = torch.from_numpy(rng.permutation(50)[:31].astype(np.int32)).cuda()
+    assert torch.equal(ops.gather_rows(src, idx), src[idx.long()])
+    odd = torch.from_numpy(rng.integers(0, 256, size=(9, 13), dtype=np.uint8)).cuda()   # byte rows
+    i2 = torch.tensor([8, 0, 3], dtype=torch.int32, device=cuda)
+    assert torch.equal(ops.gather_rows(odd, i2), odd[i2.long()])
+    a = {"codes": src, "scale_f32": torch.rand(50, device=cuda), "zp": torch.arange(50, dtype=torch.int32,
+                                                                                    device=cuda),
+         "rowsum": torch.arange(50, dtype=torch.int32, device=cuda) * 7}
+    w = torch.rand(50, device=cuda)
+    prm = ops.ep_pack_params(a, w)
+    u = ops.ep_unpack_params(prm, idx)
+    li = idx.long()
+    for k in ("scale_f32", "zp", "rowsum"):
+        assert torch.equal(u[k], a[k][li]), k
+    assert torch.equal(u["weight"], w[li])
+    dest = torch.tensor([1, 1, 0, 0, 2, 2, 3, 3], dtype=torch.int32, device=cuda)
+    top = torch.from_numpy(rng.integers(0, 8, size=(20, 2)).astype(np.int32)).cuda()
+    assert torch.equal(ops.route_keys(top, dest, 8), dest[top.long()] * 8 + top)
+
+
+def test_ep_world1_matches_layer(layer):
+    x = _x(np.random.default_rng(1), 777, layer.d)
+    pl = ExpertPlacement.sharded(layer.E, 1)
+    ep = ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(0)), pl)
+    assert torch.equal(ep(x), layer.forward(x))
+
+
+@pytest.mark.parametrize("W,replicated,T", [(2, (), (600, 333)), (4, (0, 5), (256, 1, 700, 90)),
+                                            (3, (0, 1, 2, 3, 4, 5, 6), (100, 200, 50))])
+def test_ep_loopback_matches_layer(layer, W, replicated, T):
+    rng = np.random.default_rng(2)
+    xs = [_x(rng, t, layer.d) for t in T]
+    counts = np.bincount(layer.route(torch.cat(xs))[1].cpu().numpy().ravel(), minlength=layer.E)
+    pl = ExpertPlacement.from_counts(counts, W, replicated)
+    ranks = [ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, rank=r,
+                               exchange=_Local(W, r)) for r in range(W)]
+    for x, out in zip(xs, run_loopback(ranks, xs)):
+        assert torch.equal(out, layer.forward(x))
+
+
+def test_ep_nccl_single_rank_group(tmp_path):
+    """A real NCCL process group (world 1): counts and rows go through
+    all_to_all_single; result equals the plain layer forward."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = textwrap.dedent(f"""
+        import os, sys, torch, numpy as np
+        sys.path.insert(0, {repr(os.getcwd())})
+        import torch.distributed as dist
+        from paper_2508_07329_b200.moe import MoELayer
+        from paper_2508_07329_b200.ep import CudaExpertBackend, ExpertParallelMoE, ExpertPlacement
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="{port}")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1)
+        layer = MoELayer.random(8, 256, 512, top_k=2, seed=4)
+        x = (torch.randn(300, 256, device="cuda") * 3).bfloat16()
+        pl = ExpertPlacement.sharded(8, 1)
+        ep = ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(0)), pl)
+        ok = torch.equal(ep(x), layer.forward(x))
+        dist.destroy_process_group()
+        print("EQUAL" if ok else "DIFFERENT")
+    """)
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300)
+    assert "EQUAL" in r.stdout, r.stdout + r.stderr
