@@ -52,7 +52,9 @@ struct GemmArgs {
   int64_t ldo;
   int32_t* acc_out;
   int64_t ld_acc;
-  int vec_ok;  // output pointer / ldo allow 16-byte vector stores
+  int vec_ok;      // output pointer / ldo allow 16-byte vector stores
+  int acc_vec_ok;  // acc_out / ld_acc and the W zp / rowsum tables allow 16-byte vectors
+  int param_vec_ok;  // W zp / rowsum / scale tables allow 16-byte vector loads
   // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
   const float* ns_rs32;
   int64_t ns_ld;
@@ -187,6 +189,26 @@ __device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t 
   return (int32_t)(acc - (uint32_t)zw * (uint32_t)rsa - (uint32_t)za * t);
 }
 
+// Per-column W parameters of 32 consecutive columns starting at n (16-byte
+// loads; all lanes of a warp read the same addresses -> L1 broadcast).
+struct ColParams32 {
+  int32_t zw[32], rsw[32];
+  float ws[32];
+};
+__device__ __forceinline__ void load_cols32(const GemmArgs& p, int n, ColParams32& c) {
+  const int4* z = reinterpret_cast<const int4*>(p.w_zp + n);
+  const int4* r = reinterpret_cast<const int4*>(p.w_rowsum + n);
+  const float4* w = reinterpret_cast<const float4*>(p.w_scale + n);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int4 zz = __ldg(z + q), rr = __ldg(r + q);
+    const float4 ww = __ldg(w + q);
+    c.zw[4 * q] = zz.x; c.zw[4 * q + 1] = zz.y; c.zw[4 * q + 2] = zz.z; c.zw[4 * q + 3] = zz.w;
+    c.rsw[4 * q] = rr.x; c.rsw[4 * q + 1] = rr.y; c.rsw[4 * q + 2] = rr.z; c.rsw[4 * q + 3] = rr.w;
+    c.ws[4 * q] = ww.x; c.ws[4 * q + 1] = ww.y; c.ws[4 * q + 2] = ww.z; c.ws[4 * q + 3] = ww.w;
+  }
+}
+
 // Epilogue of one tile for one thread: TMEM lane quarter q, column half
 // `half` (8 epilogue warps split the 256 columns), output row `row`.
 template <int BN, int EPI, bool BF16>
@@ -213,20 +235,40 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
       tmem_ld32(tbase + BN / 2 + c * 32, vu);
       tmem_ld_wait();
       float h[32];
+      const int ng0 = wbase + ti.n0 + c * 32;
+      if (p.param_vec_ok) {
+        ColParams32 cg, cu;
+        load_cols32(p, ng0, cg);
+        load_cols32(p, ng0 + BN / 2, cu);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int ng = wbase + ti.n0 + c * 32 + j;
-        const int nu = ng + BN / 2;
-        const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
-        const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
-        float g = (float)ag * (sa * p.w_scale[ng]);
-        float u = (float)au * (sa * p.w_scale[nu]);
-        if (p.bias) {
-          g += p.bias[ng];
-          u += p.bias[nu];
+        for (int j = 0; j < 32; ++j) {
+          const int32_t ag = zp_correct(vg[j], cg.zw[j], cg.rsw[j], za, rsa, p.K);
+          const int32_t au = zp_correct(vu[j], cu.zw[j], cu.rsw[j], za, rsa, p.K);
+          float g = (float)ag * (sa * cg.ws[j]);
+          float u = (float)au * (sa * cu.ws[j]);
+          if (p.bias) {
+            g += p.bias[ng0 + j];
+            u += p.bias[ng0 + BN / 2 + j];
+          }
+          h[j] = silu_f(g) * u * rw;
+          if (BF16) h[j] = __bfloat162float(__float2bfloat16_rn(h[j]));   // the value K1 will read
         }
-        h[j] = silu_f(g) * u * rw;
-        if (BF16) h[j] = __bfloat162float(__float2bfloat16_rn(h[j]));   // the value K1 will read
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int ng = ng0 + j;
+          const int nu = ng + BN / 2;
+          const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
+          const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
+          float g = (float)ag * (sa * p.w_scale[ng]);
+          float u = (float)au * (sa * p.w_scale[nu]);
+          if (p.bias) {
+            g += p.bias[ng];
+            u += p.bias[nu];
+          }
+          h[j] = silu_f(g) * u * rw;
+          if (BF16) h[j] = __bfloat162float(__float2bfloat16_rn(h[j]));   // the value K1 will read
+        }
       }
       if (rvalid) {
         store32<BF16>(p.out, (int64_t)row * p.ldo + ti.n0 / 2 + c * 32, h, 32, p.vec_ok);
@@ -245,22 +287,47 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
       if (!rvalid || nvalid <= 0) continue;
       if (EPI == MOE_EPI_ACC_I32) {
         int32_t* o = p.acc_out + (int64_t)row * p.ld_acc + n_lo;
+        if (nvalid == 32 && p.acc_vec_ok) {
+          const int4* wz = reinterpret_cast<const int4*>(p.w_zp + wbase + n_lo);
+          const int4* wr = reinterpret_cast<const int4*>(p.w_rowsum + wbase + n_lo);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (j < nvalid) {
-            const int n = wbase + n_lo + j;
-            o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+          for (int q = 0; q < 8; ++q) {
+            const int4 z = __ldg(wz + q), rs = __ldg(wr + q);
+            reinterpret_cast<int4*>(o)[q] =
+                make_int4(zp_correct(v[4 * q], z.x, rs.x, za, rsa, p.K), zp_correct(v[4 * q + 1], z.y, rs.y, za, rsa, p.K),
+                          zp_correct(v[4 * q + 2], z.z, rs.z, za, rsa, p.K),
+                          zp_correct(v[4 * q + 3], z.w, rs.w, za, rsa, p.K));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < nvalid) {
+              const int n = wbase + n_lo + j;
+              o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+            }
           }
         }
       } else {
         float y[32];
+        if (nvalid == 32 && p.param_vec_ok) {
+          ColParams32 cp;
+          load_cols32(p, wbase + n_lo, cp);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
-          const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
-          float val = (float)a * (sa * p.w_scale[n]);
-          if (p.bias) val += p.bias[n];
-          y[j] = val * rw;
+          for (int j = 0; j < 32; ++j) {
+            const int32_t a = zp_correct(v[j], cp.zw[j], cp.rsw[j], za, rsa, p.K);
+            float val = (float)a * (sa * cp.ws[j]);
+            if (p.bias) val += p.bias[wbase + n_lo + j];
+            y[j] = val * rw;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
+            const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+            float val = (float)a * (sa * p.w_scale[n]);
+            if (p.bias) val += p.bias[n];
+            y[j] = val * rw;
+          }
         }
         store32<BF16>(p.out, (int64_t)row * p.ldo + n_lo, y, nvalid, p.vec_ok);
       }
@@ -621,6 +688,11 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   p.row_ext = row_ext;
   const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
   p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
+  p.acc_vec_ok = acc_out && ((reinterpret_cast<uintptr_t>(acc_out) & 15) == 0) && (ld_acc % 4 == 0) &&
+                 ((reinterpret_cast<uintptr_t>(w_zp) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w_rowsum) & 15) == 0) &&
+                 (N % 4 == 0);
+  p.param_vec_ok = ((reinterpret_cast<uintptr_t>(w_zp) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w_rowsum) & 15) == 0) &&
+                   (!w_scale || (reinterpret_cast<uintptr_t>(w_scale) & 15) == 0) && (N % 4 == 0);
   cudaStream_t s = as_stream(stream);
   if (row_ext) {
     rowext_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_ext, M);
