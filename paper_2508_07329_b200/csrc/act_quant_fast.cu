@@ -278,14 +278,15 @@ __device__ __forceinline__ float min8(const float (&v)[8]) {
 // t = RN(xs * rsc + (1.5*2^23 + zp)) holds round(p) + zp in its low mantissa
 // bits (p = xs * rsc exact inside the FMA); d = RN(p - round(p)). A vector
 // of 8 takes the fast path when every code is in [2, 253] and every |d| is
-// below 0.5 - 2^-12: those codes equal the float64 reference's (|p| <= 256
-// there, so p is within 2^-14 of the reference quotient). Everything else —
+// below 0.5 - 2^-13: those codes equal the float64 reference's (|p| <= 254
+// there and p = y (1 + e), |e| <= 3 2^-24 + 2^-50, so |p - y| < 2^-14; d
+// itself carries one rounding of at most 2^-26). Everything else —
 // clipping, rounding-boundary cases, non-finite values and the elements
 // that could be row extremes (codes <= 1 / >= 254) — goes out of line.
 constexpr float kMagicF = 12582912.0f;
 constexpr float kFastTlo = 12582914.0f;          // code 2
 constexpr float kFastThi = 12583165.0f;          // code 253
-constexpr float kFastThr = 0.499755859375f;      // 0.5 - 2^-12
+constexpr float kFastThr = 0.4998779296875f;     // 0.5 - 2^-13
 
 struct FastRow {
   double scale, rscale;
@@ -298,16 +299,25 @@ struct FastRow {
 // count of possible-extreme elements. Returns (codes, cnt_max | cnt_min << 16).
 __device__ __noinline__ uint4 slow_vec8(uint4 u, const float* tab, int64_t c, const double* srow, const double* rrow,
                                         FastRow f) {
-  float xs[8];
+  float xv[8], xs[8];
+  unpack8(u, xv);
   smooth8(u, tab, c, xs);
-  uint32_t cnt = 0;
+  uint32_t cnt = 0, w[2] = {0u, 0u};
 #pragma unroll
-  for (int e = 0; e < 8; ++e) cnt += (uint32_t)(xs[e] >= f.cand_max) + ((uint32_t)(xs[e] <= f.cand_min) << 16);
-  RowEncoder enc(AffineParams{f.scale, f.rscale, f.zp}, 0.0, 0.0, 8, false);
-  enc.packed = false;
-  int sum = 0;
-  const uint2 out = enc.encode8(u, xs, c, srow, rrow, sum);
-  return make_uint4(out.x, out.y, cnt, 0u);
+  for (int e = 0; e < 8; ++e) {
+    cnt += (uint32_t)(xs[e] >= f.cand_max) + ((uint32_t)(xs[e] <= f.cand_min) << 16);
+    const float t = fmaf(xs[e], f.rsc, f.magic);
+    const float d = fmaf(xs[e], f.rsc, f.magic - t);   // magic - t = -round(p), exact
+    uint32_t code;
+    if (t >= kFastTlo && t <= kFastThi && fabsf(d) < kFastThr) {
+      code = __float_as_uint(t) & 0xFFu;
+    } else {   // clipping, rounding boundary, non-finite: the float64 reference encode
+      const double xd = srow ? div_rcp((double)xv[e], srow[c * 8 + e], rrow[c * 8 + e]) : (double)xv[e];
+      code = (uint32_t)encode_code(xd, f.scale, f.rscale, f.zp, 255);
+    }
+    w[e >> 2] |= code << (8 * (e & 3));
+  }
+  return make_uint4(w[0], w[1], cnt, 0u);
 }
 
 __device__ __forceinline__ uint32_t low_bytes4(float a, float b, float c, float d) {
@@ -491,6 +501,333 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   }
 }
 
+// ── bulk-async (TMA) streaming variant ─────────────────────────────────────
+// Same per-row algorithm as act_quant_warp_kernel, but rows are streamed
+// through a per-warp ring of kRing x 2 KB shared-memory stages filled by
+// cp.async.bulk (one elected lane issues, an mbarrier per stage completes
+// on the byte count): up to 12 KB in flight per warp regardless of register
+// pressure, so one 16-warp CTA per SM keeps ~190 KB of loads outstanding and
+// HBM saturated. Rows that fit the ring (x rows, d <= 6144) are held for the
+// second pass; longer rows without records are streamed twice.
+constexpr int kChunkBytes = 2048;
+constexpr int kChunkVec = kChunkBytes / 16;   // 128 x 16 B: 4 vectors per lane
+constexpr int kRing = 8;
+constexpr int kBulkWarps = 12;
+constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
+
+__device__ __forceinline__ uint2 fast_vec8(const uint4& u, int64_t c, const float* tab, const double* srow,
+                                           const double* rrow, const FastRow& f, uint32_t& cnt) {
+  float xs[8];
+  smooth8(u, tab, c, xs);
+  const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
+  float t[8], d[8];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    const float2 x2 = make_float2(xs[e], xs[e + 1]);
+    const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
+    const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
+    const float2 d2 = __ffma2_rn(x2, rsc2, nr);
+    t[e] = t2.x;
+    t[e + 1] = t2.y;
+    d[e] = d2.x;
+    d[e + 1] = d2.y;
+  }
+  const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
+                                 fmax3_abs_nan(d[6], d[7], 0.f));
+  if (max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr)
+    return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
+  const uint4 sv = slow_vec8(u, tab, c, srow, rrow, f);
+  cnt += sv.z;
+  return make_uint2(sv.x, sv.y);
+}
+
+// xs = x * table for 8 elements, table slice preloaded (ta: elements 0-3, tb: 4-7)
+__device__ __forceinline__ void smooth8_pre(const uint4& u, bool has_tab, const float4& ta, const float4& tb,
+                                            float (&xs)[8]) {
+  unpack8(u, xs);
+  if (has_tab) {
+    float2 q;
+    q = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(ta.x, ta.y)); xs[0] = q.x; xs[1] = q.y;
+    q = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(ta.z, ta.w)); xs[2] = q.x; xs[3] = q.y;
+    q = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(tb.x, tb.y)); xs[4] = q.x; xs[5] = q.y;
+    q = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(tb.z, tb.w)); xs[6] = q.x; xs[7] = q.y;
+  }
+}
+
+// branch-free fast encode of 8 smoothed values; slow = the vector must take slow_vec8
+__device__ __forceinline__ uint2 fast_core(const float (&xs)[8], const FastRow& f, bool& slow) {
+  const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
+  float t[8], d[8];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    const float2 x2 = make_float2(xs[e], xs[e + 1]);
+    const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
+    const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
+    const float2 d2 = __ffma2_rn(x2, rsc2, nr);
+    t[e] = t2.x;
+    t[e + 1] = t2.y;
+    d[e] = d2.x;
+    d[e + 1] = d2.y;
+  }
+  const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
+                                 fmax3_abs_nan(d[6], d[7], 0.f));
+  slow = !(max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr);
+  return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
+}
+
+template <bool GIVEN>
+__global__ void __launch_bounds__(kBulkWarps * 32, 1)
+    act_quant_bulk_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
+                          int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                          int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint8_t* ring = smem_raw + warp * kRing * kChunkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kBulkWarps * kRing * kChunkBytes) + warp * kRing;
+  if (lane == 0) {
+    for (int i = 0; i < kRing; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int64_t nvec = a.cols / 8;
+  const int64_t row_bytes = a.cols * 2;
+  const int nchunks = (int)((nvec + kChunkVec - 1) / kChunkVec);
+  const bool hold = !GIVEN && nchunks <= kRing;
+  const int items_per_row = (GIVEN || hold) ? nchunks : 2 * nchunks;
+  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
+  const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
+  const uint64_t pol = policy_evict_first();
+
+  // producer: the warp's item stream (row, chunk) in consumption order
+  int64_t prow = r_lo + warp;
+  int pitem = 0;
+  uint32_t pcount = 0;
+  int64_t prow_off = prow < r_hi ? row_view(a, prow).off : 0;
+  auto produce = [&]() {
+    if (prow >= r_hi) return;
+    if (lane == 0) {
+      const int chunk = pitem % nchunks;
+      const int64_t b0 = (int64_t)chunk * kChunkBytes;
+      const uint32_t bytes = (uint32_t)min((int64_t)kChunkBytes, row_bytes - b0);
+      const int st = (int)(pcount % kRing);
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bars[st], bytes);
+      bulk_load(ring + st * kChunkBytes, static_cast<const uint8_t*>(a.x) + prow_off * 2 + b0, bytes, &bars[st],
+                pol);
+    }
+    ++pcount;
+    if (++pitem == items_per_row) {
+      pitem = 0;
+      prow += kBulkWarps;
+      if (prow < r_hi) prow_off = row_view(a, prow).off;
+    }
+  };
+  for (int i = 0; i < kRing; ++i) produce();
+  uint32_t ccount = 0;
+  auto wait_item = [&](uint32_t it) { mbar_wait(&bars[it % kRing], (it / kRing) & 1u); };
+  auto item_vec = [&](uint32_t it) { return reinterpret_cast<const uint4*>(ring + (it % kRing) * kChunkBytes); };
+  for (int64_t r = r_lo + warp; r < r_hi; r += kBulkWarps) {
+    const RowView rv = row_view(a, r);
+    const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + rv.off;
+    const uint4* src = reinterpret_cast<const uint4*>(row);
+    const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
+    const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
+    const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
+    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+    const uint32_t base = ccount;
+    ccount += items_per_row;
+
+    RowExt rec;
+    if (GIVEN) {
+      const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
+      rec = RowExt{key_to_float((uint32_t)(kmax >> 32)), key_to_float((uint32_t)(kmin >> 32)),
+                   (int64_t)(kmax & 0xFFFFFFFFu), (int64_t)(kmin & 0xFFFFFFFFu)};
+    } else {
+      // per lane: running max / min and the vector holding them (first
+      // occurrence), then the element inside that vector
+      float tmax = -FLT_MAX, tmin = FLT_MAX;
+      int64_t vmaxc = 0, vminc = 0;
+      for (int k = 0; k < nchunks; ++k) {
+        const uint32_t it = base + k;
+        wait_item(it);
+        const uint4* v = item_vec(it);
+        const int64_t cb = (int64_t)k * kChunkVec + lane;
+        const bool full = (int64_t)(k + 1) * kChunkVec <= nvec;
+        uint4 u[4];
+        float4 ta[4], tb[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const bool ok = full || cb + 32 * b < nvec;
+          u[b] = ok ? v[lane + 32 * b] : make_uint4(0u, 0u, 0u, 0u);
+          if (tab && ok) {
+            ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b));
+            tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b) + 1);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (!(full || cb + 32 * b < nvec)) continue;
+          float xs[8];
+          smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
+          const float vmax = max8(xs), vmin = min8(xs);
+          const bool um = vmax > tmax, un = vmin < tmin;
+          tmax = um ? vmax : tmax;
+          vmaxc = um ? cb + 32 * b : vmaxc;
+          tmin = un ? vmin : tmin;
+          vminc = un ? cb + 32 * b : vminc;
+        }
+        __syncwarp();
+        if (!hold) produce();
+      }
+      warp_argmax(tmax, vmaxc);
+      warp_argmin(tmin, vminc);
+      // locate the element (first in the vector) from the resident chunk, or global
+      auto locate = [&](int64_t vc, float val) -> int64_t {
+        const uint4 u = hold ? item_vec(base + (uint32_t)(vc / kChunkVec))[vc % kChunkVec] : src[vc];
+        float xs[8];
+        smooth8(u, tab, vc, xs);
+        int j = 0;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) j = xs[e] == val ? e : j;
+        return vc * 8 + j;
+      };
+      const int64_t imax = locate(vmaxc, tmax), imin = locate(vminc, tmin);
+      rec = RowExt{tmax, tmin, imax, imin};
+    }
+    const uint32_t cfirst = (GIVEN || hold) ? base : base + nchunks;   // items of the encode pass
+    const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m)) || rec.cM >= a.cols || rec.cm >= a.cols;
+    bool spec = !exact_all;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    if (spec) {
+      mx = exact_at(row, tab, srow, rrow, rec.cM, rec.M, spec);
+      mn = exact_at(row, tab, srow, rrow, rec.cm, rec.m, spec);
+    }
+    const float lb_max = spec ? rec.M - err_bound(rec.M) : -FLT_MAX;
+    const float ub_min = spec ? rec.m + err_bound(rec.m) : FLT_MAX;
+
+    AffineParams p{};
+    int sum = 0;
+    bool done = false;
+    bool fast = spec && bits == 8 && !sym;
+    FastRow f;
+    if (fast) {
+      p = affine_params(mn, mx, bits, sym);
+      const double hc = __dadd_rn(rha(div_rcp(mx, p.scale, p.rscale)), (double)p.zp);
+      const double lc = __dadd_rn(rha(div_rcp(mn, p.scale, p.rscale)), (double)p.zp);
+      fast = hc >= 255.0 && lc <= 0.0;
+      f.scale = p.scale;
+      f.rscale = p.rscale;
+      f.zp = p.zp;
+      f.rsc = __double2float_rn(p.rscale);
+      f.magic = kMagicF + (float)p.zp;
+      f.cand_max = rec.M - 3.f * fabsf(rec.M) * kRelErr - 2.350988701644575e-38f;
+      f.cand_min = rec.m + 3.f * fabsf(rec.m) * kRelErr + 2.350988701644575e-38f;
+    }
+    if (fast) {
+      uint32_t cnt = 0;
+      for (int k = 0; k < nchunks; ++k) {
+        const uint32_t it = cfirst + k;
+        wait_item(it);
+        const uint4* v = item_vec(it);
+        const int64_t cb = (int64_t)k * kChunkVec + lane;
+        if ((int64_t)(k + 1) * kChunkVec <= nvec) {
+          // full chunk: table loads up front, no per-vector branches; the rare
+          // slow vectors are redone afterwards (same lane, same addresses)
+          uint4 u[4];
+          float4 ta[4], tb[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            u[b] = v[lane + 32 * b];
+            if (tab) {
+              ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b));
+              tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b) + 1);
+            }
+          }
+          uint2 out[4];
+          uint32_t slowm = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            float xs[8];
+            smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
+            bool sl;
+            out[b] = fast_core(xs, f, sl);
+            slowm |= (uint32_t)sl << b;
+          }
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            sum += bytesum(out[b]);
+            __stcs(dst + cb + 32 * b, out[b]);
+          }
+          if (slowm) {
+            for (int b = 0; b < 4; ++b) {
+              if (!(slowm >> b & 1u)) continue;
+              const uint4 sv = slow_vec8(u[b], tab, cb + 32 * b, srow, rrow, f);
+              cnt += sv.z;
+              const uint2 o2 = make_uint2(sv.x, sv.y);
+              sum += bytesum(o2) - bytesum(out[b]);
+              __stcs(dst + cb + 32 * b, o2);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int64_t c = cb + 32 * b;
+            if (c < nvec) {
+              const uint2 out = fast_vec8(v[lane + 32 * b], c, tab, srow, rrow, f, cnt);
+              sum += bytesum(out);
+              __stcs(dst + c, out);
+            }
+          }
+        }
+        __syncwarp();
+        produce();
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      }
+      done = cnt == 0x10001u;
+    } else {
+      for (int k = 0; k < nchunks; ++k) {   // keep the ring in step
+        wait_item(cfirst + k);
+        __syncwarp();
+        produce();
+      }
+    }
+    if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
+    if (lane == 0) {
+      if (rowsum) rowsum[r] = sum;
+      scale[r] = p.scale;
+      if (scale_f32) scale_f32[r] = (float)p.scale;
+      zp[r] = p.zp;
+    }
+  }
+}
+
+template <bool GIVEN>
+static cudaError_t launch_bulk(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
+                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                               int32_t* rowsum, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(act_quant_bulk_kernel<GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kBulkSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + kBulkWarps - 1) / kBulkWarps, num_sms()));
+  const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
+  const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
+  act_quant_bulk_kernel<GIVEN><<<(unsigned)nblk, kBulkWarps * 32, kBulkSmem, s>>>(
+      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static bool eligible(const RowArgs& a, const float* rs32, uint8_t* codes, int64_t ldc) {
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
   return a.dt == MOE_DT_BF16 && a.cols % 8 == 0 && a.ldx % 8 == 0 && ldc % 8 == 0 &&
@@ -511,18 +848,21 @@ static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long 
       a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
 }
 
+// Kernel choice (measured on B200 at the Mixtral shape, tools/k1_bench.py):
+// rows with producer records (h) stream through the bulk-async ring; rows
+// that need their own extreme pass (x) use the register kernel, whose pass
+// A re-read hits L1. MOE_B200_K1_CFG=0 / 7 forces one kernel for both.
 template <bool GIVEN>
 static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                               int32_t* rowsum, cudaStream_t s) {
-  const char* env = getenv("MOE_B200_K1_CFG");
-  const int cfg = env ? atoi(env) : 0;
-  switch (cfg) {
-    case 1: launch_cfg<GIVEN, 16, 1>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
-    case 2: launch_cfg<GIVEN, 8, 3>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
-    case 3: launch_cfg<GIVEN, 8, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s); break;
-    default: launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
-  }
+  static const int forced = [] {
+    const char* env = getenv("MOE_B200_K1_CFG");
+    return env ? atoi(env) : -1;
+  }();
+  const bool bulk = forced == 7 || (forced < 0 && GIVEN);
+  if (bulk) return launch_bulk<GIVEN>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+  launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   count_launch();
   return cudaGetLastError();
 }

@@ -149,6 +149,90 @@ __global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat
   }
 }
 
+// Register-resident gate: warp w of the CTA owns columns [256w, 256w + 256),
+// lane l the 8 columns 256w + 8l .. +8 of all E <= 8 gate rows (64 floats in
+// registers, loaded once per CTA). The CTA streams batches of 4 tokens:
+// each lane loads 16 B of x per token, forms 4 x 8 partial dot products, a
+// transpose-reduce across the warp leaves lane l with entry l of the 32
+// (token, expert) sums, and warp 0 adds the per-warp partials (fixed order
+// -> deterministic) and runs top-k. x is read once from HBM; no shared-memory
+// traffic for the weights.
+constexpr int kRouterTB = 4;
+
+__global__ void __launch_bounds__(512, 1)
+    router_gate_reg_kernel(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t d, const float* __restrict__ gw,
+                           const float* gb, int E, int k, float* logits, int32_t* idx, float* w) {
+  __shared__ float part[2][16][32];   // [buffer][warp][lane] -> entry lane = token * 8 + expert
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int64_t col0 = (int64_t)warp * 256 + lane * 8;
+  float g[8][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < E) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(gw + (int64_t)e * d + col0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(gw + (int64_t)e * d + col0) + 1);
+      g[e][0] = a.x; g[e][1] = a.y; g[e][2] = a.z; g[e][3] = a.w;
+      g[e][4] = b.x; g[e][5] = b.y; g[e][6] = b.z; g[e][7] = b.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) g[e][c] = 0.f;
+    }
+  }
+  int buf = 0;
+  for (int64_t t0 = (int64_t)blockIdx.x * kRouterTB; t0 < T; t0 += (int64_t)gridDim.x * kRouterTB, buf ^= 1) {
+    uint4 u[kRouterTB];
+#pragma unroll
+    for (int t = 0; t < kRouterTB; ++t)
+      u[t] = t0 + t < T ? __ldcs(reinterpret_cast<const uint4*>(x + (t0 + t) * d + col0)) : make_uint4(0, 0, 0, 0);
+    float v[32];
+#pragma unroll
+    for (int t = 0; t < kRouterTB; ++t) {
+      const uint32_t wd[4] = {u[t].x, u[t].y, u[t].z, u[t].w};
+      float xv[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xv[2 * i] = __uint_as_float(wd[i] << 16);
+        xv[2 * i + 1] = __uint_as_float(wd[i] & 0xFFFF0000u);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc = fmaf(xv[c], g[e][c], acc);
+        v[t * 8 + e] = acc;
+      }
+    }
+    // transpose-reduce: after the step with xor offset o the lane keeps the
+    // upper half when (lane & o); finally lane l holds entry l
+#pragma unroll
+    for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+      const bool up = lane & o;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const float send = up ? v[i] : v[i + half];
+        const float keep = up ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    part[buf][warp][lane] = v[0];
+    __syncthreads();
+    if (warp == 0) {
+      float sum = 0.f;
+      for (int ww = 0; ww < nw; ++ww) sum += part[buf][ww][lane];
+      const int t = lane >> 3, e = lane & 7;
+      if (gb && e < E) sum += gb[e];
+      const int64_t tok = t0 + t;
+      if (logits && tok < T && e < E) logits[tok * E + e] = sum;
+      float l[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) l[q] = __shfl_sync(0xffffffffu, sum, (lane & ~7) + q);
+      if (e == 0 && tok < T) topk_select(l, E, k, idx + tok * k, w + tok * k);
+    }
+  }
+}
+
 __global__ void router_topk_kernel(const float* logits, int64_t T, int E, int k, int32_t* idx, float* w) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
     float l[kMaxE];
@@ -309,7 +393,13 @@ extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   cudaStream_t s = as_stream(stream);
   const int64_t gw_bytes = (int64_t)E * d * 4;
-  if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
+  if (x_dtype == MOE_DT_BF16 && d % 256 == 0 && d <= 4096 && E <= 8 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
+    const int64_t grid = std::min<int64_t>((T + kRouterTB - 1) / kRouterTB, num_sms());
+    router_gate_reg_kernel<<<(unsigned)grid, (unsigned)(d / 256 * 32), 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x), T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
+    ::moe::count_launch();
+  } else if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
     static bool attr = false;
     if (!attr) {

@@ -1,4 +1,4 @@
-"""Probe the host-buffer pipeline: copy/compute overlap of MoELayer.forward_host."""
+"""Probe the host-buffer pipeline of MoELayer.forward_host: chunk plans."""
 import sys, time
 sys.path.insert(0, ".")
 import torch
@@ -21,17 +21,11 @@ def wall(fn, n=10):
 print("forward dev ms", wall(lambda: layer.forward(xd)))
 print("h2d ms", wall(lambda: xd.copy_(xh, non_blocking=True)))
 print("d2h ms", wall(lambda: oh.copy_(xd, non_blocking=True)))
-for ch in (16384, 8192, 4096, 2048):
-    print("forward_host chunk", ch, "ms", wall(lambda: layer.forward_host(xh, oh, chunk_tokens=ch)))
-s = torch.cuda.Stream()
-with torch.cuda.stream(s):
-    for ch in (4096, 2048):
-        print("forward_host on side stream chunk", ch, "ms", wall(lambda: layer.forward_host(xh, oh, chunk_tokens=ch)))
-s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-def both():
-    with torch.cuda.stream(s1):
-        xd.copy_(xh, non_blocking=True)
-    with torch.cuda.stream(s2):
-        layer.forward(xd[:8192])
-print("h2d || forward(8192) ms", wall(both))
-print("forward(8192) ms", wall(lambda: layer.forward(xd[:8192])))
+plans = {"4x4096": [4096] * 4, "8x2048": [2048] * 8, "default": None,
+         "ramp512": MoELayer.chunk_plan(T, 4096, 512), "ramp1024_8192": MoELayer.chunk_plan(T, 8192, 1024),
+         "ramp512_8192": MoELayer.chunk_plan(T, 8192, 512), "ramp2048": MoELayer.chunk_plan(T, 4096, 2048)}
+for name, pl in plans.items():
+    print(f"forward_host {name:14s} {str(pl if pl else MoELayer.chunk_plan(T)):60s} ms",
+          wall(lambda: layer.forward_host(xh, oh, chunks=pl)))
+for t in (1024, 2048, 4096, 8192, 16384):
+    print(f"forward dev T={t:6d} ms", wall(lambda: layer.forward(xd[:t])))

@@ -70,7 +70,7 @@ if os.environ.get("K1_PROF"):
 ref_x, ref_h = qx(), qh_plain()
 bytes_x = R * 4096 * 2 + R * 4096       # gathered bf16 rows read + codes written
 bytes_h = R * 14336 * 2 + R * 14336
-for cfg in ("0", "1", "2", "3"):
+for cfg in sys.argv[2].split(",") if len(sys.argv) > 2 else ("-1", "0", "7"):
     os.environ["MOE_B200_K1_CFG"] = cfg
     gx, gh = qx(), qh()
     ok = all(torch.equal(gx[k], ref_x[k]) for k in ("codes", "scale", "zp", "rowsum")) and \
