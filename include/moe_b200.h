@@ -56,6 +56,10 @@ enum { MOE_GRAN_PER_TENSOR = 0, MOE_GRAN_PER_TOKEN = 1, MOE_GRAN_PER_OUTPUT_ROW 
 enum { MOE_SMOOTH_NONE = 0, MOE_SMOOTH_DIVIDE = 1, MOE_SMOOTH_MULTIPLY = 2 };
 /* GEMM epilogues */
 enum { MOE_EPI_DEQUANT = 0, MOE_EPI_SWIGLU = 1, MOE_EPI_ACC_I32 = 2 };
+/* OR-ed into `epilogue`: w_rowsum holds the pre-corrected weight term
+ * rowsum_w - K * w_zp (precomputed once per weight matrix) instead of the
+ * plain code row sums; saves one integer multiply per accumulator. */
+enum { MOE_EPI_FLAG_WCORR = 0x100 };
 /* channel ordering strategies (quant.py:42-45) */
 enum { MOE_ORDER_MAX_ABS = 1, MOE_ORDER_SUM_SQUARES = 2 };
 
@@ -90,7 +94,8 @@ moe_status moe_device_check(int dev);
  * rowsum (optional) [rows] = sum of the row's codes (for the GEMM's
  * zero-point correction). row_ext (optional, per-row modes, bf16 input):
  * records [rows, 2] (min, max) of the float32 smoothed row (x * RN32(1/s)),
- * each (order-preserving key of the value << 32) | column, as produced by
+ * each (order-preserving key of the value << 32) | c with the extreme
+ * element in columns [c, c + 32) (an exact column also qualifies), as produced by
  * moe_w8a8_gemm's SwiGLU epilogue — the kernel then speculates that the two
  * recorded elements are the exact extremes and streams the row once,
  * verifying the speculation while encoding (a failed check re-encodes the
@@ -140,8 +145,8 @@ moe_status moe_channel_stats(const double* x, int64_t n, int64_t T, int strategy
  * of M rows. K must be a multiple of 16; other shapes use a SIMT path with
  * identical integer results.
  * Fusion with the next K1 (SwiGLU epilogue, tensor-core path): when
- * row_ext [M, 2] is given, the epilogue also emits the (value, column)
- * records of the float32 min and max of each stored output row times the
+ * row_ext [M, 2] is given, the epilogue also emits the (value, 32-column
+ * chunk) records of the float32 min and max of each stored output row times the
  * next layer's RN32 reciprocal smoothing (table [G, next_ld]), so that
  * moe_act_quant(row_ext=...) reads h once. */
 moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,

@@ -13,12 +13,15 @@ from pathlib import Path
 from .errors import DegenerateHessianError, NotPositiveDefiniteError, QuantizationFailedError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmoe_b200.so"
+if os.environ.get("MOE_B200_LIB"):     # experiment builds (tools/build_variant.sh); default: the in-tree build
+    LIB_PATH = Path(os.environ["MOE_B200_LIB"]).resolve()
 
 OK, EINVAL, ENOTPD, EDEGENERATE, EQUANTFAIL, ECUDA, EUNSUPPORTED = range(7)
 DT_F32, DT_F64, DT_BF16, DT_F16, DT_U8, DT_I32 = range(6)
 GRAN = {"per_tensor": 0, "per_token": 1, "per_output_row": 2}
 SMOOTH_NONE, SMOOTH_DIVIDE, SMOOTH_MULTIPLY = 0, 1, 2
 EPI_DEQUANT, EPI_SWIGLU, EPI_ACC_I32 = 0, 1, 2
+EPI_FLAG_WCORR = 0x100
 ORDER_MAX_ABS, ORDER_SUM_SQUARES = 1, 2
 
 _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double

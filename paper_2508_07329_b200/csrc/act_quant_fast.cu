@@ -198,6 +198,33 @@ __device__ __forceinline__ float key_to_float(uint32_t k) {
   return __int_as_float(i >= 0 ? i : (i ^ 0x7FFFFFFF));
 }
 
+// Producer records (value key << 32 | c): the extreme element lies in columns
+// [c, c + 32) (the GEMM epilogue records the 32-column chunk; an exact column
+// also qualifies). The warp locates the first element of the chunk whose
+// float32 smoothed value equals the recorded one; none -> column = cols
+// (an inconsistent record, handled as such by the caller).
+__device__ __forceinline__ int64_t locate32(const __nv_bfloat16* row, const float* tab, int64_t cols, int64_t base,
+                                            float val, int lane) {
+  const int64_t j = base + lane;
+  bool hit = false;
+  if (j < cols) {
+    const float xf = __bfloat162float(row[j]);
+    hit = (tab ? __fmul_rn(xf, tab[j]) : xf) == val;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  return m ? base + __ffs(m) - 1 : cols;
+}
+
+__device__ __forceinline__ RowExt given_record(const __nv_bfloat16* row, const float* tab, int64_t cols,
+                                               unsigned long long kmax, unsigned long long kmin, int lane) {
+  RowExt rec{key_to_float((uint32_t)(kmax >> 32)), key_to_float((uint32_t)(kmin >> 32)), cols, cols};
+  if (isfinite(rec.M) && isfinite(rec.m)) {
+    rec.cM = locate32(row, tab, cols, (int64_t)(kmax & 0xFFFFFFFFu), rec.M, lane);
+    rec.cm = locate32(row, tab, cols, (int64_t)(kmin & 0xFFFFFFFFu), rec.m, lane);
+  }
+  return rec;
+}
+
 template <typename F>
 __device__ __forceinline__ void for_row_batches(const uint4* src, int64_t nvec, int lane, F&& body) {
   for (int64_t c0 = lane; c0 < nvec; c0 += 32 * kBatch) {
@@ -393,8 +420,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     RowExt rec;
     if (GIVEN) {
       const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
-      rec = RowExt{key_to_float((uint32_t)(kmax >> 32)), key_to_float((uint32_t)(kmin >> 32)),
-                   (int64_t)(kmax & 0xFFFFFFFFu), (int64_t)(kmin & 0xFFFFFFFFu)};
+      rec = given_record(row, tab, a.cols, kmax, kmin, lane);
     } else {
       float tmax = -FLT_MAX, tmin = FLT_MAX;
       int64_t imax = 0, imin = 0;
@@ -643,8 +669,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     RowExt rec;
     if (GIVEN) {
       const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
-      rec = RowExt{key_to_float((uint32_t)(kmax >> 32)), key_to_float((uint32_t)(kmin >> 32)),
-                   (int64_t)(kmax & 0xFFFFFFFFu), (int64_t)(kmin & 0xFFFFFFFFu)};
+      rec = given_record(row, tab, a.cols, kmax, kmin, lane);
     } else {
       // per lane: running max / min and the vector holding them (first
       // occurrence), then the element inside that vector

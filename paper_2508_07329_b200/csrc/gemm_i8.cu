@@ -39,6 +39,7 @@ constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
 
 struct GemmArgs {
   int M, N, K, G;
+  int Kc;  // K of the zero-point correction term (0 when w_rowsum is pre-corrected)
   const int32_t* offsets;
   const float* a_scale;
   const int32_t* a_zp;
@@ -55,6 +56,8 @@ struct GemmArgs {
   int vec_ok;      // output pointer / ldo allow 16-byte vector stores
   int acc_vec_ok;  // acc_out / ld_acc and the W zp / rowsum tables allow 16-byte vectors
   int param_vec_ok;  // W zp / rowsum / scale tables allow 16-byte vector loads
+  int debug_skip_epilogue;  // MOE_B200_GEMM_SKIP_EPILOGUE=1: timing experiments only
+  int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
   const float* ns_rs32;
   int64_t ns_ld;
@@ -70,7 +73,9 @@ struct Smem {
   static constexpr int kNumBars = 2 * STAGES + 4;
   static constexpr int kTmemPtrOff = kBarOff + kNumBars * 8;
   static constexpr int kTableOff = kTmemPtrOff + 16;                  // tile_start[G+1], off[G+1]
-  static constexpr int kBytes = kTableOff + 2 * (kMaxGroups + 1) * 4 + 1024;  // + alignment slack
+  static constexpr int kOutOff = (kTableOff + 2 * (kMaxGroups + 1) * 4 + 127) / 128 * 128;
+  static constexpr int kOutBytes = 8 * 2 * 1024;                       // 8 epilogue warps x 2 x (32 rows x 32 B)
+  static constexpr int kBytes = kOutOff + kOutBytes + 1024;           // + alignment slack
 };
 
 struct TileInfo {
@@ -124,15 +129,29 @@ __device__ __forceinline__ void store32(void* out, int64_t idx, const float (&v)
 
 // ── per-row float32 extreme records of stored output * RN32(1/s_next) ─────
 // Feeds the next K1 (act_quant row_ext): the same float32 products K1 forms,
-// reduced per thread to (value, column) of the max and of the min and merged
-// per row with one 64-bit atomic each per tile: (order-preserving key << 32)
-// | column. K1 then only divides those two elements exactly and verifies
-// during its single encode pass that no other element could be an extreme.
+// reduced per thread to (value, 32-column chunk) of the max and of the min
+// and merged per row with one 64-bit atomic each per tile: (order-preserving
+// key << 32) | first column of the chunk. K1 locates the element in the
+// chunk, divides the two extremes exactly and verifies during its single
+// encode pass that no other element could be an extreme.
 struct ExtRec {
   float M, m;
   int cM, cm;
 };
 
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// max / min of the 32 products of one chunk; the record keeps the chunk's
+// first column (K1 locates the element inside the chunk with one warp ballot)
 __device__ __forceinline__ void chunk_ext(const float (&hv)[32], const float* __restrict__ t32, int col0,
                                           ExtRec& r) {
   const float4* t = reinterpret_cast<const float4*>(t32);
@@ -149,23 +168,19 @@ __device__ __forceinline__ void chunk_ext(const float (&hv)[32], const float* __
   }
   float M = xs[0], m = xs[0];
 #pragma unroll
-  for (int j = 1; j < 32; ++j) {
-    M = fmaxf(M, xs[j]);
-    m = fminf(m, xs[j]);
+  for (int j = 1; j < 31; j += 2) {
+    M = fmax3f(M, xs[j], xs[j + 1]);
+    m = fmin3f(m, xs[j], xs[j + 1]);
   }
-  if (M > r.M) {  // rare after the first chunk: locate the column
-    int j0 = 0;
-#pragma unroll
-    for (int j = 31; j >= 0; --j) j0 = xs[j] == M ? j : j0;
+  M = fmaxf(M, xs[31]);
+  m = fminf(m, xs[31]);
+  if (M > r.M) {
     r.M = M;
-    r.cM = col0 + j0;
+    r.cM = col0;
   }
   if (m < r.m) {
-    int j0 = 0;
-#pragma unroll
-    for (int j = 31; j >= 0; --j) j0 = xs[j] == m ? j : j0;
     r.m = m;
-    r.cm = col0 + j0;
+    r.cm = col0;
   }
 }
 
@@ -192,7 +207,7 @@ __device__ __forceinline__ int32_t zp_correct(uint32_t acc, int32_t zw, int32_t 
 // Per-column W parameters of 32 consecutive columns starting at n (16-byte
 // loads; all lanes of a warp read the same addresses -> L1 broadcast).
 struct ColParams32 {
-  int32_t zw[32], rsw[32];
+  int32_t zw[32], rsw[32];   // rsw: rowsum, or t = rowsum - K*zp when loaded by load_cols32_t
   float ws[32];
 };
 __device__ __forceinline__ void load_cols32(const GemmArgs& p, int n, ColParams32& c) {
@@ -209,11 +224,166 @@ __device__ __forceinline__ void load_cols32(const GemmArgs& p, int n, ColParams3
   }
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// SwiGLU epilogue hot path (vectorisable W tables, no bias): this thread's
+// row, `half` of the tile's h columns, in 16-column sub-chunks with the next
+// sub-chunk's TMEM loads in flight while the current one is computed.
+// Zero-point correction in 2 IMADs per accumulator (row terms pre-negated,
+// column term t = rowsum - Kc*zp), packed f32x2 math, silu through
+// ex2/rcp.approx (what __expf / __fdividef compile to in range).
+template <int BN, bool BF16>
+__device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase, int half,
+                                            ExtRec& ext, bool rvalid, float sa, float rw, int32_t za, int32_t rsa,
+                                            const CUtensorMap* tmO, uint8_t* obuf, uint32_t& ob) {
+  constexpr int kSub = 16;
+  constexpr int kNSub = BN / 4 / kSub;             // sub-chunks per thread (half of BN/2 h columns)
+  const int wbase = ti.g * p.N;
+  const int hc0 = half * (BN / 4);                 // first h column (tile-relative) of this thread
+  const uint32_t nrsa = 0u - (uint32_t)rsa, nza = 0u - (uint32_t)za, kc = (uint32_t)p.Kc;
+  const float2 sa2 = make_float2(sa, sa), srw2 = make_float2(sa * rw, sa * rw);
+  const float2 nl2 = make_float2(-1.4426950408889634f, -1.4426950408889634f), one2 = make_float2(1.f, 1.f);
+  // whole-warp TMA store of the 32 x 16 h block when all 32 rows are in the group
+  const bool tma = BF16 && p.tma_out && __all_sync(0xffffffffu, rvalid);
+  const int lane = threadIdx.x & 31;
+  uint32_t ag[2][kSub], au[2][kSub];
+  tmem_ld16(tbase + hc0, ag[0]);
+  tmem_ld16(tbase + BN / 2 + hc0, au[0]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int sc = 0; sc < kNSub; ++sc) {
+    const int cur = sc & 1;
+    const int hc = hc0 + sc * kSub;                // tile-relative h column of this sub-chunk
+    if (sc + 1 < kNSub) {
+      tmem_ld16(tbase + hc + kSub, ag[cur ^ 1]);
+      tmem_ld16(tbase + BN / 2 + hc + kSub, au[cur ^ 1]);
+    }
+    const int ng0 = wbase + ti.n0 + hc;
+    const int4* gz = reinterpret_cast<const int4*>(p.w_zp + ng0);
+    const int4* gr = reinterpret_cast<const int4*>(p.w_rowsum + ng0);
+    const float4* gs = reinterpret_cast<const float4*>(p.w_scale + ng0);
+    const int4* uz = reinterpret_cast<const int4*>(p.w_zp + ng0 + BN / 2);
+    const int4* ur = reinterpret_cast<const int4*>(p.w_rowsum + ng0 + BN / 2);
+    const float4* us = reinterpret_cast<const float4*>(p.w_scale + ng0 + BN / 2);
+    uint32_t hb[kSub / 2];                         // packed bf16 pairs (BF16) 
+    float h[kSub];
+#pragma unroll
+    for (int q = 0; q < kSub / 4; ++q) {
+      const int4 z4g = __ldg(gz + q), r4g = __ldg(gr + q), z4u = __ldg(uz + q), r4u = __ldg(ur + q);
+      const float4 s4g = __ldg(gs + q), s4u = __ldg(us + q);
+      const int32_t zg[4] = {z4g.x, z4g.y, z4g.z, z4g.w}, rg[4] = {r4g.x, r4g.y, r4g.z, r4g.w};
+      const int32_t zu[4] = {z4u.x, z4u.y, z4u.z, z4u.w}, ru[4] = {r4u.x, r4u.y, r4u.z, r4u.w};
+      const float sg4[4] = {s4g.x, s4g.y, s4g.z, s4g.w}, su4[4] = {s4u.x, s4u.y, s4u.z, s4u.w};
+#pragma unroll
+      for (int e2 = 0; e2 < 4; e2 += 2) {
+        const int j = 4 * q + e2;
+        int32_t ai[4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t tg = (uint32_t)rg[e2 + e] - kc * (uint32_t)zg[e2 + e];   // kc == 0: pre-corrected
+          const uint32_t tu = (uint32_t)ru[e2 + e] - kc * (uint32_t)zu[e2 + e];
+          ai[e] = (int32_t)(ag[cur][j + e] + (uint32_t)zg[e2 + e] * nrsa + tg * nza);
+          ai[2 + e] = (int32_t)(au[cur][j + e] + (uint32_t)zu[e2 + e] * nrsa + tu * nza);
+        }
+        const float2 g = __fmul2_rn(make_float2((float)ai[0], (float)ai[1]),
+                                    __fmul2_rn(sa2, make_float2(sg4[e2], sg4[e2 + 1])));
+        const float2 u = __fmul2_rn(make_float2((float)ai[2], (float)ai[3]),
+                                    __fmul2_rn(srw2, make_float2(su4[e2], su4[e2 + 1])));
+        const float2 t = __fmul2_rn(g, nl2);
+        const float2 den = __fadd2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), one2);
+        const float2 sgv = __fmul2_rn(g, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+        const float2 hv = __fmul2_rn(sgv, u);
+        if (BF16) {   // the stored value, which K1 will read
+          const __nv_bfloat162 b = __floats2bfloat162_rn(hv.x, hv.y);
+          hb[j / 2] = *reinterpret_cast<const uint32_t*>(&b);
+          h[j] = __low2float(b);
+          h[j + 1] = __high2float(b);
+        } else {
+          h[j] = hv.x;
+          h[j + 1] = hv.y;
+        }
+      }
+    }
+    if (p.debug_skip_epilogue == 2) {   // timing experiment: math only
+      if (h[0] == 1234.5f && h[kSub - 1] == -1234.5f) static_cast<float*>(p.out)[0] = h[1];
+    } else if (tma) {
+      uint8_t* buf = obuf + (ob & 1u) * 1024;
+      if (lane == 0) bulk_wait_group_read<1>();   // the store that used this buffer has read it
+      __syncwarp();
+      uint4* d = reinterpret_cast<uint4*>(buf + lane * 32);
+      d[0] = make_uint4(hb[0], hb[1], hb[2], hb[3]);
+      d[1] = make_uint4(hb[4], hb[5], hb[6], hb[7]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmO, buf, ti.n0 / 2 + hc, row);   // lane 0 holds the warp's first row
+        bulk_commit_group();
+      }
+      ++ob;
+    }
+    if (p.debug_skip_epilogue != 2 && !tma && rvalid) {
+      const int64_t o = (int64_t)row * p.ldo + ti.n0 / 2 + hc;
+      if (BF16 && p.vec_ok) {
+        uint4* d = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + o);
+        d[0] = make_uint4(hb[0], hb[1], hb[2], hb[3]);
+        d[1] = make_uint4(hb[4], hb[5], hb[6], hb[7]);
+      } else if (BF16) {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.out) + o;
+#pragma unroll
+        for (int j = 0; j < kSub; ++j) d[j] = __float2bfloat16_rn(h[j]);
+      } else {
+        float* d = static_cast<float*>(p.out) + o;
+#pragma unroll
+        for (int j = 0; j < kSub; ++j) d[j] = h[j];
+      }
+    }
+    if (p.debug_skip_epilogue != 2 && rvalid) {
+      if (p.row_ext && p.debug_skip_epilogue != 3) {
+        const float4* t4 = reinterpret_cast<const float4*>(p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + hc);
+        float xs[kSub];
+#pragma unroll
+        for (int q = 0; q < kSub / 4; ++q) {
+          const float4 tt = __ldg(t4 + q);
+          const float2 a = __fmul2_rn(make_float2(h[4 * q], h[4 * q + 1]), make_float2(tt.x, tt.y));
+          const float2 b = __fmul2_rn(make_float2(h[4 * q + 2], h[4 * q + 3]), make_float2(tt.z, tt.w));
+          xs[4 * q] = a.x;
+          xs[4 * q + 1] = a.y;
+          xs[4 * q + 2] = b.x;
+          xs[4 * q + 3] = b.y;
+        }
+        float M = xs[0], m = xs[0];
+#pragma unroll
+        for (int j = 1; j < kSub - 1; j += 2) {
+          M = fmax3f(M, xs[j], xs[j + 1]);
+          m = fmin3f(m, xs[j], xs[j + 1]);
+        }
+        M = fmaxf(M, xs[kSub - 1]);
+        m = fminf(m, xs[kSub - 1]);
+        // records carry a 32-column window start: [col, col + 32) holds the element
+        const int col = ti.n0 / 2 + hc;
+        if (M > ext.M) { ext.M = M; ext.cM = col; }
+        if (m < ext.m) { ext.m = m; ext.cm = col; }
+      }
+    }
+    if (sc + 1 < kNSub) tmem_ld_wait();
+  }
+}
+
 // Epilogue of one tile for one thread: TMEM lane quarter q, column half
 // `half` (8 epilogue warps split the 256 columns), output row `row`.
 template <int BN, int EPI, bool BF16>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase,
-                                              int half, ExtRec& ext) {
+                                              int half, ExtRec& ext, const CUtensorMap* tmO, uint8_t* obuf,
+                                              uint32_t& ob) {
   const bool rvalid = row < ti.m_end;
   float sa = 0.f, rw = 1.f;
   int32_t za = 0, rsa = 0;
@@ -226,7 +396,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
     }
   }
   const int wbase = ti.g * p.N;
-  if (EPI == MOE_EPI_SWIGLU) {
+  if (EPI == MOE_EPI_SWIGLU && p.param_vec_ok && !p.bias && (BN / 4) % 16 == 0) {
+    swiglu_fast<BN, BF16>(p, ti, row, tbase, half, ext, rvalid, sa, rw, za, rsa, tmO, obuf, ob);
+  } else if (EPI == MOE_EPI_SWIGLU) {
     // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
 #pragma unroll 1
     for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
@@ -242,8 +414,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
         load_cols32(p, ng0 + BN / 2, cu);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int32_t ag = zp_correct(vg[j], cg.zw[j], cg.rsw[j], za, rsa, p.K);
-          const int32_t au = zp_correct(vu[j], cu.zw[j], cu.rsw[j], za, rsa, p.K);
+          const int32_t ag = zp_correct(vg[j], cg.zw[j], cg.rsw[j], za, rsa, p.Kc);
+          const int32_t au = zp_correct(vu[j], cu.zw[j], cu.rsw[j], za, rsa, p.Kc);
           float g = (float)ag * (sa * cg.ws[j]);
           float u = (float)au * (sa * cu.ws[j]);
           if (p.bias) {
@@ -258,8 +430,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
         for (int j = 0; j < 32; ++j) {
           const int ng = ng0 + j;
           const int nu = ng + BN / 2;
-          const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.K);
-          const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.K);
+          const int32_t ag = zp_correct(vg[j], p.w_zp[ng], p.w_rowsum[ng], za, rsa, p.Kc);
+          const int32_t au = zp_correct(vu[j], p.w_zp[nu], p.w_rowsum[nu], za, rsa, p.Kc);
           float g = (float)ag * (sa * p.w_scale[ng]);
           float u = (float)au * (sa * p.w_scale[nu]);
           if (p.bias) {
@@ -294,16 +466,16 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
           for (int q = 0; q < 8; ++q) {
             const int4 z = __ldg(wz + q), rs = __ldg(wr + q);
             reinterpret_cast<int4*>(o)[q] =
-                make_int4(zp_correct(v[4 * q], z.x, rs.x, za, rsa, p.K), zp_correct(v[4 * q + 1], z.y, rs.y, za, rsa, p.K),
-                          zp_correct(v[4 * q + 2], z.z, rs.z, za, rsa, p.K),
-                          zp_correct(v[4 * q + 3], z.w, rs.w, za, rsa, p.K));
+                make_int4(zp_correct(v[4 * q], z.x, rs.x, za, rsa, p.Kc), zp_correct(v[4 * q + 1], z.y, rs.y, za, rsa, p.Kc),
+                          zp_correct(v[4 * q + 2], z.z, rs.z, za, rsa, p.Kc),
+                          zp_correct(v[4 * q + 3], z.w, rs.w, za, rsa, p.Kc));
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < nvalid) {
               const int n = wbase + n_lo + j;
-              o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+              o[j] = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.Kc);
             }
           }
         }
@@ -314,7 +486,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
           load_cols32(p, wbase + n_lo, cp);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int32_t a = zp_correct(v[j], cp.zw[j], cp.rsw[j], za, rsa, p.K);
+            const int32_t a = zp_correct(v[j], cp.zw[j], cp.rsw[j], za, rsa, p.Kc);
             float val = (float)a * (sa * cp.ws[j]);
             if (p.bias) val += p.bias[wbase + n_lo + j];
             y[j] = val * rw;
@@ -323,7 +495,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int n = wbase + (j < nvalid ? n_lo + j : n_lo);
-            const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.K);
+            const int32_t a = zp_correct(v[j], p.w_zp[n], p.w_rowsum[n], za, rsa, p.Kc);
             float val = (float)a * (sa * p.w_scale[n]);
             if (p.bias) val += p.bias[n];
             y[j] = val * rw;
@@ -337,7 +509,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
 
 template <int BN, int STAGES, int EPI, bool BF16, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmO, GemmArgs p) {
   using L = Smem<BN, STAGES, CG>;
   constexpr int TM = kBM * CG;  // tile rows (a CTA pair shares one 256-row tile)
   extern __shared__ uint8_t smem_raw[];
@@ -468,6 +641,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int half = (warp - 4) >> 2;  // which half of the tile columns
+    uint8_t* obuf = smem + L::kOutOff + (warp - 4) * 2048;   // this warp's TMA-store staging (2 x 1 KB)
+    uint32_t ob = 0;
     uint32_t tile_it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
       const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN);
@@ -477,7 +652,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
-      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext);
+      if (p.debug_skip_epilogue == 1) {   // timing experiments only: drain TMEM, no math / stores
+        uint32_t v[32];
+        for (int c = 0; c < BN / 64; ++c) tmem_ld32(tbase + (half * (BN / 64) + c) * 32, v);
+        tmem_ld_wait();
+      } else {
+        epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob);
+      }
       tc_fence_before();
       if (CG == 2) mbar_arrive_leader(&tempty[as]);
       else mbar_arrive(&tempty[as]);
@@ -486,6 +667,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         atomicMax(&p.row_ext[2 * (int64_t)row + 1], ext_key(ext.M, ext.cM));
       }
     }
+    if (lane == 0 && ob) bulk_wait_group<0>();   // TMA stores complete before the CTA retires
   }
   tc_fence_before();
   if (CG == 2) cluster_sync_all();
@@ -572,8 +754,8 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
 }
 
 template <int BN, int STAGES, int EPI, bool BF16, int CG>
-static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& p, int grid,
-                            cudaStream_t s) {
+static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const GemmArgs& p,
+                            int grid, cudaStream_t s) {
   auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG>;
   constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
   static bool attr_set = false;
@@ -582,7 +764,7 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
     attr_set = true;
   }
   if (CG == 1) {
-    kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, p);
+    kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, to, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
@@ -596,7 +778,7 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, p));
   }
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
@@ -605,7 +787,7 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
 
 template <int CG>
 static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const uint8_t* w, int64_t N,
-                              int64_t ldw, int num_groups, int epilogue, bool bf16, const GemmArgs& p,
+                              int64_t ldw, int num_groups, int epilogue, bool bf16, GemmArgs p,
                               cudaStream_t s) {
   constexpr int BN = 256;
   constexpr int ST = CG == 2 ? 6 : 4;
@@ -615,6 +797,20 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
     set_error("w8a8_gemm: cuTensorMapEncodeTiled failed");
     return MOE_ECUDA;
   }
+  // SwiGLU bf16 output: stored through shared memory by TMA (32 x 16 boxes)
+  CUtensorMap to = ta;
+  p.tma_out = 0;
+  if (epilogue == MOE_EPI_SWIGLU && bf16 && p.vec_ok && getenv("MOE_B200_NO_TMA_STORE") == nullptr) {
+    auto enc = tensor_map_encoder();
+    cuuint64_t dims[2] = {(cuuint64_t)(N / 2), (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)p.ldo * 2};
+    cuuint32_t box[2] = {16, 32};
+    cuuint32_t es[2] = {1, 1};
+    if (enc && enc(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.out, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.tma_out = 1;
+  }
   const int64_t TM = kBM * CG;
   const int64_t n_tiles = (N + BN - 1) / BN;
   const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
@@ -622,13 +818,13 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
   switch (epilogue) {
     case MOE_EPI_DEQUANT:
-      return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG>(ta, tb, p, grid, s)
-                  : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG>(ta, tb, p, grid, s);
+      return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG>(ta, tb, to, p, grid, s)
+                  : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG>(ta, tb, to, p, grid, s);
     case MOE_EPI_SWIGLU:
-      return bf16 ? launch_tc<BN, ST, MOE_EPI_SWIGLU, true, CG>(ta, tb, p, grid, s)
-                  : launch_tc<BN, ST, MOE_EPI_SWIGLU, false, CG>(ta, tb, p, grid, s);
+      return bf16 ? launch_tc<BN, ST, MOE_EPI_SWIGLU, true, CG>(ta, tb, to, p, grid, s)
+                  : launch_tc<BN, ST, MOE_EPI_SWIGLU, false, CG>(ta, tb, to, p, grid, s);
     default:
-      return launch_tc<BN, ST, MOE_EPI_ACC_I32, false, CG>(ta, tb, p, grid, s);
+      return launch_tc<BN, ST, MOE_EPI_ACC_I32, false, CG>(ta, tb, to, p, grid, s);
   }
 }
 
@@ -645,6 +841,8 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
                                     const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
                                     moe_stream_t stream) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
+  const bool w_corr = (epilogue & MOE_EPI_FLAG_WCORR) != 0;
+  epilogue &= 0xFF;
   if (row_ext) {
     MOE_REQUIRE(epilogue == MOE_EPI_SWIGLU, "w8a8_gemm: row_ext is produced by the SwiGLU epilogue");
     MOE_REQUIRE(next_smooth_recip_f32 && next_ld >= N / 2 && next_ld % 4 == 0,
@@ -669,6 +867,7 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
+  p.Kc = w_corr ? 0 : (int)K;
   p.G = num_groups;
   p.offsets = group_offsets;
   p.a_scale = a_scale;
@@ -693,6 +892,8 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
                  (N % 4 == 0);
   p.param_vec_ok = ((reinterpret_cast<uintptr_t>(w_zp) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w_rowsum) & 15) == 0) &&
                    (!w_scale || (reinterpret_cast<uintptr_t>(w_scale) & 15) == 0) && (N % 4 == 0);
+  static const int skip_epi = getenv("MOE_B200_GEMM_SKIP_EPILOGUE") ? atoi(getenv("MOE_B200_GEMM_SKIP_EPILOGUE")) : 0;
+  p.debug_skip_epilogue = skip_epi;
   cudaStream_t s = as_stream(stream);
   if (row_ext) {
     rowext_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_ext, M);

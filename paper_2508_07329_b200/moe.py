@@ -68,8 +68,8 @@ class MoELayer:
                     raise ValueError("expert weights must be quantized per output row")
             a, b = e["w1"].device(), e["w3"].device()
             w13.append({k: _interleave_rows(a[k], b[k]) for k in ("codes", "scale", "scale_f32", "zp", "rowsum")})
-        self.w13 = {k: torch.cat([p[k] for p in w13], 0).contiguous() for k in w13[0]}
-        self.w2 = _stack_dev([e["w2"] for e in experts])
+        self.w13 = ops.with_wcorr({k: torch.cat([p[k] for p in w13], 0).contiguous() for k in w13[0]})
+        self.w2 = ops.with_wcorr(_stack_dev([e["w2"] for e in experts]))
         self.s13 = torch.stack([torch.as_tensor(np.asarray(_np(e["s13"])), dtype=torch.float64)
                                 for e in experts]).cuda().contiguous()
         self.s2 = torch.stack([torch.as_tensor(np.asarray(_np(e["s2"])), dtype=torch.float64)

@@ -142,13 +142,23 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
         o = out if out is not None else torch.empty((M, cols), dtype=out_dtype, device=dev)
         ldo = o.stride(0)
         odt = L.DT_BF16 if o.dtype == torch.bfloat16 else L.DT_F32
+    # weights may carry the pre-corrected sidecar rowsum - K*zp (with_wcorr)
+    w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
     L.call("moe_w8a8_gemm", L.ptr(ac), M, K, ac.stride(0), L.ptr(a_scale), L.ptr(a_zp), L.ptr(a["rowsum"]),
-           L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w["rowsum"]),
-           L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue, L.ptr(o), odt, ldo,
+           L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w_rs),
+           L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue | flags, L.ptr(o), odt, ldo,
            L.ptr(acc), acc.stride(0) if acc is not None else 0,
            L.ptr(next_smooth_recip_f32),
            next_smooth_recip_f32.shape[-1] if next_smooth_recip_f32 is not None else 0, L.ptr(row_ext), _s())
     return acc if epilogue == L.EPI_ACC_I32 else o
+
+
+def with_wcorr(w: dict) -> dict:
+    """Add the pre-corrected weight sidecar rowsum - K * zp (int32, wrapping)
+    used by the GEMM epilogue instead of rowsum (MOE_EPI_FLAG_WCORR)."""
+    K = w["codes"].shape[1]
+    corr = (w["rowsum"].to(torch.int64) - K * w["zp"].to(torch.int64)).to(torch.int32)
+    return {**w, "rowsum_corr": corr.contiguous()}
 
 
 def quant_sq_error(acc: torch.Tensor, a_scale: torch.Tensor, w_scale: torch.Tensor, ref: torch.Tensor) -> torch.Tensor:

@@ -188,8 +188,10 @@ def test_swiglu_row_ext_feeds_k1(cuda):
     want = _true_records(h.float().cpu().numpy(), recip32.cpu().numpy()[group]).view(np.uint64)
     np.testing.assert_array_equal(e >> np.uint64(32), want >> np.uint64(32))     # extreme values
     cols = (e & np.uint64(0xFFFFFFFF)).astype(np.int64)
-    np.testing.assert_array_equal(xs[r, cols[:, 0]], xs.min(1))                  # columns hold them
-    np.testing.assert_array_equal(xs[r, cols[:, 1]], xs.max(1))
+    # the recorded column starts the 32-column chunk holding the extreme
+    win = np.minimum(cols[:, :, None] + np.arange(32)[None, None, :], xs.shape[1] - 1)
+    assert (xs[r[:, None], win[:, 0]] == xs.min(1)[:, None]).any(axis=1).all()
+    assert (xs[r[:, None], win[:, 1]] == xs.max(1)[:, None]).any(axis=1).all()
     gd = torch.from_numpy(group).to(cuda)
     with_ext = ops.act_quant(h, smooth=s2d, smooth_recip=recip, smooth_recip_f32=recip32, row_group=gd,
                              row_ext=ext)
