@@ -218,17 +218,54 @@ __global__ void __launch_bounds__(512, 1)
     }
     part[buf][warp][lane] = v[0];
     __syncthreads();
-    if (warp == 0) {
+    // warp t finishes token t0 + t: lanes 0..7 = experts (fixed-order
+    // sum over the warps' partials), top-k by shuffle arg-max rounds
+    for (int t = warp; t < kRouterTB; t += nw) {   // d < 1024: fewer than 4 warps
+      const int e = lane & 7;
       float sum = 0.f;
-      for (int ww = 0; ww < nw; ++ww) sum += part[buf][ww][lane];
-      const int t = lane >> 3, e = lane & 7;
+      for (int ww = 0; ww < nw; ++ww) sum += part[buf][ww][t * 8 + e];
       if (gb && e < E) sum += gb[e];
       const int64_t tok = t0 + t;
-      if (logits && tok < T && e < E) logits[tok * E + e] = sum;
-      float l[8];
+      if (logits && tok < T && e < E && lane < 8) logits[tok * E + e] = sum;
+      if (tok < T) {
+        // lanes >= 8 and experts >= E never win
+        float l = (lane < 8 && e < E) ? sum : -INFINITY;
+        float sel[kMaxK];
+        int id[kMaxK];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) l[q] = __shfl_sync(0xffffffffu, sum, (lane & ~7) + q);
-      if (e == 0 && tok < T) topk_select(l, E, k, idx + tok * k, w + tok * k);
+        for (int j = 0; j < kMaxK; ++j) {
+          if (j >= k) break;
+          float bv = l;
+          int bi = lane;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {   // larger value wins, ties -> lower id
+            const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (v2 > bv || (v2 == bv && i2 < bi)) {
+              bv = v2;
+              bi = i2;
+            }
+          }
+          sel[j] = bv;
+          id[j] = bi;
+          if (lane == bi) l = -INFINITY;
+        }
+        if (lane == 0) {
+          float den = 0.f, ex[kMaxK];
+#pragma unroll
+          for (int j = 0; j < kMaxK; ++j) {
+            if (j >= k) break;
+            ex[j] = expf(sel[j] - sel[0]);
+            den += ex[j];
+          }
+#pragma unroll
+          for (int j = 0; j < kMaxK; ++j) {
+            if (j >= k) break;
+            idx[tok * k + j] = id[j];
+            w[tok * k + j] = ex[j] / den;
+          }
+        }
+      }
     }
   }
 }
@@ -243,7 +280,7 @@ __global__ void router_topk_kernel(const float* logits, int64_t T, int E, int k,
 
 // ── stable counting sort ───────────────────────────────────────────────────
 constexpr int kPermThreads = 256;
-constexpr int kPermChunk = 4096;  // (token, slot) pairs per block
+constexpr int kPermChunk = 1024;  // (token, slot) pairs per block
 
 __global__ void permute_count_kernel(const int32_t* idx, int64_t n, int E, int32_t* block_counts) {
   __shared__ int cnt[kMaxE];

@@ -290,10 +290,12 @@ def test_swiglu_epilogue(cuda):
 
 
 # ── K3 / K4 / K6 ─────────────────────────────────────────────────────────
-@pytest.mark.parametrize("E,k", [(8, 2), (16, 4), (5, 1)])
-def test_router_gate_topk(cuda, E, k):
-    rng = np.random.default_rng(E * 10 + k)
-    T, d = 2048, 1024
+@pytest.mark.parametrize("E,k,T,d", [(8, 2, 2048, 1024), (16, 4, 2048, 1024), (5, 1, 2048, 1024),
+                                     (8, 2, 333, 256), (8, 2, 1001, 4096), (7, 3, 517, 512), (8, 2, 77, 96)])
+def test_router_gate_topk(cuda, E, k, T, d):
+    """Register-gate kernel (d % 256 == 0, d <= 4096, E <= 8: 1-16 warps per
+    CTA, ragged token batches), the shared-memory and the generic kernels."""
+    rng = np.random.default_rng(E * 10 + k + d)
     x = _acts(rng, T, d, scale=3.0)
     wg = (rng.normal(size=(E, d)) / np.sqrt(d)).astype(np.float32)
     logits, idx, w = ops.router_gate(torch.from_numpy(x).to(cuda).bfloat16(), torch.from_numpy(wg).to(cuda), k)
