@@ -58,6 +58,7 @@ struct GemmArgs {
   int param_vec_ok;  // W zp / rowsum / scale tables allow 16-byte vector loads
   int debug_skip_epilogue;  // MOE_B200_GEMM_SKIP_EPILOGUE=1: timing experiments only
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
+  int band;                 // m-tiles per raster band (map_tile)
   // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
   const float* ns_rs32;
   int64_t ns_ld;
@@ -82,14 +83,30 @@ struct TileInfo {
   int g, m0, m_end, n0;
 };
 
-// tile t -> (group, first row, group end, first column); tiles of TM rows,
-// m fastest within an N block so a group's weight block is reused in L2.
-__device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start, const int* off, int TM, int BN) {
+// tile t -> (group, first row, group end, first column). Within a group the
+// m-tiles are walked in bands of `band` tiles: for each band every N block,
+// m fastest inside the band. A band's activations (band * TM * K bytes) stay
+// L2-resident while the weight blocks stream past them; the host sizes the
+// band so that this fits (whole group when K is small, e.g. W13 at K=4096;
+// 8 tiles for W2 at K=14336, where the full 59 MB group slice thrashed L2).
+__device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start, const int* off, int TM, int BN,
+                                             int n_tiles, int band) {
   int g = 0;
   while (g + 1 < G && t >= tile_start[g + 1]) ++g;
   const int local = t - tile_start[g];
   const int mt = (off[g + 1] - off[g] + TM - 1) / TM;
-  const int n_tile = local / mt, m_tile = local - n_tile * mt;
+  const int bs = band < mt ? band : mt;
+  const int full = mt / bs;                       // complete bands
+  int m_tile, n_tile;
+  if (local < full * bs * n_tiles) {
+    const int b = local / (bs * n_tiles), w = local - b * bs * n_tiles;
+    n_tile = w / bs;
+    m_tile = b * bs + (w - n_tile * bs);
+  } else {                                        // trailing partial band
+    const int rm = mt - full * bs, w = local - full * bs * n_tiles;
+    n_tile = w / rm;
+    m_tile = full * bs + (w - n_tile * rm);
+  }
   return TileInfo{g, off[g] + m_tile * TM, off[g + 1], n_tile * BN};
 }
 
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0;
     for (int t = unit; t < total_tiles; t += n_units) {
-      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN);
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const int arow = ti.m0 + (int)rank * kBM;
       const int wrow = ti.g * p.N + ti.n0 + (int)rank * (BN / CG);
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
@@ -645,7 +662,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t ob = 0;
     uint32_t tile_it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
-      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN);
+      const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
@@ -813,6 +830,11 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   }
   const int64_t TM = kBM * CG;
   const int64_t n_tiles = (N + BN - 1) / BN;
+  // raster band: keep ~24 MB of activations L2-resident per band
+  {
+    static const int64_t budget = getenv("MOE_B200_BAND_MB") ? atoll(getenv("MOE_B200_BAND_MB")) << 20 : (24LL << 20);
+    p.band = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 20, budget / (TM * std::max<int64_t>(K, 1))));
+  }
   const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
   const int64_t max_units = num_sms() / CG;
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
