@@ -15,9 +15,12 @@ experts = [{"w1": rng.normal(size=(F, D)) * 0.03, "w3": rng.normal(size=(F, D)) 
 wg = (rng.normal(size=(E, D)) / np.sqrt(D)).astype(np.float32)
 
 
+OUTLIERS = rng.choice(D, D // 100, replace=False)    # a property of the model: same channels in every batch
+
+
 def toks(T):
     x = rng.normal(size=(T, D))
-    x[:, rng.choice(D, D // 100, replace=False)] *= 50.0
+    x[:, OUTLIERS] *= 50.0
     return torch.from_numpy(x.astype(np.float32)).cuda().bfloat16().float()
 
 
