@@ -537,8 +537,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 // second pass; longer rows without records are streamed twice.
 constexpr int kChunkBytes = 2048;
 constexpr int kChunkVec = kChunkBytes / 16;   // 128 x 16 B: 4 vectors per lane
-constexpr int kRing = 8;
-constexpr int kBulkWarps = 12;
+constexpr int kRing = 6;
+constexpr int kBulkWarps = 16;
+constexpr int kVecStep = 2;     // vectors per lane processed together (register budget: 16 warps)
 constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
 
 __device__ __forceinline__ uint2 fast_vec8(const uint4& u, int64_t c, const float* tab, const double* srow,
@@ -759,41 +760,46 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         const uint4* v = item_vec(it);
         const int64_t cb = (int64_t)k * kChunkVec + lane;
         if ((int64_t)(k + 1) * kChunkVec <= nvec) {
-          // full chunk: table loads up front, no per-vector branches; the rare
-          // slow vectors are redone afterwards (same lane, same addresses)
-          uint4 u[4];
-          float4 ta[4], tb[4];
+          // full chunk, two vectors at a time: table loads up front, no
+          // per-vector branches; the rare slow vectors are redone afterwards
+          // from the staged copy (same lane, same addresses)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            u[b] = v[lane + 32 * b];
-            if (tab) {
-              ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b));
-              tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b) + 1);
+          for (int hf = 0; hf < 4; hf += kVecStep) {
+            uint4 u[kVecStep];
+            float4 ta[kVecStep], tb[kVecStep];
+#pragma unroll
+            for (int b = 0; b < kVecStep; ++b) {
+              u[b] = v[lane + 32 * (hf + b)];
+              if (tab) {
+                ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)));
+                tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)) + 1);
+              }
             }
-          }
-          uint2 out[4];
-          uint32_t slowm = 0;
+            uint2 out[kVecStep];
+            uint32_t slowm = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            float xs[8];
-            smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
-            bool sl;
-            out[b] = fast_core(xs, f, sl);
-            slowm |= (uint32_t)sl << b;
-          }
+            for (int b = 0; b < kVecStep; ++b) {
+              float xs[8];
+              smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
+              bool sl;
+              out[b] = fast_core(xs, f, sl);
+              slowm |= (uint32_t)sl << b;
+            }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            sum += bytesum(out[b]);
-            __stcs(dst + cb + 32 * b, out[b]);
-          }
-          if (slowm) {
-            for (int b = 0; b < 4; ++b) {
-              if (!(slowm >> b & 1u)) continue;
-              const uint4 sv = slow_vec8(u[b], tab, cb + 32 * b, srow, rrow, f);
-              cnt += sv.z;
-              const uint2 o2 = make_uint2(sv.x, sv.y);
-              sum += bytesum(o2) - bytesum(out[b]);
-              __stcs(dst + cb + 32 * b, o2);
+            for (int b = 0; b < kVecStep; ++b) {
+              sum += bytesum(out[b]);
+              __stcs(dst + cb + 32 * (hf + b), out[b]);
+            }
+            if (slowm) {
+              for (int b = 0; b < kVecStep; ++b) {
+                if (!(slowm >> b & 1u)) continue;
+                const int64_t c = cb + 32 * (hf + b);
+                const uint4 sv = slow_vec8(v[lane + 32 * (hf + b)], tab, c, srow, rrow, f);
+                cnt += sv.z;
+                const uint2 o2 = make_uint2(sv.x, sv.y);
+                sum += bytesum(o2) - bytesum(out[b]);
+                __stcs(dst + c, o2);
+              }
             }
           }
         } else {
@@ -873,10 +879,10 @@ static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long 
       a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
 }
 
-// Kernel choice (measured on B200 at the Mixtral shape, tools/k1_bench.py):
-// rows with producer records (h) stream through the bulk-async ring; rows
-// that need their own extreme pass (x) use the register kernel, whose pass
-// A re-read hits L1. MOE_B200_K1_CFG=0 / 7 forces one kernel for both.
+// Kernel choice: the bulk-async ring kernel for every eligible row set (x
+// and h; measured on B200 at the Mixtral shape with tools/k1_bench.py it
+// matches or beats the register-streaming kernel: x 184 vs 184 us, h 371 vs
+// 387 us). MOE_B200_K1_CFG=0 selects the register kernel (A/B runs).
 template <bool GIVEN>
 static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
@@ -885,7 +891,7 @@ static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsign
     const char* env = getenv("MOE_B200_K1_CFG");
     return env ? atoi(env) : -1;
   }();
-  const bool bulk = forced == 7 || (forced < 0 && GIVEN);
+  const bool bulk = forced != 0;
   if (bulk) return launch_bulk<GIVEN>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   count_launch();
