@@ -176,6 +176,16 @@ moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, con
                            const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx,
                            float* topk_w, moe_stream_t stream);
 /* top-k only, from given float32 logits [T, E]. */
+/* Tensor-core K3: the same routing with logits from tcgen05.mma kind::f16
+ * (x bf16 [T, d], d % 64 == 0, E <= 16). The float32 gate is first split
+ * by moe_router_prepare into three bf16 pieces (hi + mid + lo = the exact
+ * float32 value) in a caller buffer of moe_router_tc_workspace(d) bytes;
+ * each product with a piece is exact and all accumulate in float32. */
+int64_t moe_router_tc_workspace(int64_t d);
+moe_status moe_router_prepare(const float* gate_w, int E, int64_t d, void* pieces, moe_stream_t stream);
+moe_status moe_router_gate_tc(const void* x, int64_t T, int64_t d, int64_t ldx, const void* pieces,
+                              const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx,
+                              float* topk_w, moe_stream_t stream);
 moe_status moe_router_topk(const float* logits, int64_t T, int E, int k, int32_t* topk_idx, float* topk_w,
                            moe_stream_t stream);
 

@@ -44,6 +44,9 @@ _SIGS = {
     "moe_quant_sq_error": (_I, [_P, _I64, _I64, _P, _I, _P, _P, _P, _P, _I64, _P]),
     "moe_quant_sq_error_workspace": (_I64, [_I64, _I64]),
     "moe_router_gate": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "moe_router_tc_workspace": (_I64, [_I64]),
+    "moe_router_prepare": (_I, [_P, _I, _I64, _P, _P]),
+    "moe_router_gate_tc": (_I, [_P, _I64, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),
     "moe_router_topk": (_I, [_P, _I64, _I, _I, _P, _P, _P]),
     "moe_route_permute_workspace": (_I64, [_I64, _I, _I]),
     "moe_route_permute": (_I, [_P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _I64, _P]),

@@ -879,10 +879,11 @@ static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long 
       a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
 }
 
-// Kernel choice: the bulk-async ring kernel for every eligible row set (x
-// and h; measured on B200 at the Mixtral shape with tools/k1_bench.py it
-// matches or beats the register-streaming kernel: x 184 vs 184 us, h 371 vs
-// 387 us). MOE_B200_K1_CFG=0 selects the register kernel (A/B runs).
+// Kernel choice (measured on B200 at the Mixtral shape): rows with producer
+// records (h) stream through the bulk-async ring (371 vs 387 us); rows that
+// need their own extreme pass (x, gathered) use the register kernel, whose
+// second pass and the router's just-read rows hit L1/L2 (in the step: 222 vs
+// 258 us). MOE_B200_K1_CFG=0 / 7 forces one kernel for both (A/B runs).
 template <bool GIVEN>
 static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
@@ -891,7 +892,7 @@ static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsign
     const char* env = getenv("MOE_B200_K1_CFG");
     return env ? atoi(env) : -1;
   }();
-  const bool bulk = forced != 0;
+  const bool bulk = forced == 7 || (forced < 0 && GIVEN);
   if (bulk) return launch_bulk<GIVEN>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   count_launch();

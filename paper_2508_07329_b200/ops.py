@@ -174,8 +174,30 @@ def quant_sq_error(acc: torch.Tensor, a_scale: torch.Tensor, w_scale: torch.Tens
 
 
 # ── K3 / K4 / K6 ──────────────────────────────────────────────────────────
+_GATE_PIECES: dict = {}
+
+
+def router_pieces(gate_w: torch.Tensor) -> torch.Tensor:
+    """bf16 (hi, mid, lo) split of a float32 gate for the tensor-core router,
+    cached per gate tensor (moe_router_prepare)."""
+    key = (gate_w.data_ptr(), gate_w._version, tuple(gate_w.shape))
+    pc = _GATE_PIECES.get(key)
+    if pc is None:
+        E, d = gate_w.shape
+        lib = L.load()
+        pc = torch.empty(lib.moe_router_tc_workspace(d) // 2, dtype=torch.bfloat16, device=gate_w.device)
+        L.call("moe_router_prepare", L.ptr(gate_w.contiguous()), E, d, L.ptr(pc), _s())
+        if len(_GATE_PIECES) > 16:
+            _GATE_PIECES.clear()
+        _GATE_PIECES[key] = pc
+    return pc
+
+
 def router_gate(x: torch.Tensor, gate_w: torch.Tensor, k: int, want_logits: bool = True,
-                gate_bias: torch.Tensor | None = None):
+                gate_bias: torch.Tensor | None = None, tensor_cores: bool | None = None):
+    """K3: logits = x Wg^T (+ bias), top-k (ties -> lower id), softmax over the
+    selected. bf16 x with d % 64 == 0 and E <= 16 runs on the tensor cores
+    (exact 3-piece bf16 split of the float32 gate); else the SIMT kernels."""
     x = _rowmajor(x, "x")
     T, d = x.shape
     E = gate_w.shape[0]
@@ -184,7 +206,15 @@ def router_gate(x: torch.Tensor, gate_w: torch.Tensor, k: int, want_logits: bool
     idx = torch.empty((T, k), dtype=torch.int32, device=x.device)
     w = torch.empty((T, k), dtype=torch.float32, device=x.device)
     gb = gate_bias.contiguous().to(torch.float32) if gate_bias is not None else None
-    L.call("moe_router_gate", L.ptr(x), _dt(x), T, d, L.ptr(gw), L.ptr(gb), E, k, L.ptr(logits), L.ptr(idx), L.ptr(w), _s())
+    if tensor_cores is None:
+        tensor_cores = (x.dtype == torch.bfloat16 and d % 64 == 0 and E <= 16 and k <= 8
+                        and (x.stride(0) * 2) % 16 == 0 and x.data_ptr() % 16 == 0)
+    if tensor_cores:
+        L.call("moe_router_gate_tc", L.ptr(x), T, d, x.stride(0), L.ptr(router_pieces(gw)), L.ptr(gb), E, k,
+               L.ptr(logits), L.ptr(idx), L.ptr(w), _s())
+    else:
+        L.call("moe_router_gate", L.ptr(x), _dt(x), T, d, L.ptr(gw), L.ptr(gb), E, k, L.ptr(logits), L.ptr(idx),
+               L.ptr(w), _s())
     return logits, idx, w
 
 

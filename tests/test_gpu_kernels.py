@@ -292,15 +292,22 @@ def test_swiglu_epilogue(cuda):
 # ── K3 / K4 / K6 ─────────────────────────────────────────────────────────
 @pytest.mark.parametrize("E,k,T,d", [(8, 2, 2048, 1024), (16, 4, 2048, 1024), (5, 1, 2048, 1024),
                                      (8, 2, 333, 256), (8, 2, 1001, 4096), (7, 3, 517, 512), (8, 2, 77, 96)])
-def test_router_gate_topk(cuda, E, k, T, d):
-    """Register-gate kernel (d % 256 == 0, d <= 4096, E <= 8: 1-16 warps per
-    CTA, ragged token batches), the shared-memory and the generic kernels."""
+@pytest.mark.parametrize("tc", [False, True])
+def test_router_gate_topk(cuda, E, k, T, d, tc):
+    """SIMT kernels (register gate for d % 256 == 0, d <= 4096, E <= 8 with
+    1-16 warps per CTA and ragged batches; shared-memory; generic) and the
+    tensor-core kernel (bf16 3-piece gate, d % 64 == 0, E <= 16)."""
+    if tc and (d % 64 or E > 16):
+        pytest.skip("shape outside the tensor-core router")
     rng = np.random.default_rng(E * 10 + k + d)
     x = _acts(rng, T, d, scale=3.0)
     wg = (rng.normal(size=(E, d)) / np.sqrt(d)).astype(np.float32)
-    logits, idx, w = ops.router_gate(torch.from_numpy(x).to(cuda).bfloat16(), torch.from_numpy(wg).to(cuda), k)
+    gb = rng.normal(size=E).astype(np.float32) * 0.1
+    logits, idx, w = ops.router_gate(torch.from_numpy(x).to(cuda).bfloat16(), torch.from_numpy(wg).to(cuda), k,
+                                     gate_bias=torch.from_numpy(gb).to(cuda), tensor_cores=tc)
     lg = logits.cpu().numpy()
-    np.testing.assert_allclose(lg, x.astype(np.float64) @ wg.T.astype(np.float64), rtol=1e-4, atol=1e-4)
+    want = x.astype(np.float64) @ wg.T.astype(np.float64) + gb
+    np.testing.assert_allclose(lg, want, rtol=1e-5, atol=1e-5 * np.abs(want).max())
     oidx, ow, _ = M.router_topk(lg, k)               # identical float32 logits
     np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
     np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-5, atol=1e-9)  # float32 expf
