@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runtime even at N=1 (validation)")
+    ap.add_argument("--ep-transport", choices=("peer", "nccl"), default="peer",
+                    help="EP: peer-memory fused dispatch/combine (symmetric memory) or NCCL all-to-all")
     ap.add_argument("--ep-stage1", type=int, default=1, help="EP (N>1): plan_two_stage path residents per layer")
     ap.add_argument("--ep-stage2", type=int, default=1, help="EP (N>1): frequency supplement per layer")
     return ap.parse_args()
@@ -225,12 +227,20 @@ def main() -> None:
     if world > 1 or args.ep:
         # expert parallelism: plan_two_stage over the GPU-measured routing of
         # all ranks -> replicated residents, the rest bin-packed (ep.py)
-        from paper_2508_07329_b200.ep import CudaExpertBackend, ExpertParallelMoE, plan_placement
+        from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertParallelMoE, PeerBuffers,
+                                              PeerExpertParallelMoE, plan_placement)
         placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
-        model = ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank)),
-                                  placement)
+        backend = CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank))
+        if args.ep_transport == "peer":
+            # receive capacity: every rank could route all its tokens to one owner
+            bufs = (PeerBuffers.symmetric(D, world * T * TOPK, T * TOPK) if world > 1
+                    else PeerBuffers.loopback(1, D, T * TOPK, T * TOPK)[0])
+            model = PeerExpertParallelMoE(backend, placement, bufs)
+        else:
+            model = ExpertParallelMoE(backend, placement)
         counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
-        ep_info = {"replicated": list(placement.replicated), "owner": list(placement.owner),
+        ep_info = {"transport": args.ep_transport, "replicated": list(placement.replicated),
+                   "owner": list(placement.owner),
                    "local_fraction_est": placement.local_fraction(counts)}
         del layer.w13, layer.w2            # this rank keeps only its local experts' weights
         torch.cuda.empty_cache()

@@ -257,6 +257,31 @@ moe_status moe_ep_pack_params(const float* scale_f32, const int32_t* zp, const i
 moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, float* scale_f32,
                                 int32_t* zp, int32_t* rowsum, float* weight, moe_stream_t stream);
 
+/* Fused expert-parallel transport (peer memory over NVLink instead of an
+ * NCCL all-to-all; buffers from torch symmetric memory):
+ * act_quant_dispatch: K1 on gathered rows (as moe_act_quant per_token with
+ *   gather_rows / row_group) writing each row's codes straight into
+ *   codes_tab[dst_rank[r]] + dst_row[r] * ldc and its 16-byte sidecar
+ *   (scale_f32, zp, rowsum, routing weight) into params_tab[...][dst_row[r]].
+ * w8a8_gemm_scatter: moe_w8a8_gemm (DEQUANT) whose output row m is stored at
+ *   out_tab[out_rank[m]] + out_row[m] * ldo (the combine's home buffers).
+ * block_map: for rows in contiguous blocks [block_start[b], block_start[b+1]),
+ *   out0[i] = val0[b], out1[i] = val1[b] + i - block_start[b] (the
+ *   destination rank / row of every dispatched or returned row). */
+moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                                  const int32_t* gather_rows, const double* smooth, const double* smooth_recip,
+                                  const float* smooth_recip_f32, const int32_t* row_group, int bits, int symmetric,
+                                  void* const* codes_tab, void* const* params_tab, const int32_t* dst_rank,
+                                  const int32_t* dst_row, const float* row_weight, int64_t ldc, moe_stream_t stream);
+moe_status moe_w8a8_gemm_scatter(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                                 const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                                 int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,
+                                 const float* bias, const float* row_weight, const int32_t* group_offsets,
+                                 int num_groups, int epilogue, void* const* out_tab, const int32_t* out_rank,
+                                 const int32_t* out_row, int out_dtype, int64_t ldo, moe_stream_t stream);
+moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
+                         const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
     const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
     const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
-    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+    uint2* dst = reinterpret_cast<uint2*>(out_row_ptr(a, codes, ldc, r));
 
     // (value, column) records of the float32 extremes: producer's, or pass A
     RowExt rec;
@@ -519,12 +519,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     }
     if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
     if (lane == 0) {
-      if (rowsum) rowsum[r] = sum;
-      scale[r] = p.scale;
-      if (scale_f32) scale_f32[r] = (float)p.scale;
-      zp[r] = p.zp;
+      if (a.ep.codes_tab) {
+        const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
+        a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
+            make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
+      } else {
+        if (rowsum) rowsum[r] = sum;
+        scale[r] = p.scale;
+        if (scale_f32) scale_f32[r] = (float)p.scale;
+        zp[r] = p.zp;
+      }
     }
   }
+  if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
 }
 
 // ── bulk-async (TMA) streaming variant ─────────────────────────────────────
@@ -663,7 +670,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
     const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
     const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
-    uint2* dst = reinterpret_cast<uint2*>(codes + r * ldc);
+    uint2* dst = reinterpret_cast<uint2*>(out_row_ptr(a, codes, ldc, r));
     const uint32_t base = ccount;
     ccount += items_per_row;
 
@@ -831,12 +838,19 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     }
     if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
     if (lane == 0) {
-      if (rowsum) rowsum[r] = sum;
-      scale[r] = p.scale;
-      if (scale_f32) scale_f32[r] = (float)p.scale;
-      zp[r] = p.zp;
+      if (a.ep.codes_tab) {
+        const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
+        a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
+            make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
+      } else {
+        if (rowsum) rowsum[r] = sum;
+        scale[r] = p.scale;
+        if (scale_f32) scale_f32[r] = (float)p.scale;
+        zp[r] = p.zp;
+      }
     }
   }
+  if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
 }
 
 template <bool GIVEN>

@@ -51,6 +51,22 @@ __global__ void unpack_params_kernel(const int4* params, const int32_t* index, i
   }
 }
 
+// rows grouped in contiguous blocks [start[b], start[b+1]): out0[i] = val0[b],
+// out1[i] = val1[b] + (i - start[b])   (binary search over nb blocks)
+__global__ void block_map_kernel(int64_t n, int nb, const int32_t* start, const int32_t* val0, const int32_t* val1,
+                                 int32_t* out0, int32_t* out1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nb;   // last b with start[b] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (start[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    out0[i] = val0[lo];
+    out1[i] = val1[lo] + (int32_t)(i - start[lo]);
+  }
+}
+
 static unsigned grid_for(int64_t n, int per_block) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per_block - 1) / per_block, 8 * (int64_t)num_sms()));
 }
@@ -111,6 +127,16 @@ extern "C" moe_status moe_ep_unpack_params(const int32_t* params, const int32_t*
   if (n == 0) return MOE_OK;
   unpack_params_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(reinterpret_cast<const int4*>(params), index,
                                                                          n, scale_f32, zp, rowsum, weight);
+  ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
+                                    const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream) {
+  MOE_REQUIRE(n >= 0 && nblocks >= 1 && block_start && val0 && val1 && out0 && out1, "block_map: bad arguments");
+  if (n == 0) return MOE_OK;
+  block_map_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, nblocks, block_start, val0, val1, out0, out1);
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;

@@ -59,6 +59,9 @@ struct GemmArgs {
   int debug_skip_epilogue;  // MOE_B200_GEMM_SKIP_EPILOGUE=1: timing experiments only
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   int band;                 // m-tiles per raster band (map_tile)
+  void* const* out_tab;     // DEQUANT: row m goes to out_tab[out_rank[m]] + out_row[m] * ldo (EP combine)
+  const int32_t* out_rank;
+  const int32_t* out_row;
   // optional (SwiGLU): float32 per-row bounds of stored output * RN32(1/s_next)
   const float* ns_rs32;
   int64_t ns_ld;
@@ -518,7 +521,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
             y[j] = val * rw;
           }
         }
-        store32<BF16>(p.out, (int64_t)row * p.ldo + n_lo, y, nvalid, p.vec_ok);
+        void* obase = p.out_tab ? p.out_tab[p.out_rank[row]] : p.out;
+        const int64_t orow = p.out_tab ? (int64_t)p.out_row[row] : (int64_t)row;
+        store32<BF16>(obase, orow * p.ldo + n_lo, y, nvalid, p.vec_ok);
       }
     }
   }
@@ -854,14 +859,14 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
 
 using namespace moe;
 
-extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
-                                    const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
-                                    int64_t ldw, const float* w_scale, const int32_t* w_zp,
-                                    const int32_t* w_rowsum, const float* bias, const float* row_weight,
-                                    const int32_t* group_offsets, int num_groups, int epilogue, void* out,
-                                    int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                                    const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
-                                    moe_stream_t stream) {
+static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                             const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N, int64_t ldw,
+                             const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum, const float* bias,
+                             const float* row_weight, const int32_t* group_offsets, int num_groups, int epilogue,
+                             void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
+                             const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
+                             void* const* out_tab, const int32_t* out_rank, const int32_t* out_row,
+                             moe_stream_t stream) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
   const bool w_corr = (epilogue & MOE_EPI_FLAG_WCORR) != 0;
   epilogue &= 0xFF;
@@ -907,6 +912,9 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   p.ns_rs32 = next_smooth_recip_f32;
   p.ns_ld = next_ld;
   p.row_ext = row_ext;
+  p.out_tab = out_tab;
+  p.out_rank = out_rank;
+  p.out_row = out_row;
   const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
   p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
   p.acc_vec_ok = acc_out && ((reinterpret_cast<uintptr_t>(acc_out) & 15) == 0) && (ld_acc % 4 == 0) &&
@@ -940,4 +948,32 @@ extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int6
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
+}
+
+extern "C" moe_status moe_w8a8_gemm(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                                    const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                                    int64_t ldw, const float* w_scale, const int32_t* w_zp,
+                                    const int32_t* w_rowsum, const float* bias, const float* row_weight,
+                                    const int32_t* group_offsets, int num_groups, int epilogue, void* out,
+                                    int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
+                                    const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
+                                    moe_stream_t stream) {
+  return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, bias, row_weight,
+                    group_offsets, num_groups, epilogue, out, out_dtype, ldo, acc_out, ld_acc, next_smooth_recip_f32,
+                    next_ld, row_ext, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" moe_status moe_w8a8_gemm_scatter(const uint8_t* a, int64_t M, int64_t K, int64_t lda,
+                                            const float* a_scale, const int32_t* a_zp, const int32_t* a_rowsum,
+                                            const uint8_t* w, int64_t N, int64_t ldw, const float* w_scale,
+                                            const int32_t* w_zp, const int32_t* w_rowsum, const float* bias,
+                                            const float* row_weight, const int32_t* group_offsets, int num_groups,
+                                            int epilogue, void* const* out_tab, const int32_t* out_rank,
+                                            const int32_t* out_row, int out_dtype, int64_t ldo, moe_stream_t stream) {
+  MOE_REQUIRE(out_tab && out_rank && out_row, "w8a8_gemm_scatter: null output table");
+  MOE_REQUIRE((epilogue & 0xFF) == MOE_EPI_DEQUANT, "w8a8_gemm_scatter: dequant epilogue only");
+  // the vector-store check inspects `out`: the table's buffers share the allocation granularity
+  return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, bias, row_weight,
+                    group_offsets, num_groups, epilogue, const_cast<void*>(reinterpret_cast<const void*>(out_tab)),
+                    out_dtype, ldo, nullptr, 0, nullptr, 0, nullptr, out_tab, out_rank, out_row, stream);
 }

@@ -15,6 +15,17 @@ struct SmoothArgs {
   int64_t cols;
 };
 
+// Expert-parallel dispatch output: rows go straight into the receive
+// buffers of their destination ranks (peer memory over NVLink), with the
+// 16-byte sidecar (scale_f32, zp, rowsum, routing weight) beside them.
+struct EpOut {
+  uint8_t* const* codes_tab;   // [W] receive-buffer base per rank; NULL: ordinary local output
+  int4* const* params_tab;     // [W] sidecar base per rank
+  const int32_t* dst_rank;     // [rows]
+  const int32_t* dst_row;      // [rows]
+  const float* weight;         // [rows] routing weight (sidecar .w); NULL -> 1
+};
+
 struct RowArgs {
   const void* x;
   int dt;
@@ -22,7 +33,12 @@ struct RowArgs {
   const int32_t* gather;  // output row -> input row (optional)
   const int32_t* group;   // output row -> smoothing table row (optional)
   SmoothArgs sm;
+  EpOut ep;               // optional (zero: local output arrays)
 };
+
+__device__ __forceinline__ uint8_t* out_row_ptr(const RowArgs& a, uint8_t* codes, int64_t ldc, int64_t r) {
+  return a.ep.codes_tab ? a.ep.codes_tab[a.ep.dst_rank[r]] + (int64_t)a.ep.dst_row[r] * ldc : codes + r * ldc;
+}
 
 struct RowView {
   int64_t off;    // element offset of the source row

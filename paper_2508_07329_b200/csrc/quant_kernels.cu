@@ -256,3 +256,26 @@ extern "C" moe_status moe_channel_stats(const double* x, int64_t n, int64_t T, i
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }
+
+extern "C" moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                                             const int32_t* gather_rows, const double* smooth,
+                                             const double* smooth_recip, const float* smooth_recip_f32,
+                                             const int32_t* row_group, int bits, int symmetric,
+                                             void* const* codes_tab, void* const* params_tab,
+                                             const int32_t* dst_rank, const int32_t* dst_row, const float* row_weight,
+                                             int64_t ldc, moe_stream_t stream) {
+  MOE_REQUIRE(x && gather_rows && codes_tab && params_tab && dst_rank && dst_row, "act_quant_dispatch: null pointer");
+  MOE_REQUIRE(rows >= 1 && cols >= 1 && ldx >= cols && ldc >= cols, "act_quant_dispatch: bad sizes");
+  MOE_REQUIRE(x_dtype == MOE_DT_BF16 && smooth && smooth_recip && smooth_recip_f32,
+              "act_quant_dispatch: bf16 rows with divide-smoothing tables (f64, RN(1/s) and its f32 copy)");
+  MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
+  RowArgs a{x, x_dtype, rows, cols, ldx, gather_rows, row_group, SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, cols}};
+  a.ep = EpOut{reinterpret_cast<uint8_t* const*>(codes_tab), reinterpret_cast<int4* const*>(params_tab), dst_rank,
+               dst_row, row_weight};
+  cudaError_t err = cudaSuccess;
+  MOE_REQUIRE(launch_act_quant_fast(a, smooth_recip_f32, bits, symmetric, nullptr, ldc, nullptr, nullptr, nullptr,
+                                    nullptr, as_stream(stream), &err),
+              "act_quant_dispatch: needs cols % 8 == 0 and 16-byte aligned rows");
+  MOE_CUDA_TRY(err);
+  return MOE_OK;
+}

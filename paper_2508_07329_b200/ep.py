@@ -248,6 +248,90 @@ class ExpertParallelMoE:
         return out_host
 
 
+def _peer_counts_all(ex, send_counts: np.ndarray) -> np.ndarray:
+    """All ranks' [W, E] send counts -> C[s, r, e] (one small all-gather)."""
+    if getattr(ex, "world", 1) == 1 or ex.dist is None:
+        return send_counts[None]
+    t = torch.as_tensor(send_counts, dtype=torch.int64, device="cuda").contiguous()
+    out = torch.empty((ex.world,) + tuple(t.shape), dtype=torch.int64, device="cuda")
+    ex.dist.all_gather_into_tensor(out, t, group=ex.group)
+    return out.cpu().numpy()
+
+
+class PeerExpertParallelMoE(ExpertParallelMoE):
+    """Expert-parallel forward over peer memory (no bulk NCCL traffic):
+    K1 writes every dispatched row straight into its owner's receive buffer
+    (already expert-contiguous, so no regroup), the owner's GEMM2 epilogue
+    writes each output row straight into the home rank's ``yhome`` slot, and
+    the home rank combines locally. Per forward: one small all-gather of the
+    [W, E] counts and two cross-rank barriers."""
+
+    def __init__(self, backend, placement: ExpertPlacement, buffers: PeerBuffers, exchange=None,
+                 rank: int | None = None):
+        super().__init__(backend, placement, exchange, rank)
+        self.bufs = buffers
+
+    def peer_prepare(self, x):
+        W, E = self.pl.world, self.pl.experts
+        idx, w = self.be.route(x)
+        keys = self.be.route_keys(idx, self.dest, E)
+        perm = self.be.permute(keys, w, W * E)
+        off = self.be.to_host(perm["offsets"]).astype(np.int64)
+        return DispatchState(x.shape[0], perm, [x], np.diff(off).reshape(W, E))
+
+    def peer_send(self, st: DispatchState, C: np.ndarray):
+        rank_of, base = peer_send_layout(C, self.rank, self.pl)
+        n = st.perm["src_token"].numel()
+        if n == 0:
+            return
+        dst_rank, dst_row = ops.block_map(n, st.perm["offsets"], self.be.to_index_tensor(rank_of),
+                                          self.be.to_index_tensor(base))
+        self.be.dispatch_send(st.payload[0], st.perm, self.pl.experts, self.bufs, dst_rank, dst_row)
+
+    def peer_compute(self, C: np.ndarray, mark=None):
+        starts, ranks, homes, counts = peer_recv_layout(C, self.rank, self.local)
+        R = int(starts[-1])
+        if R == 0:
+            return
+        out_rank, out_row = ops.block_map(R, self.be.to_index_tensor(starts), self.be.to_index_tensor(ranks),
+                                          self.be.to_index_tensor(homes))
+        self.be.experts_peer(self.bufs, R, counts, out_rank, out_row, mark or (lambda _n: None))
+
+    def peer_finish(self, st: DispatchState):
+        return self.be.combine(self.bufs.yhome[: st.perm["src_token"].numel()], st.perm, st.T)
+
+    def forward(self, x: torch.Tensor, timer=None) -> torch.Tensor:
+        mark = timer.mark if timer is not None else (lambda _n: None)
+        mark("start")
+        st = self.peer_prepare(x)
+        C = _peer_counts_all(self.ex, st.send_counts)
+        mark("dispatch_prepare")
+        self.peer_send(st, C)
+        self.bufs.barrier()
+        mark("dispatch_k1_peer")
+        self.peer_compute(C, mark)
+        self.bufs.barrier()
+        mark("gemm2_peer_barrier")
+        out = self.peer_finish(st)
+        mark("combine")
+        return out
+
+    __call__ = forward
+
+
+def run_loopback_peer(ranks: list, xs: list) -> list:
+    """``run_loopback`` for the peer transport: every rank's K1 writes into
+    the other ranks' buffers, then every rank's experts write their outputs
+    into the home ranks' buffers, then every rank combines."""
+    sts = [m.peer_prepare(x) for m, x in zip(ranks, xs)]
+    C = np.stack([st.send_counts for st in sts])
+    for m, st in zip(ranks, sts):
+        m.peer_send(st, C)
+    for m in ranks:
+        m.peer_compute(C)
+    return [m.peer_finish(st) for m, st in zip(ranks, sts)]
+
+
 def run_loopback(ranks: list, xs: list) -> list:
     """Drive W ``ExpertParallelMoE`` instances (one per simulated rank) in one
     process, performing the two all-to-all exchanges by concatenation. Used
@@ -264,6 +348,95 @@ def run_loopback(ranks: list, xs: list) -> list:
         y = m.compute(recv, recv_counts)
         y_parts.append(list(torch.split(y, recv_counts.sum(axis=1).tolist())))
     return [ranks[s].finish(sts[s], torch.cat([y_parts[r][s] for r in range(W)])) for s in range(W)]
+
+
+# ── fused transport: peer memory instead of an all-to-all ────────────────
+class PeerBuffers:
+    """One rank's receive and return buffers, addressable by every rank of
+    the EP group: ``codes`` [cap, d] u8 and ``params`` [cap, 4] int32 (the
+    dispatched rows, written by the senders' K1), ``yhome`` [cap_home, d]
+    bf16 (this rank's tokens' expert outputs, written by the owners' GEMM2
+    epilogue), plus device tables of all ranks' base pointers.
+
+    ``symmetric`` allocates through torch symmetric memory (NVLink peer
+    mappings, one process per GPU); ``loopback`` builds W ranks' buffers in
+    one process on one device (tests / single-GPU emulation: same kernels,
+    the peers are just other buffers)."""
+
+    def __init__(self, rank: int, world: int, codes, params, yhome, tabs, barrier=None):
+        self.rank, self.world = rank, world
+        self.codes, self.params, self.yhome = codes, params, yhome
+        self.codes_tab, self.params_tab, self.y_tab = tabs
+        self._barrier = barrier
+
+    def barrier(self):
+        if self._barrier is not None:
+            self._barrier()
+
+    @staticmethod
+    def _tab(ptrs, device):
+        return torch.tensor([int(p) for p in ptrs], dtype=torch.int64, device=device)
+
+    @classmethod
+    def symmetric(cls, d: int, cap: int, cap_home: int, group=None) -> "PeerBuffers":
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group or dist.group.WORLD
+        dev = torch.device("cuda", torch.cuda.current_device())
+        codes = symm_mem.empty(cap, d, dtype=torch.uint8, device=dev)
+        params = symm_mem.empty(cap, 4, dtype=torch.int32, device=dev)
+        yhome = symm_mem.empty(cap_home, d, dtype=torch.bfloat16, device=dev)
+        hs = [symm_mem.rendezvous(t, group) for t in (codes, params, yhome)]
+        tabs = tuple(cls._tab(h.buffer_ptrs, dev) for h in hs)
+        return cls(dist.get_rank(group), dist.get_world_size(group), codes, params, yhome, tabs,
+                   barrier=lambda: hs[0].barrier(channel=0))
+
+    @classmethod
+    def loopback(cls, world: int, d: int, cap: int, cap_home: int, device="cuda") -> list:
+        bufs = [(torch.empty((cap, d), dtype=torch.uint8, device=device),
+                 torch.empty((cap, 4), dtype=torch.int32, device=device),
+                 torch.empty((cap_home, d), dtype=torch.bfloat16, device=device)) for _ in range(world)]
+        tabs = tuple(cls._tab([b[i].data_ptr() for b in bufs], device) for i in range(3))
+        return [cls(r, world, *bufs[r], tabs) for r in range(world)]
+
+
+def peer_send_layout(C: np.ndarray, me: int, placement: ExpertPlacement) -> tuple[np.ndarray, np.ndarray]:
+    """Sender side. C[s, r, e] = rows rank s sends to rank r for expert e.
+    Rank r's receive buffer is expert-major (its local experts ascending),
+    sender-minor. Returns per sort key (r, e) (r-major): destination rank and
+    the first receive-buffer row of this sender's block."""
+    W, _, E = C.shape
+    rank_of = np.repeat(np.arange(W, dtype=np.int32), E)
+    base = np.zeros(W * E, dtype=np.int64)
+    for r in range(W):
+        off = 0
+        for e in placement.local_experts(r):
+            base[r * E + e] = off + C[:me, r, e].sum()
+            off += C[:, r, e].sum()
+    return rank_of, base.astype(np.int32)
+
+
+def peer_recv_layout(C: np.ndarray, me: int, local: tuple) -> tuple:
+    """Receiver side: block starts of the (expert, sender) blocks in the
+    receive buffer, each block's home rank and home row (the sender's sorted
+    row of its first element), and the per-local-expert row counts."""
+    W, _, E = C.shape
+    stray = np.ones(E, dtype=bool)
+    stray[list(local)] = False
+    if C[:, me, stray].any():
+        raise RuntimeError("received rows for an expert this rank does not hold (placement mismatch)")
+    sender_off = np.concatenate([np.zeros((W, 1), np.int64), np.cumsum(C.reshape(W, W * E), axis=1)[:, :-1]], axis=1)
+    starts, ranks, homes = [], [], []
+    pos = 0
+    for e in local:
+        for s in range(W):
+            starts.append(pos)
+            ranks.append(s)
+            homes.append(sender_off[s, me * E + e])
+            pos += int(C[s, me, e])
+    starts.append(pos)
+    counts = np.array([C[:, me, e].sum() for e in local], dtype=np.int64)
+    return (np.asarray(starts, np.int32), np.asarray(ranks, np.int32), np.asarray(homes, np.int32), counts)
 
 
 # ── the B200 backend ──────────────────────────────────────────────────────
@@ -364,6 +537,36 @@ class CudaExpertBackend:
 
     def combine(self, y_home, perm, T):
         return ops.combine(y_home, perm["token_pos"], T, self.k, out_dtype=self.out_dtype)
+
+    # peer transport
+    def dispatch_send(self, x, perm, E, bufs, dst_rank, dst_row):
+        W = perm["offsets"].numel() // E
+        s, sr, sr32 = self._smooth_tables(W)
+        ops.act_quant_dispatch(x, perm["src_token"], perm["row_expert"], smooth=s, smooth_recip=sr,
+                               smooth_recip_f32=sr32, codes_tab=bufs.codes_tab, params_tab=bufs.params_tab,
+                               dst_rank=dst_rank, dst_row=dst_row, row_weight=perm["row_weight"],
+                               ldc=bufs.codes.stride(0))
+
+    def experts_peer(self, bufs, R, group_counts, out_rank, out_row, mark=lambda _n: None):
+        b = self.bank
+        G = len(self.local_experts)
+        prm = ops.ep_unpack_params(bufs.params[:R], None)
+        a1 = {"codes": bufs.codes[:R], "scale_f32": prm["scale_f32"], "zp": prm["zp"], "rowsum": prm["rowsum"]}
+        offs = self.to_index_tensor(np.concatenate([[0], np.cumsum(group_counts)]))
+        row_group = self.to_index_tensor(np.repeat(np.arange(G), group_counts))
+        fuse = b.d % 16 == 0 and b.d >= 128
+        ext = torch.empty((R, 2), dtype=torch.int64, device="cuda") if fuse else None
+        h = ops.w8a8_gemm(a1, b.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16, group_offsets=offs,
+                          num_groups=G, n_per_group=2 * b.F, next_smooth_recip_f32=b.s2_recip32 if fuse else None,
+                          row_ext=ext)
+        mark("gemm13_swiglu")
+        a2 = ops.act_quant(h, smooth=b.s2, smooth_recip=b.s2_recip, smooth_recip_f32=b.s2_recip32,
+                           row_group=row_group, row_ext=ext)
+        mark("quant_h")
+        ops.w8a8_gemm_scatter(a2, b.w2, out_tab=bufs.y_tab, out_rank=out_rank, out_row=out_row,
+                              ldo=bufs.yhome.stride(0), row_weight=prm["weight"], group_offsets=offs, num_groups=G,
+                              n_per_group=b.d)
+        mark("gemm2")
 
 
 def plan_placement(idx: torch.Tensor, experts: int, top_k: int, world: int, top_k_per_layer: int = 1,

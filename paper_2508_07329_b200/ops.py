@@ -336,3 +336,42 @@ def ep_unpack_params(params: torch.Tensor, index: torch.Tensor | None) -> dict:
     L.call("moe_ep_unpack_params", L.ptr(params.contiguous()), L.ptr(index), n, L.ptr(out["scale_f32"]),
            L.ptr(out["zp"]), L.ptr(out["rowsum"]), L.ptr(out["weight"]), _s())
     return out
+
+
+# ── fused expert-parallel transport (peer memory) ──────────────────────────
+def block_map(n: int, block_start: torch.Tensor, val0: torch.Tensor, val1: torch.Tensor):
+    """Rows in blocks [start[b], start[b+1]) -> (val0[b], val1[b] + i - start[b])."""
+    dev = block_start.device
+    o0 = torch.empty(n, dtype=torch.int32, device=dev)
+    o1 = torch.empty(n, dtype=torch.int32, device=dev)
+    L.call("moe_block_map", n, val0.numel(), L.ptr(block_start.contiguous()), L.ptr(val0.contiguous()),
+           L.ptr(val1.contiguous()), L.ptr(o0), L.ptr(o1), _s())
+    return o0, o1
+
+
+def act_quant_dispatch(x: torch.Tensor, gather: torch.Tensor, row_group: torch.Tensor, *, smooth, smooth_recip,
+                       smooth_recip_f32, codes_tab: torch.Tensor, params_tab: torch.Tensor, dst_rank: torch.Tensor,
+                       dst_row: torch.Tensor, row_weight: torch.Tensor | None, ldc: int, bits: int = 8,
+                       symmetric: bool = False) -> None:
+    """K1 per token whose rows land directly in the destination ranks' receive buffers."""
+    x = _rowmajor(x, "x")
+    n = gather.numel()
+    L.call("moe_act_quant_dispatch", L.ptr(x), _dt(x), n, x.shape[1], x.stride(0), L.ptr(gather.contiguous()),
+           L.ptr(smooth), L.ptr(smooth_recip), L.ptr(smooth_recip_f32), L.ptr(row_group.contiguous()), bits,
+           int(bool(symmetric)), L.ptr(codes_tab), L.ptr(params_tab), L.ptr(dst_rank), L.ptr(dst_row),
+           L.ptr(row_weight), ldc, _s())
+
+
+def w8a8_gemm_scatter(a: dict, w: dict, *, out_tab: torch.Tensor, out_rank: torch.Tensor, out_row: torch.Tensor,
+                      ldo: int, out_dtype=torch.bfloat16, row_weight: torch.Tensor | None = None,
+                      group_offsets: torch.Tensor | None = None, num_groups: int = 1,
+                      n_per_group: int | None = None) -> None:
+    """DEQUANT grouped GEMM whose output rows go to out_tab[out_rank[m]] + out_row[m] * ldo."""
+    ac, wc = a["codes"], w["codes"]
+    M, K = ac.shape
+    N = n_per_group if n_per_group is not None else wc.shape[0] // num_groups
+    w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
+    L.call("moe_w8a8_gemm_scatter", L.ptr(ac), M, K, ac.stride(0), L.ptr(a["scale_f32"]), L.ptr(a["zp"]),
+           L.ptr(a["rowsum"]), L.ptr(wc), N, wc.stride(0), L.ptr(w["scale_f32"]), L.ptr(w["zp"]), L.ptr(w_rs), None,
+           L.ptr(row_weight), L.ptr(group_offsets), num_groups, L.EPI_DEQUANT | flags, L.ptr(out_tab),
+           L.ptr(out_rank), L.ptr(out_row), L.DT_BF16 if out_dtype == torch.bfloat16 else L.DT_F32, ldo, _s())

@@ -163,3 +163,31 @@ def test_ep_gloo_world2_matches_moe_forward():
         for r in range(2):
             got, want = np.load(os.path.join(d, f"r{r}.npy"))
             np.testing.assert_array_equal(got, want)
+
+
+# ── fused (peer memory) transport: host layout math ───────────────────────
+def test_peer_layouts_agree():
+    """Every sender's destination row for (receiver, expert) equals the
+    receiver's block start for (expert, sender); blocks tile the receive
+    buffer; home rows are the senders' sorted rows."""
+    rng = np.random.default_rng(9)
+    from paper_2508_07329_b200.ep import peer_recv_layout, peer_send_layout
+    W, E = 3, 6
+    pl = ExpertPlacement.from_counts(rng.integers(1, 100, E), W, replicated=(1,))
+    C = np.zeros((W, W, E), dtype=np.int64)
+    for s in range(W):
+        for e in range(E):
+            r = s if pl.owner[e] == -1 else pl.owner[e]
+            C[s, r, e] = rng.integers(0, 7)
+    for r in range(W):
+        starts, ranks, homes, counts = peer_recv_layout(C, r, pl.local_experts(r))
+        assert starts[-1] == C[:, r, :].sum()
+        assert counts.sum() == starts[-1]
+        b = 0
+        for e in pl.local_experts(r):
+            for s in range(W):
+                rank_of, base = peer_send_layout(C, s, pl)
+                assert ranks[b] == s and rank_of[r * E + e] == r
+                assert base[r * E + e] == starts[b]
+                assert homes[b] == C[s].reshape(-1)[: r * E + e].sum()
+                b += 1

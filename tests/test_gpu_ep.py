@@ -107,3 +107,51 @@ def test_ep_nccl_single_rank_group(tmp_path):
     """)
     r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300)
     assert "EQUAL" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("W,replicated,T", [(1, (), (500,)), (2, (), (600, 333)), (4, (0, 5), (256, 1, 700, 90)),
+                                            (3, (0, 1, 2, 3, 4, 5, 6), (100, 200, 50))])
+def test_ep_peer_loopback_matches_layer(layer, W, replicated, T):
+    """Fused peer-memory transport (K1 writes into the owners' receive
+    buffers, GEMM2 writes into the home ranks' buffers), W ranks emulated in
+    one process: bit-identical to the single-GPU forward."""
+    from paper_2508_07329_b200.ep import PeerBuffers, PeerExpertParallelMoE, run_loopback_peer
+    rng = np.random.default_rng(3)
+    xs = [_x(rng, t, layer.d) for t in T]
+    counts = np.bincount(layer.route(torch.cat(xs))[1].cpu().numpy().ravel(), minlength=layer.E)
+    pl = ExpertPlacement.from_counts(counts, W, replicated)
+    cap_home = max(T) * layer.k
+    bufs = PeerBuffers.loopback(W, layer.d, W * cap_home, cap_home)
+    ranks = [PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, bufs[r],
+                                   rank=r, exchange=_Local(W, r)) for r in range(W)]
+    for x, out in zip(xs, run_loopback_peer(ranks, xs)):
+        assert torch.equal(out, layer.forward(x))
+
+
+def test_ep_peer_symmetric_memory_single_rank(tmp_path):
+    """The peer transport over torch symmetric memory (NCCL world of 1):
+    buffers rendezvoused, device barrier, result equals the plain forward."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = textwrap.dedent(f"""
+        import os, sys, torch
+        sys.path.insert(0, {repr(os.getcwd())})
+        import torch.distributed as dist
+        from paper_2508_07329_b200.moe import MoELayer
+        from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertPlacement, PeerBuffers,
+                                              PeerExpertParallelMoE)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="{port}")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        layer = MoELayer.random(8, 256, 512, top_k=2, seed=4)
+        x = (torch.randn(300, 256, device="cuda") * 3).bfloat16()
+        pl = ExpertPlacement.sharded(8, 1)
+        bufs = PeerBuffers.symmetric(256, 600, 600)
+        ep = PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(0)), pl, bufs)
+        ok = torch.equal(ep(x), layer.forward(x))
+        dist.destroy_process_group()
+        print("EQUAL" if ok else "DIFFERENT")
+    """)
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300)
+    assert "EQUAL" in r.stdout, r.stdout + r.stderr[-3000:]
