@@ -32,7 +32,7 @@ def launches(path: str, tag: str):
         k[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     ks = list(by_id.values())
     # the last step: from the last router launch to the end
-    start = max(i for i, k in enumerate(ks) if "router_gate" in k["name"])
+    start = max(i for i, k in enumerate(ks) if "router_gate" in k["name"] or "router_tc" in k["name"])
     step = ks[start:]
     tot = sum(k["gpu__time_duration.sum"] for k in step)
     out = [f"# Launch list, last forward step ({tag})", "",
