@@ -127,3 +127,35 @@ def test_w8a8_linear(cuda, T, din, dout):
                             lin.w["zp"].cpu().numpy(), bias)
     np.testing.assert_allclose(y, want, rtol=1e-5, atol=1e-5 * np.abs(want).max())
     assert L.EPI_DEQUANT == 0
+
+
+@pytest.fixture(scope="module")
+def small_layer(cuda):
+    return MoELayer.random(8, 512, 1024, seed=11)
+
+
+def test_moe_token_independence(cuda, small_layer):
+    """Each token's output depends on that token alone, bit for bit — across
+    batch sizes that take the single-CTA (M < 2048 rows) and the CTA-pair
+    GEMM paths, ragged expert groups and the host pipeline's chunking."""
+    x = torch.from_numpy(_x(np.random.default_rng(4), 2500, 512)).to(cuda).bfloat16()
+    full = small_layer.forward(x)
+    for n in (1, 7, 300, 1024):
+        assert torch.equal(small_layer.forward(x[:n].contiguous()), full[:n]), n
+    part = small_layer.forward(x[1000:2100].contiguous())
+    assert torch.equal(part, full[1000:2100])
+
+
+def test_moe_permutation_equivariance(cuda, small_layer):
+    x = torch.from_numpy(_x(np.random.default_rng(5), 1500, 512)).to(cuda).bfloat16()
+    perm = torch.from_numpy(np.random.default_rng(6).permutation(1500)).to(cuda)
+    assert torch.equal(small_layer.forward(x[perm].contiguous()), small_layer.forward(x)[perm])
+
+
+def test_forward_host_matches_device(cuda, small_layer):
+    x = torch.from_numpy(_x(np.random.default_rng(7), 5000, 512)).bfloat16()
+    dev = small_layer.forward(x.to(cuda))
+    host = small_layer.forward_host(x.pin_memory(), chunk_tokens=4096)      # chunks 4096 + 904
+    assert torch.equal(host, dev.cpu())
+    host2 = small_layer.forward_host(x.pin_memory(), chunks=[1000, 3000, 1000])
+    assert torch.equal(host2, dev.cpu())
