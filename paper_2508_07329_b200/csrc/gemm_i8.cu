@@ -56,7 +56,6 @@ struct GemmArgs {
   int vec_ok;      // output pointer / ldo allow 16-byte vector stores
   int acc_vec_ok;  // acc_out / ld_acc and the W zp / rowsum tables allow 16-byte vectors
   int param_vec_ok;  // W zp / rowsum / scale tables allow 16-byte vector loads
-  int debug_skip_epilogue;  // MOE_B200_GEMM_SKIP_EPILOGUE=1: timing experiments only
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   int band;                 // m-tiles per raster band (map_tile)
   void* const* out_tab;     // DEQUANT: row m goes to out_tab[out_rank[m]] + out_row[m] * ldo (EP combine)
@@ -333,9 +332,7 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
         }
       }
     }
-    if (p.debug_skip_epilogue == 2) {   // timing experiment: math only
-      if (h[0] == 1234.5f && h[kSub - 1] == -1234.5f) static_cast<float*>(p.out)[0] = h[1];
-    } else if (tma) {
+    if (tma) {
       uint8_t* buf = obuf + (ob & 1u) * 1024;
       if (lane == 0) bulk_wait_group_read<1>();   // the store that used this buffer has read it
       __syncwarp();
@@ -350,7 +347,7 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
       }
       ++ob;
     }
-    if (p.debug_skip_epilogue != 2 && !tma && rvalid) {
+    if (!tma && rvalid) {
       const int64_t o = (int64_t)row * p.ldo + ti.n0 / 2 + hc;
       if (BF16 && p.vec_ok) {
         uint4* d = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + o);
@@ -366,8 +363,8 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
         for (int j = 0; j < kSub; ++j) d[j] = h[j];
       }
     }
-    if (p.debug_skip_epilogue != 2 && rvalid) {
-      if (p.row_ext && p.debug_skip_epilogue != 3) {
+    if (rvalid) {
+      if (p.row_ext) {
         const float4* t4 = reinterpret_cast<const float4*>(p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + hc);
         float xs[kSub];
 #pragma unroll
@@ -674,13 +671,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
-      if (p.debug_skip_epilogue == 1) {   // timing experiments only: drain TMEM, no math / stores
-        uint32_t v[32];
-        for (int c = 0; c < BN / 64; ++c) tmem_ld32(tbase + (half * (BN / 64) + c) * 32, v);
-        tmem_ld_wait();
-      } else {
-        epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob);
-      }
+      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob);
       tc_fence_before();
       if (CG == 2) mbar_arrive_leader(&tempty[as]);
       else mbar_arrive(&tempty[as]);
@@ -922,8 +913,6 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
                  (N % 4 == 0);
   p.param_vec_ok = ((reinterpret_cast<uintptr_t>(w_zp) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w_rowsum) & 15) == 0) &&
                    (!w_scale || (reinterpret_cast<uintptr_t>(w_scale) & 15) == 0) && (N % 4 == 0);
-  static const int skip_epi = getenv("MOE_B200_GEMM_SKIP_EPILOGUE") ? atoi(getenv("MOE_B200_GEMM_SKIP_EPILOGUE")) : 0;
-  p.debug_skip_epilogue = skip_epi;
   cudaStream_t s = as_stream(stream);
   if (row_ext) {
     rowext_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_ext, M);
