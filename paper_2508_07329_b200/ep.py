@@ -198,6 +198,17 @@ class ExpertParallelMoE:
             raise ValueError(f"backend holds experts {backend.local_experts}, placement gives {self.local}")
         self.dest = backend.to_index_tensor(placement.dest_table(self.rank))
 
+    def migrate(self, placement: ExpertPlacement) -> None:
+        """Re-placement step of the statistics loop: adopt a new placement
+        (e.g. from fresh routing statistics). This rank uploads the weights of
+        the experts it now holds from the layer spec and drops the others."""
+        if placement.world != self.pl.world or placement.experts != self.pl.experts:
+            raise ValueError("placement shape changed")
+        self.pl = placement
+        self.local = placement.local_experts(self.rank)
+        self.be = self.be.with_local_experts(self.local)
+        self.dest = self.be.to_index_tensor(placement.dest_table(self.rank))
+
     # phases (kept separate so a single process can drive several ranks: run_loopback)
     def dispatch(self, x: torch.Tensor) -> DispatchState:
         W, E = self.pl.world, self.pl.experts
@@ -452,6 +463,7 @@ class CudaExpertBackend:
         from .moe import MoELayer
 
         self.local_experts = tuple(local_experts)
+        self.spec = experts
         self.E = len(experts)
         self.k = top_k
         self.out_dtype = out_dtype
@@ -465,6 +477,12 @@ class CudaExpertBackend:
         self.d = self.s13.shape[1]
         self.device = self.s13.device
         self._tiled = {}
+
+    def with_local_experts(self, local_experts) -> "CudaExpertBackend":
+        """The same layer holding a different expert subset (migration)."""
+        return CudaExpertBackend(self.gate_w.cpu().numpy(), self.spec, local_experts, top_k=self.k,
+                                 gate_bias=None if self.gate_b is None else self.gate_b.cpu().numpy(),
+                                 out_dtype=self.out_dtype)
 
     @classmethod
     def from_layer_spec(cls, layer, local_experts):
@@ -592,6 +610,27 @@ def plan_placement(idx: torch.Tensor, experts: int, top_k: int, world: int, top_
     freq = expert_freq(trace)
     plan = plan_two_stage(path_stats(trace), freq, top_k_per_layer, supplement_k_per_layer)
     return ExpertPlacement.from_plan(plan, 0, freq, world)
+
+
+def plan_stack_placements(stats, world: int, top_k_per_layer: int = 1, supplement_k_per_layer: int = 1,
+                          group=None) -> list:
+    """Per-layer placements for an EP MoE stack from GPU-measured FULL-PATH
+    statistics (``RoutingStats`` of all layers, gathered over the ranks):
+    plan_two_stage (placement.py:125-176) ranks whole activation paths across
+    layers, then bin-packs each layer's remaining experts."""
+    from .placement import plan_two_stage
+    from .trace import PHASE_PREFILL, RoutingEvent, Trace, expert_freq, path_stats
+
+    paths = [ev.path for ev in stats.to_trace().events]
+    if torch.distributed.is_initialized() and torch.distributed.get_world_size(group) > 1:
+        gathered = [None] * torch.distributed.get_world_size(group)
+        torch.distributed.all_gather_object(gathered, paths, group=group)
+        paths = [p for part in gathered for p in part]
+    trace = Trace(stats.layers, stats.experts, stats.top_k,
+                  [RoutingEvent(t, PHASE_PREFILL, p) for t, p in enumerate(paths)])
+    freq = expert_freq(trace)
+    plan = plan_two_stage(path_stats(trace), freq, top_k_per_layer, supplement_k_per_layer)
+    return [ExpertPlacement.from_plan(plan, l, freq, world) for l in range(stats.layers)]
 
 
 def _np(a):

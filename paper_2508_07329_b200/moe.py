@@ -243,3 +243,41 @@ class MoELayer:
 
 def _np(a):
     return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+
+
+class MoEStack:
+    """A stack of W8A8 MoE layers with residual connections,
+    x_{l+1} = x_l + MoE_l(x_l) (bf16), the token path of SURVEY.md C5 minus
+    attention. ``forward(x, stats=RoutingStats(L, E, k))`` records every
+    layer's routing, so ``stats.to_trace()`` is a reference trace whose
+    events are the tokens' full activation paths (trace.py:40-44) — the
+    input of placement.plan_path / plan_two_stage."""
+
+    def __init__(self, layers: list):
+        if not layers:
+            raise ValueError("empty stack")
+        self.layers = layers
+        self.E, self.k, self.d = layers[0].E, layers[0].k, layers[0].d
+
+    @classmethod
+    def random(cls, L: int, E: int, d: int, F: int, top_k: int = 2, seed: int = 1, **kw) -> "MoEStack":
+        return cls([MoELayer.random(E, d, F, top_k=top_k, seed=seed + 17 * l, router_seed=2 + 17 * l, **kw)
+                    for l in range(L)])
+
+    def forward(self, x: torch.Tensor, stats=None) -> torch.Tensor:
+        for l, layer in enumerate(self.layers):
+            y = layer.forward(x, stats=_LayerStats(stats, l) if stats is not None else None)
+            x = (x.float() + y.float()).to(x.dtype)
+        return x
+
+    __call__ = forward
+
+
+class _LayerStats:
+    """Binds a RoutingStats to one layer index for MoELayer.forward."""
+
+    def __init__(self, stats, layer: int):
+        self.stats, self.layer = stats, layer
+
+    def record(self, idx):
+        self.stats.record(idx, self.layer)
