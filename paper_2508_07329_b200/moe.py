@@ -226,6 +226,50 @@ class MoELayer:
         d2h.synchronize()
         return out_host
 
+    def forward_host_stream(self, batches: list, depth: int = 2) -> list:
+        """Serving loop over several host batches [(x_host, out_host), ...]:
+        the same per-batch work as ``forward_host`` (H2D of the batch's
+        tokens, forward, D2H of its result), software-pipelined ACROSS
+        batches on three streams with ``depth`` device staging buffers, so
+        the H2D of batch b+1 and the D2H of batch b-1 overlap the forward of
+        batch b. Every batch is forwarded whole (no per-chunk weight
+        re-streaming). Returns the out_host tensors after the last D2H."""
+        if not batches:
+            return []
+        T = max(x.shape[0] for x, _ in batches)
+        cur = torch.cuda.current_stream()
+        io = getattr(self, "_stream_io", None)
+        if io is None or io["bufs"][0].shape[0] < T or len(io["bufs"]) < depth:
+            io = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+                  "bufs": [torch.empty((T, self.d), dtype=batches[0][0].dtype, device="cuda") for _ in range(depth)]}
+            self._stream_io = io
+        h2d, d2h, bufs = io["h2d"], io["d2h"], io["bufs"]
+        h2d.wait_stream(cur)
+        done = [None] * len(batches)          # forward of batch i finished (its staging slot is free)
+        outs = []
+        for i, (xh, oh) in enumerate(batches):
+            slot = bufs[i % depth]
+            n = xh.shape[0]
+            if oh is None:
+                oh = torch.empty((n, self.d), dtype=self.out_dtype, pin_memory=True)
+            with torch.cuda.stream(h2d):
+                if i >= depth:
+                    h2d.wait_event(done[i - depth])
+                slot[:n].copy_(xh, non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(h2d)
+            cur.wait_event(loaded)
+            y = self.forward(slot[:n])
+            done[i] = torch.cuda.Event()
+            done[i].record(cur)
+            d2h.wait_event(done[i])
+            with torch.cuda.stream(d2h):
+                oh.copy_(y, non_blocking=True)
+            y.record_stream(d2h)
+            outs.append(oh)
+        d2h.synchronize()
+        return outs
+
     # ------------------------------------------------------------------
     def expert_host(self, e: int) -> dict:
         """Host copies of expert e in the oracle's layout (codes/scales/zps of

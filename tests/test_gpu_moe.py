@@ -159,3 +159,11 @@ def test_forward_host_matches_device(cuda, small_layer):
     assert torch.equal(host, dev.cpu())
     host2 = small_layer.forward_host(x.pin_memory(), chunks=[1000, 3000, 1000])
     assert torch.equal(host2, dev.cpu())
+
+
+def test_forward_host_stream_matches_device(cuda, small_layer):
+    rng = np.random.default_rng(8)
+    xs = [torch.from_numpy(_x(rng, t, 512)).bfloat16().pin_memory() for t in (700, 1500, 3, 900, 1500)]
+    outs = small_layer.forward_host_stream([(x, None) for x in xs], depth=2)
+    for x, o in zip(xs, outs):
+        assert torch.equal(o, small_layer.forward(x.to(cuda)).cpu())
