@@ -21,6 +21,7 @@
 // encode out of line. Codes, scales, zero points and row sums are identical
 // to the exact kernel (tests/test_gpu_kernels.py).
 #include <algorithm>
+#include <type_traits>
 
 #include "k1_common.cuh"
 #include "ptx.cuh"
@@ -315,12 +316,64 @@ constexpr float kFastTlo = 12582914.0f;          // code 2
 constexpr float kFastThi = 12583165.0f;          // code 253
 constexpr float kFastThr = 0.4998779296875f;     // 0.5 - 2^-13
 
+// Per-row constants of the fast encode. Two variants:
+//  * two-sided rows (asymmetric, the extremes land on codes <= 0 / >= 255):
+//    vectors are fast when every code is in [2, 253]; elements that could
+//    be extremes necessarily fall outside and are counted out of line;
+//  * general rows (one-sided, e.g. ReLU outputs with min 0, or symmetric):
+//    codes in [0, 255] plus an explicit float32 candidate check
+//    xlo <= xs <= xhi. An extreme that is exactly 0 needs no candidates:
+//    zeros quantize exactly and only a strictly negative (positive) element
+//    could beat a zero minimum (maximum).
 struct FastRow {
   double scale, rscale;
   float rsc, magic;
-  float cand_max, cand_min;  // xs >= cand_max (<= cand_min) may be an exact extreme
+  float tlo, thi;            // fast-vector t range (code window)
+  float xlo, xhi;            // xs < xlo (> xhi) may be an exact min (max): counted
+  uint32_t expect;           // candidate count that confirms the speculation (max | min << 16)
   int zp;
 };
+constexpr float kCodeT0 = 12582912.0f;          // t of code 0
+constexpr float kCodeT255 = 12583167.0f;        // t of code 255
+
+// 0: no fast path, 1: two-sided, 2: general
+__device__ __forceinline__ int init_fast_row(FastRow& f, const AffineParams& p, float M, float m, double mn, double mx,
+                                             int bits, int sym) {
+  if (bits != 8) return 0;
+  f.scale = p.scale;
+  f.rscale = p.rscale;
+  f.zp = p.zp;
+  f.rsc = __double2float_rn(p.rscale);
+  f.magic = kMagicF + (float)p.zp;
+  const float cand_max = M - 3.f * fabsf(M) * kRelErr - 2.350988701644575e-38f;
+  const float cand_min = m + 3.f * fabsf(m) * kRelErr + 2.350988701644575e-38f;
+  f.xlo = nextafterf(cand_min, FLT_MAX);
+  f.xhi = nextafterf(cand_max, -FLT_MAX);
+  const double hc = __dadd_rn(rha(div_rcp(mx, p.scale, p.rscale)), (double)p.zp);
+  const double lc = __dadd_rn(rha(div_rcp(mn, p.scale, p.rscale)), (double)p.zp);
+  // two-sided window only when zero (hence the bulk of typical activations)
+  // quantizes well inside [2, 253]; one-sided rows (zp at an edge, e.g. ReLU)
+  // take the general window, where the edge codes stay on the fast path
+  if (!sym && hc >= 255.0 && lc <= 0.0 && p.zp >= 16 && p.zp <= 239 && m != 0.f && M != 0.f) {
+    f.tlo = kFastTlo;
+    f.thi = kFastThi;
+    f.expect = 0x10001u;
+    return 1;
+  }
+  f.tlo = kCodeT0;
+  f.thi = kCodeT255;
+  uint32_t e = 0x10001u;
+  if (m == 0.f) {           // zero minimum: only negatives are candidates
+    f.xlo = 0.f;
+    e -= 0x10000u;
+  }
+  if (M == 0.f) {
+    f.xhi = 0.f;
+    e -= 1u;
+  }
+  f.expect = e;
+  return 2;
+}
 
 // Rare vectors: generic float32 encode (clip, exact float64 redo) plus the
 // count of possible-extreme elements. Returns (codes, cnt_max | cnt_min << 16).
@@ -332,11 +385,11 @@ __device__ __noinline__ uint4 slow_vec8(uint4 u, const float* tab, int64_t c, co
   uint32_t cnt = 0, w[2] = {0u, 0u};
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    cnt += (uint32_t)(xs[e] >= f.cand_max) + ((uint32_t)(xs[e] <= f.cand_min) << 16);
+    cnt += (uint32_t)(xs[e] > f.xhi) + ((uint32_t)(xs[e] < f.xlo) << 16);
     const float t = fmaf(xs[e], f.rsc, f.magic);
     const float d = fmaf(xs[e], f.rsc, f.magic - t);   // magic - t = -round(p), exact
     uint32_t code;
-    if (t >= kFastTlo && t <= kFastThi && fabsf(d) < kFastThr) {
+    if (t >= kCodeT0 && t <= kCodeT255 && fabsf(d) < kFastThr) {   // in range: no clipping
       code = __float_as_uint(t) & 0xFFu;
     } else {   // clipping, rounding boundary, non-finite: the float64 reference encode
       const double xd = srow ? div_rcp((double)xv[e], srow[c * 8 + e], rrow[c * 8 + e]) : (double)xv[e];
@@ -393,6 +446,66 @@ __device__ __noinline__ int fallback_row(const uint4* src, int64_t nvec, int lan
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   *out = p;
   return sum;
+}
+
+template <bool GEN>
+__device__ __forceinline__ bool fast_ok(const float (&xs)[8], const float (&t)[8], float dm, const FastRow& f) {
+  bool ok = max8(t) <= f.thi && min8(t) >= f.tlo && dm < kFastThr;
+  if (GEN) ok = ok && max8(xs) <= f.xhi && min8(xs) >= f.xlo;
+  return ok;
+}
+
+__device__ __forceinline__ float t_and_d(const float (&xs)[8], const FastRow& f, float (&t)[8]) {
+  const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
+  float d[8];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    const float2 x2 = make_float2(xs[e], xs[e + 1]);
+    const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
+    const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
+    const float2 d2 = __ffma2_rn(x2, rsc2, nr);
+    t[e] = t2.x;
+    t[e + 1] = t2.y;
+    d[e] = d2.x;
+    d[e + 1] = d2.y;
+  }
+  return fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
+                       fmax3_abs_nan(d[6], d[7], 0.f));
+}
+
+template <bool GEN>
+__device__ __forceinline__ uint2 fast_vec8(const uint4& u, int64_t c, const float* tab, const double* srow,
+                                           const double* rrow, const FastRow& f, uint32_t& cnt) {
+  float xs[8], t[8];
+  smooth8(u, tab, c, xs);
+  const float dm = t_and_d(xs, f, t);
+  if (fast_ok<GEN>(xs, t, dm, f))
+    return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
+  const uint4 sv = slow_vec8(u, tab, c, srow, rrow, f);
+  cnt += sv.z;
+  return make_uint2(sv.x, sv.y);
+}
+
+// xs = x * table for 8 elements, table slice preloaded (ta: elements 0-3, tb: 4-7)
+__device__ __forceinline__ void smooth8_pre(const uint4& u, bool has_tab, const float4& ta, const float4& tb,
+                                            float (&xs)[8]) {
+  unpack8(u, xs);
+  if (has_tab) {
+    float2 q;
+    q = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(ta.x, ta.y)); xs[0] = q.x; xs[1] = q.y;
+    q = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(ta.z, ta.w)); xs[2] = q.x; xs[3] = q.y;
+    q = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(tb.x, tb.y)); xs[4] = q.x; xs[5] = q.y;
+    q = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(tb.z, tb.w)); xs[6] = q.x; xs[7] = q.y;
+  }
+}
+
+// branch-free fast encode of 8 smoothed values; slow = the vector must take slow_vec8
+template <bool GEN>
+__device__ __forceinline__ uint2 fast_core(const float (&xs)[8], const FastRow& f, bool& slow) {
+  float t[8];
+  const float dm = t_and_d(xs, f, t);
+  slow = !fast_ok<GEN>(xs, t, dm, f);
+  return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
 }
 
 template <bool GIVEN, int WARPS, int MINB>
@@ -464,57 +577,30 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     AffineParams p{};
     int sum = 0;
     bool done = false;
-    if (spec && bits == 8 && !sym) {
+    if (spec) {
       p = affine_params(mn, mx, bits, sym);
-      const double hc = __dadd_rn(rha(div_rcp(mx, p.scale, p.rscale)), (double)p.zp);
-      const double lc = __dadd_rn(rha(div_rcp(mn, p.scale, p.rscale)), (double)p.zp);
-      if (hc >= 255.0 && lc <= 0.0) {
-        FastRow f;
-        f.scale = p.scale;
-        f.rscale = p.rscale;
-        f.zp = p.zp;
-        f.rsc = __double2float_rn(p.rscale);
-        f.magic = kMagicF + (float)p.zp;
-        f.cand_max = rec.M - 3.f * fabsf(rec.M) * kRelErr - 2.350988701644575e-38f;
-        f.cand_min = rec.m + 3.f * fabsf(rec.m) * kRelErr + 2.350988701644575e-38f;
-        const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
+      FastRow f;
+      const int mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
+      if (mode) {
         uint32_t cnt = 0;
-        for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
-          float xs[8];
-          smooth8(u, tab, c, xs);
-          float t[8], d[8];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float2 x2 = make_float2(xs[e], xs[e + 1]);
-            const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
-            const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
-            const float2 d2 = __ffma2_rn(x2, rsc2, nr);
-            t[e] = t2.x;
-            t[e + 1] = t2.y;
-            d[e] = d2.x;
-            d[e + 1] = d2.y;
-          }
-          const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
-                                         fmax3_abs_nan(d[6], d[7], 0.f));
-          uint2 out;
-          if (max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr) {
-            out = make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
-          } else {
-            const uint4 s = slow_vec8(u, tab, c, srow, rrow, f);
-            out = make_uint2(s.x, s.y);
-            cnt += s.z;
-          }
-          sum += bytesum(out);
-          __stcs(dst + c, out);
-        });
+        auto run = [&](auto gen) {
+          constexpr bool G = decltype(gen)::value;
+          for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
+            const uint2 out = fast_vec8<G>(u, c, tab, srow, rrow, f, cnt);
+            sum += bytesum(out);
+            __stcs(dst + c, out);
+          });
+        };
+        if (mode == 1) run(std::false_type{});
+        else run(std::true_type{});
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           sum += __shfl_xor_sync(0xffffffffu, sum, o);
           cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         }
-        // exactly one possible extreme on each side: the recorded elements
-        // are the exact extremes and the codes stand
-        done = cnt == 0x10001u;
+        // exactly the expected possible extremes (the recorded elements):
+        // they are the exact extremes and the codes stand
+        done = cnt == f.expect;
       }
     }
     if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
@@ -548,66 +634,6 @@ constexpr int kRing = 6;
 constexpr int kBulkWarps = 16;
 constexpr int kVecStep = 2;     // vectors per lane processed together (register budget: 16 warps)
 constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
-
-__device__ __forceinline__ uint2 fast_vec8(const uint4& u, int64_t c, const float* tab, const double* srow,
-                                           const double* rrow, const FastRow& f, uint32_t& cnt) {
-  float xs[8];
-  smooth8(u, tab, c, xs);
-  const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
-  float t[8], d[8];
-#pragma unroll
-  for (int e = 0; e < 8; e += 2) {
-    const float2 x2 = make_float2(xs[e], xs[e + 1]);
-    const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
-    const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
-    const float2 d2 = __ffma2_rn(x2, rsc2, nr);
-    t[e] = t2.x;
-    t[e + 1] = t2.y;
-    d[e] = d2.x;
-    d[e + 1] = d2.y;
-  }
-  const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
-                                 fmax3_abs_nan(d[6], d[7], 0.f));
-  if (max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr)
-    return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
-  const uint4 sv = slow_vec8(u, tab, c, srow, rrow, f);
-  cnt += sv.z;
-  return make_uint2(sv.x, sv.y);
-}
-
-// xs = x * table for 8 elements, table slice preloaded (ta: elements 0-3, tb: 4-7)
-__device__ __forceinline__ void smooth8_pre(const uint4& u, bool has_tab, const float4& ta, const float4& tb,
-                                            float (&xs)[8]) {
-  unpack8(u, xs);
-  if (has_tab) {
-    float2 q;
-    q = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(ta.x, ta.y)); xs[0] = q.x; xs[1] = q.y;
-    q = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(ta.z, ta.w)); xs[2] = q.x; xs[3] = q.y;
-    q = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(tb.x, tb.y)); xs[4] = q.x; xs[5] = q.y;
-    q = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(tb.z, tb.w)); xs[6] = q.x; xs[7] = q.y;
-  }
-}
-
-// branch-free fast encode of 8 smoothed values; slow = the vector must take slow_vec8
-__device__ __forceinline__ uint2 fast_core(const float (&xs)[8], const FastRow& f, bool& slow) {
-  const float2 rsc2 = make_float2(f.rsc, f.rsc), mag2 = make_float2(f.magic, f.magic);
-  float t[8], d[8];
-#pragma unroll
-  for (int e = 0; e < 8; e += 2) {
-    const float2 x2 = make_float2(xs[e], xs[e + 1]);
-    const float2 t2 = __ffma2_rn(x2, rsc2, mag2);
-    const float2 nr = __fadd2_rn(mag2, make_float2(-t2.x, -t2.y));   // -round(p), exact
-    const float2 d2 = __ffma2_rn(x2, rsc2, nr);
-    t[e] = t2.x;
-    t[e + 1] = t2.y;
-    d[e] = d2.x;
-    d[e + 1] = d2.y;
-  }
-  const float dm = fmax3_abs_nan(fmax3_abs_nan(d[0], d[1], d[2]), fmax3_abs_nan(d[3], d[4], d[5]),
-                                 fmax3_abs_nan(d[6], d[7], 0.f));
-  slow = !(max8(t) <= kFastThi && min8(t) >= kFastTlo && dm < kFastThr);
-  return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
-}
 
 template <bool GIVEN>
 __global__ void __launch_bounds__(kBulkWarps * 32, 1)
@@ -744,23 +770,16 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     AffineParams p{};
     int sum = 0;
     bool done = false;
-    bool fast = spec && bits == 8 && !sym;
     FastRow f;
-    if (fast) {
+    int mode = 0;
+    if (spec) {
       p = affine_params(mn, mx, bits, sym);
-      const double hc = __dadd_rn(rha(div_rcp(mx, p.scale, p.rscale)), (double)p.zp);
-      const double lc = __dadd_rn(rha(div_rcp(mn, p.scale, p.rscale)), (double)p.zp);
-      fast = hc >= 255.0 && lc <= 0.0;
-      f.scale = p.scale;
-      f.rscale = p.rscale;
-      f.zp = p.zp;
-      f.rsc = __double2float_rn(p.rscale);
-      f.magic = kMagicF + (float)p.zp;
-      f.cand_max = rec.M - 3.f * fabsf(rec.M) * kRelErr - 2.350988701644575e-38f;
-      f.cand_min = rec.m + 3.f * fabsf(rec.m) * kRelErr + 2.350988701644575e-38f;
+      mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
     }
-    if (fast) {
+    if (mode) {
       uint32_t cnt = 0;
+      auto run = [&](auto gen) {
+      constexpr bool G = decltype(gen)::value;
       for (int k = 0; k < nchunks; ++k) {
         const uint32_t it = cfirst + k;
         wait_item(it);
@@ -789,7 +808,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
               float xs[8];
               smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
               bool sl;
-              out[b] = fast_core(xs, f, sl);
+              out[b] = fast_core<G>(xs, f, sl);
               slowm |= (uint32_t)sl << b;
             }
 #pragma unroll
@@ -814,7 +833,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
           for (int b = 0; b < 4; ++b) {
             const int64_t c = cb + 32 * b;
             if (c < nvec) {
-              const uint2 out = fast_vec8(v[lane + 32 * b], c, tab, srow, rrow, f, cnt);
+              const uint2 out = fast_vec8<G>(v[lane + 32 * b], c, tab, srow, rrow, f, cnt);
               sum += bytesum(out);
               __stcs(dst + c, out);
             }
@@ -823,12 +842,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         __syncwarp();
         produce();
       }
+      };
+      if (mode == 1) run(std::false_type{});
+      else run(std::true_type{});
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
         cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       }
-      done = cnt == 0x10001u;
+      done = cnt == f.expect;
     } else {
       for (int k = 0; k < nchunks; ++k) {   // keep the ring in step
         wait_item(cfirst + k);

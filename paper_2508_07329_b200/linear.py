@@ -22,7 +22,7 @@ class W8A8Linear:
                  act_symmetric: bool = False, out_dtype=torch.bfloat16):
         if weight.granularity != PER_OUTPUT_ROW:
             raise ValueError("W8A8Linear weights must be quantized per output row")
-        self.w = weight.device()
+        self.w = ops.with_wcorr(weight.device())     # pre-corrected sidecar: 2 IMADs per accumulator
         self.out_features, self.in_features = self.w["codes"].shape
         self.smooth = None
         self.smooth_recip = None

@@ -64,6 +64,30 @@ def test_act_quant_gather_grouped_bitexact(cuda):
     np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
 
 
+@pytest.mark.parametrize("sym", [False, True])
+def test_act_quant_one_sided_rows(cuda, sym):
+    """ReLU-like rows (min exactly 0, many zeros), non-positive rows and
+    symmetric codes take the general fast path (code window [0, 255] plus an
+    explicit candidate check, zero extremes exempt): bit-exact vs the oracle."""
+    rng = np.random.default_rng(31 + sym)
+    T, d = 257, 2048
+    x = rng.normal(size=(T, d)).astype(np.float32) * np.exp(rng.normal(size=(T, 1)))
+    x[: T // 3] = np.maximum(x[: T // 3], 0.0)                 # ReLU rows: ~50 % exact zeros
+    x[T // 3: 2 * T // 3] = -np.abs(x[T // 3: 2 * T // 3])     # non-positive rows
+    x[5, :] = 0.0
+    x[6, :] = 0.0
+    x[6, 100] = 3.0                                             # a single non-zero
+    x = bf16_round(x)
+    s = _smooth(rng, 1, d)
+    xd = torch.from_numpy(x).to(cuda).bfloat16()
+    r = ops.act_quant(xd, smooth=torch.from_numpy(s).to(cuda), symmetric=sym)
+    codes, sc, zp = Q.rtn(x.astype(np.float64) / s[0], Q.cfg(8, sym, "per_token"))
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), sc)
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+    np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), codes.astype(np.int64).sum(1))
+
+
 def test_act_quant_golden_k1(cuda, golden):
     x = golden["k1_x_bf16"]
     r = ops.act_quant(torch.from_numpy(x.astype(np.float32)).to(cuda).bfloat16(),
