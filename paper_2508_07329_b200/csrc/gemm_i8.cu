@@ -35,7 +35,12 @@ constexpr int kBM = 128;           // rows per CTA (UMMA M per CTA)
 constexpr int kBK = 128;           // bytes of K per stage = one SW128 atom row
 constexpr int kUmmaK = 32;         // K per tcgen05.mma for 8-bit inputs
 constexpr int kMaxGroups = 64;
-constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
+#ifndef MOE_GEMM_EPI_WARPS
+#define MOE_GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = MOE_GEMM_EPI_WARPS;         // epilogue warps: kEpiWarps / 4 per TMEM lane quarter
+constexpr int kParts = kEpiWarps / 4;                  // column parts of a tile per lane quarter
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;     // 4 control warps + the epilogue warps
 
 struct GemmArgs {
   int M, N, K, G;
@@ -77,7 +82,7 @@ struct Smem {
   static constexpr int kTmemPtrOff = kBarOff + kNumBars * 8;
   static constexpr int kTableOff = kTmemPtrOff + 16;                  // tile_start[G+1], off[G+1]
   static constexpr int kOutOff = (kTableOff + 2 * (kMaxGroups + 1) * 4 + 127) / 128 * 128;
-  static constexpr int kOutBytes = 8 * 2 * 1024;                       // 8 epilogue warps x 2 x (32 rows x 32 B)
+  static constexpr int kOutBytes = kEpiWarps * 2 * 1024;               // per epilogue warp 2 x (32 rows x 32 B)
   static constexpr int kBytes = kOutOff + kOutBytes + 1024;           // + alignment slack
 };
 
@@ -265,9 +270,9 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
                                             ExtRec& ext, bool rvalid, float sa, float rw, int32_t za, int32_t rsa,
                                             const CUtensorMap* tmO, uint8_t* obuf, uint32_t& ob) {
   constexpr int kSub = 16;
-  constexpr int kNSub = BN / 4 / kSub;             // sub-chunks per thread (half of BN/2 h columns)
+  constexpr int kNSubAll = BN / 2 / kSub;          // sub-chunks of a tile row (BN/2 h columns)
+  constexpr int kIters = (kNSubAll + kParts - 1) / kParts;
   const int wbase = ti.g * p.N;
-  const int hc0 = half * (BN / 4);                 // first h column (tile-relative) of this thread
   const uint32_t nrsa = 0u - (uint32_t)rsa, nza = 0u - (uint32_t)za, kc = (uint32_t)p.Kc;
   const float2 sa2 = make_float2(sa, sa), srw2 = make_float2(sa * rw, sa * rw);
   const float2 nl2 = make_float2(-1.4426950408889634f, -1.4426950408889634f), one2 = make_float2(1.f, 1.f);
@@ -275,16 +280,18 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
   const bool tma = BF16 && p.tma_out && __all_sync(0xffffffffu, rvalid);
   const int lane = threadIdx.x & 31;
   uint32_t ag[2][kSub], au[2][kSub];
-  tmem_ld16(tbase + hc0, ag[0]);
-  tmem_ld16(tbase + BN / 2 + hc0, au[0]);
+  tmem_ld16(tbase + half * kSub, ag[0]);
+  tmem_ld16(tbase + BN / 2 + half * kSub, au[0]);
   tmem_ld_wait();
 #pragma unroll
-  for (int sc = 0; sc < kNSub; ++sc) {
-    const int cur = sc & 1;
-    const int hc = hc0 + sc * kSub;                // tile-relative h column of this sub-chunk
-    if (sc + 1 < kNSub) {
-      tmem_ld16(tbase + hc + kSub, ag[cur ^ 1]);
-      tmem_ld16(tbase + BN / 2 + hc + kSub, au[cur ^ 1]);
+  for (int it = 0; it < kIters; ++it) {
+    const int sc = half + it * kParts;             // this thread's sub-chunks: part, part + kParts, ...
+    if (sc >= kNSubAll) break;
+    const int cur = it & 1;
+    const int hc = sc * kSub;                      // tile-relative h column of this sub-chunk
+    if (sc + kParts < kNSubAll) {
+      tmem_ld16(tbase + hc + kParts * kSub, ag[cur ^ 1]);
+      tmem_ld16(tbase + BN / 2 + hc + kParts * kSub, au[cur ^ 1]);
     }
     const int ng0 = wbase + ti.n0 + hc;
     const int4* gz = reinterpret_cast<const int4*>(p.w_zp + ng0);
@@ -391,7 +398,7 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
         if (m < ext.m) { ext.m = m; ext.cm = col; }
       }
     }
-    if (sc + 1 < kNSub) tmem_ld_wait();
+    if (sc + kParts < kNSubAll) tmem_ld_wait();
   }
 }
 
@@ -418,7 +425,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
   } else if (EPI == MOE_EPI_SWIGLU) {
     // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
 #pragma unroll 1
-    for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
+    for (int c = half; c < BN / 64; c += kParts) {
       uint32_t vg[32], vu[32];
       tmem_ld32(tbase + c * 32, vg);
       tmem_ld32(tbase + BN / 2 + c * 32, vu);
@@ -466,7 +473,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
     }
   } else {
 #pragma unroll 1
-    for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+    for (int c = half; c < BN / 32; c += kParts) {
       uint32_t v[32];
       tmem_ld32(tbase + c * 32, v);
       tmem_ld_wait();
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 256 * CG);  // all epilogue threads of the pair (leader's copy)
+      mbar_init(&tempty[s], 32 * kEpiWarps * CG);  // all epilogue threads of the pair (leader's copy)
     }
     fence_mbar_init();
   }
@@ -659,7 +666,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
     const int q = warp & 3;            // TMEM lane quarter this warp may access
-    const int half = (warp - 4) >> 2;  // which half of the tile columns
+    const int half = (warp - 4) >> 2;  // which column part of the tile (0 .. kParts-1)
     uint8_t* obuf = smem + L::kOutOff + (warp - 4) * 2048;   // this warp's TMA-store staging (2 x 1 KB)
     uint32_t ob = 0;
     uint32_t tile_it = 0;
