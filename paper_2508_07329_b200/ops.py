@@ -174,22 +174,18 @@ def quant_sq_error(acc: torch.Tensor, a_scale: torch.Tensor, w_scale: torch.Tens
 
 
 # ── K3 / K4 / K6 ──────────────────────────────────────────────────────────
-_GATE_PIECES: dict = {}
-
-
 def router_pieces(gate_w: torch.Tensor) -> torch.Tensor:
-    """bf16 (hi, mid, lo) split of a float32 gate for the tensor-core router,
-    cached per gate tensor (moe_router_prepare)."""
-    key = (gate_w.data_ptr(), gate_w._version, tuple(gate_w.shape))
-    pc = _GATE_PIECES.get(key)
-    if pc is None:
-        E, d = gate_w.shape
-        lib = L.load()
-        pc = torch.empty(lib.moe_router_tc_workspace(d) // 2, dtype=torch.bfloat16, device=gate_w.device)
-        L.call("moe_router_prepare", L.ptr(gate_w.contiguous()), E, d, L.ptr(pc), _s())
-        if len(_GATE_PIECES) > 16:
-            _GATE_PIECES.clear()
-        _GATE_PIECES[key] = pc
+    """bf16 (hi, mid, lo) split of a float32 gate for the tensor-core router
+    (moe_router_prepare), cached ON the gate tensor (valid while its version
+    counter is unchanged; freed with it)."""
+    cached = getattr(gate_w, "_moe_router_pieces", None)
+    if cached is not None and cached[0] == gate_w._version:
+        return cached[1]
+    E, d = gate_w.shape
+    lib = L.load()
+    pc = torch.empty(lib.moe_router_tc_workspace(d) // 2, dtype=torch.bfloat16, device=gate_w.device)
+    L.call("moe_router_prepare", L.ptr(gate_w.contiguous()), E, d, L.ptr(pc), _s())
+    gate_w._moe_router_pieces = (gate_w._version, pc)
     return pc
 
 
