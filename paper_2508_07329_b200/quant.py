@@ -239,12 +239,16 @@ class _LossContext:
         self.xt = xd.T.contiguous()                       # tokens-major
         self.ref = self.xt @ self.wd.T                    # [T, R] float64 (cuBLAS DGEMM)
 
-    def sq_error(self, f_dev: torch.Tensor | None, w_codes: dict | None = None) -> float:
+    def sq_error_dev(self, f_dev: torch.Tensor | None, w_codes: dict | None = None) -> torch.Tensor:
+        """||Q(W f) Q(X / f) - W X||_F^2 as a device scalar (no host sync)."""
         cfg = self.cfg
         wq = w_codes if w_codes is not None else _k1(self.wd, cfg, PER_OUTPUT_ROW, f_dev, L.SMOOTH_MULTIPLY)
         xq = _k1(self.xt, cfg, cfg.granularity, f_dev, L.SMOOTH_DIVIDE)
         acc = ops.w8a8_gemm(xq, wq, epilogue=L.EPI_ACC_I32)
-        return float(ops.quant_sq_error(acc, xq["scale"], wq["scale"], self.ref).item())
+        return ops.quant_sq_error(acc, xq["scale"], wq["scale"], self.ref)
+
+    def sq_error(self, f_dev: torch.Tensor | None, w_codes: dict | None = None) -> float:
+        return float(self.sq_error_dev(f_dev, w_codes).item())
 
 
 def quant_loss(w, x, factors, cfg: QuantConfig) -> float:
@@ -263,11 +267,14 @@ def search_smoothing(w, x, cfg: QuantConfig, grid_steps: int = DEFAULT_GRID_STEP
     ctx = _LossContext(w, x, cfg)
     stat_dev = ops.channel_stats(ctx.xt.T.contiguous(), L.ORDER_MAX_ABS)
     stat = np.maximum(stat_dev.cpu().numpy(), STAT_FLOOR)
+    grid = np.linspace(0.0, 1.0, grid_steps)
+    factors = [stat ** e for e in grid]                     # numpy pow: bit-identical to the reference's
+    # every grid point's loss stays on the device; one host sync for all of them
+    sq = torch.stack([ctx.sq_error_dev(torch.from_numpy(f).cuda()).reshape(()) for f in factors]).cpu().numpy()
     best = None
-    for e in np.linspace(0.0, 1.0, grid_steps):
-        f = stat ** e
-        loss = float(np.sqrt(ctx.sq_error(torch.from_numpy(f).cuda())))
-        if best is None or loss < best.loss:
+    for e, f, v in zip(grid, factors, sq):
+        loss = float(np.sqrt(float(v)))
+        if best is None or loss < best.loss:             # strict: ties keep the smaller exponent
             best = SmoothingResult(float(e), f, loss)
     return best
 
