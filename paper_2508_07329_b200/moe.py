@@ -290,9 +290,9 @@ def _np(a):
 
 
 class MoEStack:
-    """A stack of W8A8 MoE layers with residual connections,
-    x_{l+1} = x_l + MoE_l(x_l) (bf16), the token path of SURVEY.md C5 minus
-    attention. ``forward(x, stats=RoutingStats(L, E, k))`` records every
+    """A stack of W8A8 MoE layers with pre-norm residual connections,
+    x_{l+1} = x_l + MoE_l(RMSNorm(x_l)) (bf16, Mixtral's block structure),
+    the token path of SURVEY.md C5 minus attention. ``forward(x, stats=RoutingStats(L, E, k))`` records every
     layer's routing, so ``stats.to_trace()`` is a reference trace whose
     events are the tokens' full activation paths (trace.py:40-44) — the
     input of placement.plan_path / plan_two_stage."""
@@ -308,9 +308,16 @@ class MoEStack:
         return cls([MoELayer.random(E, d, F, top_k=top_k, seed=seed + 17 * l, router_seed=2 + 17 * l, **kw)
                     for l in range(L)])
 
+    @staticmethod
+    def norm(x: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
+        """RMSNorm without a learned gain (random-weight stacks): keeps the
+        residual stream's scale bounded across layers."""
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(dim=-1, keepdim=True) + eps)).to(x.dtype)
+
     def forward(self, x: torch.Tensor, stats=None) -> torch.Tensor:
         for l, layer in enumerate(self.layers):
-            y = layer.forward(x, stats=_LayerStats(stats, l) if stats is not None else None)
+            y = layer.forward(self.norm(x), stats=_LayerStats(stats, l) if stats is not None else None)
             x = (x.float() + y.float()).to(x.dtype)
         return x
 

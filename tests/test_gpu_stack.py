@@ -47,8 +47,9 @@ def test_stack_trace_and_placement(stack, tmp_path):
     # per-layer inputs and selections, recomputed layer by layer
     sel, h = [], x
     for layer in stack.layers:
-        sel.append(layer.route(h)[1].cpu().numpy())
-        h = (h.float() + layer.forward(h).float()).to(h.dtype)
+        hn = stack.norm(h)
+        sel.append(layer.route(hn)[1].cpu().numpy())
+        h = (h.float() + layer.forward(hn).float()).to(h.dtype)
     assert torch.equal(h, out)
     counts = stats.counts.cpu().numpy()
     for l in range(L):
@@ -89,7 +90,7 @@ def test_stack_expert_parallel_with_migration(stack):
     def ep_stack(parts):
         hs = list(parts)
         for l in range(L):
-            ys = run_loopback_peer(ranks_per_layer[l], hs)
+            ys = run_loopback_peer(ranks_per_layer[l], [stack.norm(h) for h in hs])
             hs = [(h.float() + y.float()).to(h.dtype) for h, y in zip(hs, ys)]
         return hs
 

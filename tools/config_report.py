@@ -147,7 +147,7 @@ def c3():
                       "(tests/test_gpu_moe.py::test_w8a8_linear[8192-4096-16384])"}
 
 
-def c5(L_=32, T=4096):
+def c5(L_=32, T=16384):
     """32-layer Mixtral-shape W8A8 MoE stack (no attention) on ONE B200, path statistics -> 8-rank placement."""
     from paper_2508_07329_b200.ep import plan_stack_placements
     t0 = time.perf_counter()
