@@ -226,6 +226,23 @@ class MoELayer:
         d2h.synchronize()
         return out_host
 
+    def graphed(self, T: int, out_dtype=None) -> "GraphedForward":
+        """Capture one forward over a fixed token count into a CUDA graph
+        (static input / output buffers): the 10 kernel launches of a step
+        replay as one graph launch — for small, launch-bound batches."""
+        xs = torch.zeros((T, self.d), dtype=torch.bfloat16, device="cuda")
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):          # warm-up outside the capture (kernel attributes, pools)
+            for _ in range(2):
+                self.forward(xs, out_dtype=out_dtype)
+        cur.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ys = self.forward(xs, out_dtype=out_dtype)
+        return GraphedForward(graph, xs, ys)
+
     def forward_host_stream(self, batches: list, depth: int = 2) -> list:
         """Serving loop over several host batches [(x_host, out_host), ...]:
         the same per-batch work as ``forward_host`` (H2D of the batch's
@@ -332,3 +349,19 @@ class _LayerStats:
 
     def record(self, idx):
         self.stats.record(idx, self.layer)
+
+
+class GraphedForward:
+    """A captured ``MoELayer.forward``: call with [T, d] bf16 tokens; returns
+    the static output buffer (overwritten by the next call)."""
+
+    def __init__(self, graph, x_static: torch.Tensor, y_static: torch.Tensor):
+        self.graph, self.x, self.y = graph, x_static, y_static
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        if x.shape != self.x.shape:
+            raise ValueError(f"graph captured for {tuple(self.x.shape)}, got {tuple(x.shape)}")
+        if x.data_ptr() != self.x.data_ptr():
+            self.x.copy_(x)
+        self.graph.replay()
+        return self.y

@@ -167,3 +167,11 @@ def test_forward_host_stream_matches_device(cuda, small_layer):
     outs = small_layer.forward_host_stream([(x, None) for x in xs], depth=2)
     for x, o in zip(xs, outs):
         assert torch.equal(o, small_layer.forward(x.to(cuda)).cpu())
+
+
+def test_graphed_forward_matches_eager(cuda, small_layer):
+    rng = np.random.default_rng(21)
+    g = small_layer.graphed(700)
+    for _ in range(2):
+        x = torch.from_numpy(_x(rng, 700, 512)).to(cuda).bfloat16()
+        assert torch.equal(g(x), small_layer.forward(x))

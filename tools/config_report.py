@@ -106,6 +106,8 @@ def c2():
     x = outliers(rng, 4096, 1024)
     xd = torch.from_numpy(x).cuda().bfloat16()
     ms = dev_ms(lambda: layer.forward(xd))
+    g = layer.graphed(4096)
+    ms_graph = dev_ms(lambda: g(xd))
     out, aux = layer.forward(xd, out_dtype=torch.float32, return_aux=True)
     experts = [layer.expert_host(e) for e in range(8)]
     lg = aux["logits"].cpu().numpy()
@@ -118,7 +120,8 @@ def c2():
     ops_tok = 2 * 6 * 1024 * 3584
     return {"config": "C2 toy MoE d=1024 E=8 top-2 ffn=3584, 4096 tokens",
             "gpu_tokens_per_s": 4096 / (ms / 1e3), "gpu_ms": ms,
-            "layer_int8_tops": 4096 * ops_tok / (ms / 1e3) / 1e12,
+            "gpu_cuda_graph_tokens_per_s": 4096 / (ms_graph / 1e3), "gpu_cuda_graph_ms": ms_graph,
+            "layer_int8_tops": 4096 * ops_tok / (min(ms, ms_graph) / 1e3) / 1e12,
             "cpu_oracle_fakequant_tokens_per_s": 512 / cs, "cpu_cores": os.cpu_count(),
             "parity": f"normwise rel. error vs float64 oracle on the GPU's logits: {rel:.2e} (stagewise bit-exact: "
                       "tests/test_gpu_moe.py::test_moe_c2_stagewise)"}
