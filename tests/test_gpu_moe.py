@@ -84,6 +84,12 @@ def test_moe_c2_stagewise(cuda):
     _stagewise(cuda, T=4096, d=1024, F=3584)
 
 
+@pytest.mark.parametrize("E,k", [(16, 4), (4, 1), (32, 2)])
+def test_moe_expert_counts_stagewise(cuda, E, k):
+    """Other expert counts / top-k: every stage bit-exact / within tolerance."""
+    _stagewise(cuda, T=1024, d=512, F=1024, E=E, k=k, seed=E + k)
+
+
 def test_moe_mixtral_shape_slice_stagewise(cuda):
     _stagewise(cuda, T=512, d=4096, F=14336, seed=3)
 
