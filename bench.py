@@ -357,6 +357,12 @@ def main() -> None:
                 "frac": (achieved / peak_i8) if achieved else None, "traffic": traffic,
                 "peak_note": peak_note,
                 "algorithmic_ops_per_step": gemm_ops,
+                # operands + outputs each touched once: A1 (T k d) + W13 (2 E F d) + h (2 T k F)
+                # + A2 (T k F) + W2 (E d F) + y (2 T k d) bytes
+                "algorithmic_bytes_per_step": (T * TOPK * D + 2 * E * F * D + 2 * T * TOPK * F
+                                               + T * TOPK * F + E * D * F + 2 * T * TOPK * D),
+                "traffic_note": "traffic = ncu dram__bytes_read+write of the two grouped GEMM launches per step "
+                                "(profiles/traffic.json)",
                 "frac_of_spec_4500": (achieved / 4500.0) if achieved else None}
 
     cpu = None
