@@ -879,12 +879,9 @@ template <bool GIVEN>
 static cudaError_t launch_bulk(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                                uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
                                int32_t* rowsum, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(act_quant_bulk_kernel<GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kBulkSmem);
+  {
+    const cudaError_t e = set_max_smem_once(reinterpret_cast<const void*>(act_quant_bulk_kernel<GIVEN>), kBulkSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + kBulkWarps - 1) / kBulkWarps, num_sms()));
   const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;

@@ -779,11 +779,7 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
                             int grid, cudaStream_t s) {
   auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG>;
   constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr_set = true;
-  }
+  MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(kern), bytes));
   if (CG == 1) {
     kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, to, p);
   } else {

@@ -438,12 +438,7 @@ extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int
     ::moe::count_launch();
   } else if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
-    static bool attr = false;
-    if (!attr) {
-      MOE_CUDA_TRY(cudaFuncSetAttribute(router_gate_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024));
-      attr = true;
-    }
+    MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(router_gate_smem_kernel<8>), 200 * 1024));
     const int64_t grid = std::min<int64_t>((T + 15) / 16, num_sms());
     router_gate_smem_kernel<8><<<(unsigned)grid, 512, (size_t)gw_bytes, s>>>(
         static_cast<const __nv_bfloat16*>(x), T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);

@@ -242,11 +242,7 @@ extern "C" moe_status moe_router_gate_tc(const void* x, int64_t T, int64_t d, in
     set_error("router_gate_tc: cuTensorMapEncodeTiled failed");
     return MOE_ECUDA;
   }
-  static bool attr = false;
-  if (!attr) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem));
-    attr = true;
-  }
+  MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(router_tc_kernel), kRtSmem));
   const int64_t tiles = (T + kRtM - 1) / kRtM;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
   router_tc_kernel<<<grid, 128, kRtSmem, as_stream(stream)>>>(tx, tg, T, d, gate_bias, E, k, logits, topk_idx,
