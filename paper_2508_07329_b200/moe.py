@@ -288,6 +288,60 @@ class MoELayer:
         return outs
 
     # ------------------------------------------------------------------
+    def save(self, out_dir) -> None:
+        """Persist the layer in the reference's own formats: every expert
+        matrix as a MOEP ``gpu_int`` blob (quant.py:506-538; byte-identical to
+        precision_pack), the smoothing vectors and router as MOEK float64
+        matrices (numkit.py:110-157), plus a small layer.json."""
+        import json
+        from pathlib import Path
+
+        from . import formats
+        from .quant import precision_pack
+
+        out = Path(out_dir)
+        out.mkdir(parents=True, exist_ok=True)
+        for e in range(self.E):
+            ex = self.host_experts[e]
+            for name in ("w1", "w3", "w2"):
+                (out / f"expert{e}_{name}.moep").write_bytes(precision_pack(ex[name], "gpu_int").blob)
+            for name in ("s13", "s2"):
+                (out / f"expert{e}_{name}.moek").write_bytes(
+                    formats.moek_encode(np.asarray(_np(ex[name]), np.float64).reshape(1, -1)))
+        (out / "gate.moek").write_bytes(formats.moek_encode(self.gate_w.cpu().numpy().astype(np.float64)))
+        if self.gate_b is not None:
+            (out / "gate_bias.moek").write_bytes(
+                formats.moek_encode(self.gate_b.cpu().numpy().astype(np.float64).reshape(1, -1)))
+        (out / "layer.json").write_text(json.dumps({"experts": self.E, "top_k": self.k, "d": self.d, "ffn": self.F,
+                                                    "out_dtype": str(self.out_dtype).replace("torch.", "")}))
+
+    @classmethod
+    def load(cls, in_dir) -> "MoELayer":
+        """Inverse of ``save``: 8-bit MOEP payloads go straight to the device
+        as the u8 GEMM operand (formats.moep_to_device, no repacking)."""
+        import json
+        from pathlib import Path
+
+        from . import formats
+
+        src = Path(in_dir)
+        meta = json.loads((src / "layer.json").read_text())
+        experts = []
+        for e in range(meta["experts"]):
+            ex = {}
+            for name in ("w1", "w3", "w2"):
+                t = formats.moep_to_device((src / f"expert{e}_{name}.moep").read_bytes())
+                ex[name] = QuantizedMatrix(t["codes"], t["scale"], t["zp"], t["bits"], t["granularity"])
+            for name in ("s13", "s2"):
+                ex[name] = formats.moek_decode((src / f"expert{e}_{name}.moek").read_bytes()).ravel()
+            experts.append(ex)
+        gate = formats.moek_decode((src / "gate.moek").read_bytes()).astype(np.float32)
+        gb = src / "gate_bias.moek"
+        bias = formats.moek_decode(gb.read_bytes()).ravel().astype(np.float32) if gb.exists() else None
+        return cls(gate, experts, top_k=meta["top_k"], out_dtype=getattr(torch, meta["out_dtype"]),
+                   gate_bias=bias)
+
+    # ------------------------------------------------------------------
     def expert_host(self, e: int) -> dict:
         """Host copies of expert e in the oracle's layout (codes/scales/zps of
         w1, w3, w2 and the smoothing vectors) — for parity tests and the CPU

@@ -181,3 +181,17 @@ def test_graphed_forward_matches_eager(cuda, small_layer):
     for _ in range(2):
         x = torch.from_numpy(_x(rng, 700, 512)).to(cuda).bfloat16()
         assert torch.equal(g(x), small_layer.forward(x))
+
+
+def test_layer_save_load_reference_formats(cuda, small_layer, tmp_path):
+    """save -> MOEP gpu_int blobs (byte-identical to the oracle's packing of
+    the same codes) + MOEK vectors; load uploads the 8-bit payloads as the
+    GEMM operand; the reloaded layer's forward is bit-identical."""
+    from oracle import quant_ref as Q
+    small_layer.save(tmp_path)
+    ex0 = small_layer.expert_host(0)
+    blob = (tmp_path / "expert0_w2.moep").read_bytes()
+    assert blob == Q.pack_gpu_int(ex0["w2_codes"], ex0["w2_scale"], ex0["w2_zp"], 8, "per_output_row")
+    back = MoELayer.load(tmp_path)
+    x = torch.from_numpy(_x(np.random.default_rng(31), 600, 512)).to(cuda).bfloat16()
+    assert torch.equal(back.forward(x), small_layer.forward(x))
