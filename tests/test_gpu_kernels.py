@@ -242,7 +242,9 @@ def _dev_operand(cuda, codes, zp, scale):
 @pytest.mark.parametrize("M_,N,K", [(300, 512, 512), (128, 256, 4096), (1000, 768, 272), (77, 40, 48),
                                     (513, 1024, 14336),
                                     # CTA-pair (cta_group::2) path: M >= 2048, ragged last tile
-                                    (2500, 768, 4096), (4096, 512, 1024), (2049, 256, 14336)])
+                                    (2500, 768, 4096), (4096, 512, 1024), (2049, 256, 14336),
+                                    # N not a multiple of the 256-wide tile (partial last N tile)
+                                    (2300, 200, 512), (700, 328, 256)])
 def test_gemm_accumulators_bitexact(cuda, M_, N, K):
     rng = np.random.default_rng(M_ * 7 + N + K)
     a = _rand_operand(rng, M_, K)
