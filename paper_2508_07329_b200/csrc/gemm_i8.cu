@@ -83,7 +83,12 @@ struct Smem {
   static constexpr int kTableOff = kTmemPtrOff + 16;                  // tile_start[G+1], off[G+1]
   static constexpr int kOutOff = (kTableOff + 2 * (kMaxGroups + 1) * 4 + 127) / 128 * 128;
   static constexpr int kOutBytes = kEpiWarps * 2 * 1024;               // per epilogue warp 2 x (32 rows x 32 B)
-  static constexpr int kBytes = kOutOff + kOutBytes + 1024;           // + alignment slack
+  // SwiGLU: per-tile W column parameters (zw, t = rowsum - Kc*zw, ws) and the
+  // next layer's f32 reciprocal smoothing, staged by the epilogue warps while
+  // they wait for the tile's accumulators (double-buffered)
+  static constexpr int kParamBuf = BN * 12 + (BN / 2) * 4;
+  static constexpr int kParamOff = kOutOff + kOutBytes;
+  static constexpr int kBytes = kParamOff + 2 * kParamBuf + 1024;     // + alignment slack
 };
 
 struct TileInfo {
@@ -268,14 +273,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
 template <int BN, bool BF16>
 __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase, int half,
                                             ExtRec& ext, bool rvalid, float sa, float rw, int32_t za, int32_t rsa,
-                                            const CUtensorMap* tmO, uint8_t* obuf, uint32_t& ob) {
+                                            const CUtensorMap* tmO, uint8_t* obuf, uint32_t& ob,
+                                            const uint8_t* pbuf) {
   constexpr int kSub = 16;
   constexpr int kNSubAll = BN / 2 / kSub;          // sub-chunks of a tile row (BN/2 h columns)
   constexpr int kIters = (kNSubAll + kParts - 1) / kParts;
   const int wbase = ti.g * p.N;
-  const uint32_t nrsa = 0u - (uint32_t)rsa, nza = 0u - (uint32_t)za, kc = (uint32_t)p.Kc;
+  const uint32_t nrsa = 0u - (uint32_t)rsa, nza = 0u - (uint32_t)za;
   const float2 sa2 = make_float2(sa, sa), srw2 = make_float2(sa * rw, sa * rw);
   const float2 nl2 = make_float2(-1.4426950408889634f, -1.4426950408889634f), one2 = make_float2(1.f, 1.f);
+  // this tile's staged column parameters (shared memory)
+  const int32_t* zw_s = reinterpret_cast<const int32_t*>(pbuf);
+  const int32_t* t_s = zw_s + BN;
+  const float* ws_s = reinterpret_cast<const float*>(t_s + BN);
+  const float* ns_s = ws_s + BN;
   // whole-warp TMA store of the 32 x 16 h block when all 32 rows are in the group
   const bool tma = BF16 && p.tma_out && __all_sync(0xffffffffu, rvalid);
   const int lane = threadIdx.x & 31;
@@ -293,19 +304,18 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
       tmem_ld16(tbase + hc + kParts * kSub, ag[cur ^ 1]);
       tmem_ld16(tbase + BN / 2 + hc + kParts * kSub, au[cur ^ 1]);
     }
-    const int ng0 = wbase + ti.n0 + hc;
-    const int4* gz = reinterpret_cast<const int4*>(p.w_zp + ng0);
-    const int4* gr = reinterpret_cast<const int4*>(p.w_rowsum + ng0);
-    const float4* gs = reinterpret_cast<const float4*>(p.w_scale + ng0);
-    const int4* uz = reinterpret_cast<const int4*>(p.w_zp + ng0 + BN / 2);
-    const int4* ur = reinterpret_cast<const int4*>(p.w_rowsum + ng0 + BN / 2);
-    const float4* us = reinterpret_cast<const float4*>(p.w_scale + ng0 + BN / 2);
+    const int4* gz = reinterpret_cast<const int4*>(zw_s + hc);
+    const int4* gr = reinterpret_cast<const int4*>(t_s + hc);
+    const float4* gs = reinterpret_cast<const float4*>(ws_s + hc);
+    const int4* uz = reinterpret_cast<const int4*>(zw_s + BN / 2 + hc);
+    const int4* ur = reinterpret_cast<const int4*>(t_s + BN / 2 + hc);
+    const float4* us = reinterpret_cast<const float4*>(ws_s + BN / 2 + hc);
     uint32_t hb[kSub / 2];                         // packed bf16 pairs (BF16) 
     float h[kSub];
 #pragma unroll
     for (int q = 0; q < kSub / 4; ++q) {
-      const int4 z4g = __ldg(gz + q), r4g = __ldg(gr + q), z4u = __ldg(uz + q), r4u = __ldg(ur + q);
-      const float4 s4g = __ldg(gs + q), s4u = __ldg(us + q);
+      const int4 z4g = gz[q], r4g = gr[q], z4u = uz[q], r4u = ur[q];
+      const float4 s4g = gs[q], s4u = us[q];
       const int32_t zg[4] = {z4g.x, z4g.y, z4g.z, z4g.w}, rg[4] = {r4g.x, r4g.y, r4g.z, r4g.w};
       const int32_t zu[4] = {z4u.x, z4u.y, z4u.z, z4u.w}, ru[4] = {r4u.x, r4u.y, r4u.z, r4u.w};
       const float sg4[4] = {s4g.x, s4g.y, s4g.z, s4g.w}, su4[4] = {s4u.x, s4u.y, s4u.z, s4u.w};
@@ -315,10 +325,8 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
         int32_t ai[4];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const uint32_t tg = (uint32_t)rg[e2 + e] - kc * (uint32_t)zg[e2 + e];   // kc == 0: pre-corrected
-          const uint32_t tu = (uint32_t)ru[e2 + e] - kc * (uint32_t)zu[e2 + e];
-          ai[e] = (int32_t)(ag[cur][j + e] + (uint32_t)zg[e2 + e] * nrsa + tg * nza);
-          ai[2 + e] = (int32_t)(au[cur][j + e] + (uint32_t)zu[e2 + e] * nrsa + tu * nza);
+          ai[e] = (int32_t)(ag[cur][j + e] + (uint32_t)zg[e2 + e] * nrsa + (uint32_t)rg[e2 + e] * nza);
+          ai[2 + e] = (int32_t)(au[cur][j + e] + (uint32_t)zu[e2 + e] * nrsa + (uint32_t)ru[e2 + e] * nza);
         }
         const float2 g = __fmul2_rn(make_float2((float)ai[0], (float)ai[1]),
                                     __fmul2_rn(sa2, make_float2(sg4[e2], sg4[e2 + 1])));
@@ -372,11 +380,11 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
     }
     if (rvalid) {
       if (p.row_ext) {
-        const float4* t4 = reinterpret_cast<const float4*>(p.ns_rs32 + ti.g * p.ns_ld + ti.n0 / 2 + hc);
+        const float4* t4 = reinterpret_cast<const float4*>(ns_s + hc);
         float xs[kSub];
 #pragma unroll
         for (int q = 0; q < kSub / 4; ++q) {
-          const float4 tt = __ldg(t4 + q);
+          const float4 tt = t4[q];
           const float2 a = __fmul2_rn(make_float2(h[4 * q], h[4 * q + 1]), make_float2(tt.x, tt.y));
           const float2 b = __fmul2_rn(make_float2(h[4 * q + 2], h[4 * q + 3]), make_float2(tt.z, tt.w));
           xs[4 * q] = a.x;
@@ -407,7 +415,7 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
 template <int BN, int EPI, bool BF16>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase,
                                               int half, ExtRec& ext, const CUtensorMap* tmO, uint8_t* obuf,
-                                              uint32_t& ob) {
+                                              uint32_t& ob, const uint8_t* pbuf) {
   const bool rvalid = row < ti.m_end;
   float sa = 0.f, rw = 1.f;
   int32_t za = 0, rsa = 0;
@@ -421,7 +429,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
   }
   const int wbase = ti.g * p.N;
   if (EPI == MOE_EPI_SWIGLU && p.param_vec_ok && !p.bias && (BN / 4) % 16 == 0) {
-    swiglu_fast<BN, BF16>(p, ti, row, tbase, half, ext, rvalid, sa, rw, za, rsa, tmO, obuf, ob);
+    swiglu_fast<BN, BF16>(p, ti, row, tbase, half, ext, rvalid, sa, rw, za, rsa, tmO, obuf, ob, pbuf);
   } else if (EPI == MOE_EPI_SWIGLU) {
     // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
 #pragma unroll 1
@@ -673,12 +681,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
       const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
+      uint8_t* pbuf = smem + L::kParamOff + (tile_it & 1) * L::kParamBuf;
+      if constexpr (EPI == MOE_EPI_SWIGLU) {
+        if (p.param_vec_ok && !p.bias) {
+          // stage this tile's column parameters while the MMAs run (the loads'
+          // latency overlaps the accumulator wait)
+          int32_t* zw_s = reinterpret_cast<int32_t*>(pbuf);
+          int32_t* t_s = zw_s + BN;
+          float* ws_s = reinterpret_cast<float*>(t_s + BN);
+          float* ns_s = ws_s + BN;
+          for (int e = threadIdx.x - 128; e < BN; e += 32 * kEpiWarps) {
+            const int n = ti.g * p.N + ti.n0 + e;
+            const int32_t z = p.w_zp[n];
+            zw_s[e] = z;
+            t_s[e] = (int32_t)((uint32_t)p.w_rowsum[n] - (uint32_t)p.Kc * (uint32_t)z);
+            ws_s[e] = p.w_scale[n];
+            if (p.row_ext && e < BN / 2) ns_s[e] = p.ns_rs32[ti.g * p.ns_ld + ti.n0 / 2 + e];
+          }
+          named_bar_sync(1, 32 * kEpiWarps);
+        }
+      }
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
-      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob);
+      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob, pbuf);
       tc_fence_before();
       if (CG == 2) mbar_arrive_leader(&tempty[as]);
       else mbar_arrive(&tempty[as]);
