@@ -121,7 +121,7 @@ class MoELayer:
         return logits, idx, w
 
     def forward(self, x: torch.Tensor, out_dtype=None, y_dtype=None, return_aux: bool = False, stats=None,
-                timer=None):
+                timer=None, out: torch.Tensor | None = None):
         """x [T, d] (bf16) on device -> [T, d]. ``timer`` (optional) gets a
         ``mark(stage)`` call after every kernel stage (CUDA events)."""
         if x.dim() != 2 or x.shape[1] != self.d:
@@ -155,7 +155,7 @@ class MoELayer:
         y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)
         mark("gemm2")
-        out = ops.combine(y, perm["token_pos"], T, self.k, out_dtype=out_dtype)
+        out = ops.combine(y, perm["token_pos"], T, self.k, out_dtype=out_dtype, out=out)
         mark("combine")
         if return_aux:
             return out, {"logits": logits, "idx": idx, "w": w, "perm": perm, "a1": a1, "h": h, "a2": a2, "y": y}
@@ -247,10 +247,12 @@ class MoELayer:
         """Serving loop over several host batches [(x_host, out_host), ...]:
         the same per-batch work as ``forward_host`` (H2D of the batch's
         tokens, forward, D2H of its result), software-pipelined ACROSS
-        batches on three streams with ``depth`` device staging buffers, so
-        the H2D of batch b+1 and the D2H of batch b-1 overlap the forward of
-        batch b. Every batch is forwarded whole (no per-chunk weight
-        re-streaming). Returns the out_host tensors after the last D2H."""
+        batches on three streams with ``depth`` device staging buffers for
+        the inputs and ``depth`` for the outputs, so the H2D of batch b+1 and
+        the D2H of batch b-1 overlap the forward of batch b. Every batch is
+        forwarded whole (no per-chunk weight re-streaming); the staging ring
+        keeps the allocator out of the loop (no cross-stream frees).
+        Returns the out_host tensors after the last D2H."""
         if not batches:
             return []
         T = max(x.shape[0] for x, _ in batches)
@@ -258,14 +260,16 @@ class MoELayer:
         io = getattr(self, "_stream_io", None)
         if io is None or io["bufs"][0].shape[0] < T or len(io["bufs"]) < depth:
             io = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
-                  "bufs": [torch.empty((T, self.d), dtype=batches[0][0].dtype, device="cuda") for _ in range(depth)]}
+                  "bufs": [torch.empty((T, self.d), dtype=batches[0][0].dtype, device="cuda") for _ in range(depth)],
+                  "outs": [torch.empty((T, self.d), dtype=self.out_dtype, device="cuda") for _ in range(depth)]}
             self._stream_io = io
-        h2d, d2h, bufs = io["h2d"], io["d2h"], io["bufs"]
+        h2d, d2h, bufs, obufs = io["h2d"], io["d2h"], io["bufs"], io["outs"]
         h2d.wait_stream(cur)
-        done = [None] * len(batches)          # forward of batch i finished (its staging slot is free)
+        done = [None] * len(batches)          # forward of batch i finished (its input slot is free)
+        copied = [None] * len(batches)        # D2H of batch i finished (its output slot is free)
         outs = []
         for i, (xh, oh) in enumerate(batches):
-            slot = bufs[i % depth]
+            slot, oslot = bufs[i % depth], obufs[i % depth]
             n = xh.shape[0]
             if oh is None:
                 oh = torch.empty((n, self.d), dtype=self.out_dtype, pin_memory=True)
@@ -276,13 +280,16 @@ class MoELayer:
                 loaded = torch.cuda.Event()
                 loaded.record(h2d)
             cur.wait_event(loaded)
-            y = self.forward(slot[:n])
+            if i >= depth:
+                cur.wait_event(copied[i - depth])
+            self.forward(slot[:n], out=oslot[:n])
             done[i] = torch.cuda.Event()
             done[i].record(cur)
-            d2h.wait_event(done[i])
             with torch.cuda.stream(d2h):
-                oh.copy_(y, non_blocking=True)
-            y.record_stream(d2h)
+                d2h.wait_event(done[i])
+                oh.copy_(oslot[:n], non_blocking=True)
+                copied[i] = torch.cuda.Event()
+                copied[i].record(d2h)
             outs.append(oh)
         d2h.synchronize()
         return outs
