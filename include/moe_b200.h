@@ -71,6 +71,18 @@ int moe_abi_version(void);
 uint64_t moe_launch_count(void);
 /* 0 if device `dev` is an sm_100 part the kernels were built for. */
 moe_status moe_device_check(int dev);
+/* Process-wide kernel-selection knobs (atomic; results never depend on them,
+ * only which of the bit-identical kernels runs). Sets `key` to `value` and
+ * returns the previous value in *old (optional); value < 0 only queries.
+ *   MOE_TUNE_K1_SMALL_ROWS: per-token K1 calls with at most this many rows
+ *   use the CTA-per-row kernel instead of the per-warp fast kernels
+ *   (default 256; env MOE_B200_K1_SMALL sets the initial value).
+ *   MOE_TUNE_ROUTER_CLUSTER_TILES: tensor-core router calls with at most
+ *   this many 128-token tiles split K over a thread-block cluster; larger
+ *   ones use the persistent multi-accumulator kernel (same logits;
+ *   default 64 tiles). */
+enum { MOE_TUNE_K1_SMALL_ROWS = 1, MOE_TUNE_ROUTER_CLUSTER_TILES = 2 };
+moe_status moe_tune(int key, int64_t value, int64_t* old);
 
 /* ---- K1: smoothing + RTN affine quantization ----------------------------
  * Replaces quant.rtn_quantize (quant.py:214-231) applied to

@@ -22,6 +22,8 @@ GRAN = {"per_tensor": 0, "per_token": 1, "per_output_row": 2}
 SMOOTH_NONE, SMOOTH_DIVIDE, SMOOTH_MULTIPLY = 0, 1, 2
 EPI_DEQUANT, EPI_SWIGLU, EPI_ACC_I32 = 0, 1, 2
 EPI_FLAG_WCORR = 0x100
+TUNE_K1_SMALL_ROWS = 1
+TUNE_ROUTER_CLUSTER_TILES = 2
 ORDER_MAX_ABS, ORDER_SUM_SQUARES = 1, 2
 
 _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double
@@ -32,6 +34,7 @@ _SIGS = {
     "moe_abi_version": (_I, []),
     "moe_launch_count": (C.c_uint64, []),
     "moe_device_check": (_I, [_I]),
+    "moe_tune": (_I, [_I, _I64, _P]),
     "moe_act_quant_workspace": (_I64, [_I64, _I64, _I]),
     "moe_act_quant": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _I64, _P, _P,
                            _P, _P, _P, _P, _I64, _P]),
@@ -152,3 +155,26 @@ def call(name: str, *args, what: str | None = None):
 
 
 _SYNC = os.environ.get("MOE_B200_SYNC", "0") == "1"   # debug: synchronize after every entry point
+
+
+def tune(key: int, value: int = -1) -> int:
+    """Set a kernel-selection knob (``moe_tune``); returns the previous
+    value (value < 0 only queries). Results never depend on the knobs."""
+    lib = load_library()
+    old = C.c_int64(0)
+    check(lib.moe_tune(key, value, C.byref(old)), "moe_tune")
+    return int(old.value)
+
+
+class tuned:
+    """Context manager: ``with tuned(TUNE_K1_SMALL_ROWS, 0): ...``."""
+
+    def __init__(self, key: int, value: int):
+        self.key, self.value = key, value
+
+    def __enter__(self):
+        self.old = tune(self.key, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        tune(self.key, self.old)

@@ -875,6 +875,204 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
 }
 
+// ── CTA-per-row variant for small row counts ───────────────────────────────
+// Decode-size batches have a few dozen rows: one warp per row leaves most
+// SMs idle and runs each row as one long dependent chain (~25 us for 32
+// rows). Here a 512-thread CTA owns one row, every thread holds up to four
+// 16-byte vectors of it in registers (rows up to 16384 bf16), and the
+// per-row reductions are block-wide; the per-vector arithmetic (float32
+// filter, speculative extremes, candidate count, exact fallback) is the
+// warp kernel's, so the results are identical.
+constexpr int kCtaThreads = 512;
+constexpr int kCtaNV = 4;
+
+struct OpMaxU64 {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a > b ? a : b; }
+};
+struct OpMinU64 {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a < b ? a : b; }
+};
+// order-preserving 32-bit key of a float (no NaNs here)
+__device__ __forceinline__ uint32_t fkey(float v) {
+  const uint32_t b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+struct CtaRowState {
+  RowExt rec;
+  AffineParams p;
+  FastRow f;
+  float lb_max, ub_min;
+  int mode;
+  bool exact_all;
+};
+
+template <bool GIVEN>
+__global__ void __launch_bounds__(kCtaThreads)
+    act_quant_cta_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
+                         int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                         int32_t* zp, int32_t* rowsum) {
+  __shared__ unsigned long long sh64[kCtaThreads / 32];
+  __shared__ double shd[kCtaThreads / 32];
+  __shared__ int64_t shi[kCtaThreads / 32];
+  __shared__ CtaRowState st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r = blockIdx.x;
+  const int64_t nvec = a.cols / 8;
+  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
+  const RowView rv = row_view(a, r);
+  const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + rv.off;
+  const uint4* src = reinterpret_cast<const uint4*>(row);
+  const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;
+  const double* srow = smooth ? a.sm.s + rv.gbase : nullptr;
+  const double* rrow = smooth ? a.sm.rs + rv.gbase : nullptr;
+  uint2* dst = reinterpret_cast<uint2*>(out_row_ptr(a, codes, ldc, r));
+
+  uint4 u[kCtaNV];
+#pragma unroll
+  for (int i = 0; i < kCtaNV; ++i) {
+    const int64_t c = tid + (int64_t)i * kCtaThreads;
+    u[i] = c < nvec ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (GIVEN) {
+    if (warp == 0) {
+      const RowExt rec = given_record(row, tab, a.cols, ext[2 * r + 1], ext[2 * r], lane);
+      if (lane == 0) st.rec = rec;
+    }
+  } else {
+    // pass A: float32 extremes and a column holding each (larger / smaller
+    // value wins, ties to the lower column)
+    float tmax = -FLT_MAX, tmin = FLT_MAX;
+    int64_t imax = 0, imin = 0;
+#pragma unroll
+    for (int i = 0; i < kCtaNV; ++i) {
+      const int64_t c = tid + (int64_t)i * kCtaThreads;
+      if (c >= nvec) continue;
+      float xs[8];
+      smooth8(u[i], tab, c, xs);
+      const float vmax = max8(xs), vmin = min8(xs);
+      if (vmax > tmax) {
+        int j = 0;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) j = xs[e] == vmax ? e : j;
+        tmax = vmax;
+        imax = c * 8 + j;
+      }
+      if (vmin < tmin) {
+        int j = 0;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) j = xs[e] == vmin ? e : j;
+        tmin = vmin;
+        imin = c * 8 + j;
+      }
+    }
+    const unsigned long long kM = block_reduce(
+        ((unsigned long long)fkey(tmax) << 32) | (0xFFFFFFFFu - (uint32_t)imax), sh64, OpMaxU64());
+    const unsigned long long km = block_reduce(((unsigned long long)fkey(tmin) << 32) | (uint32_t)imin, sh64,
+                                               OpMinU64());
+    if (tid == 0)
+      st.rec = RowExt{funkey((uint32_t)(kM >> 32)), funkey((uint32_t)(km >> 32)),
+                      (int64_t)(0xFFFFFFFFu - (uint32_t)kM), (int64_t)(uint32_t)km};
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const RowExt rec = st.rec;
+    const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m)) || rec.cM >= a.cols || rec.cm >= a.cols;
+    bool spec = !exact_all;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    if (spec) {
+      mx = exact_at(row, tab, srow, rrow, rec.cM, rec.M, spec);
+      mn = exact_at(row, tab, srow, rrow, rec.cm, rec.m, spec);
+    }
+    st.lb_max = spec ? rec.M - err_bound(rec.M) : -FLT_MAX;
+    st.ub_min = spec ? rec.m + err_bound(rec.m) : FLT_MAX;
+    st.exact_all = exact_all;
+    st.mode = 0;
+    if (spec) {
+      st.p = affine_params(mn, mx, bits, sym);
+      st.mode = init_fast_row(st.f, st.p, rec.M, rec.m, mn, mx, bits, sym);
+    }
+  }
+  __syncthreads();
+  const int mode = st.mode;
+  AffineParams p = st.p;
+  int sum = 0;
+  bool done = false;
+  if (mode) {
+    const FastRow f = st.f;
+    uint32_t cnt = 0;
+    auto run = [&](auto gen) {
+      constexpr bool G = decltype(gen)::value;
+#pragma unroll
+      for (int i = 0; i < kCtaNV; ++i) {
+        const int64_t c = tid + (int64_t)i * kCtaThreads;
+        if (c >= nvec) continue;
+        const uint2 out = fast_vec8<G>(u[i], c, tab, srow, rrow, f, cnt);
+        sum += bytesum(out);
+        __stcs(dst + c, out);
+      }
+    };
+    if (mode == 1) run(std::false_type{});
+    else run(std::true_type{});
+    sum = (int)block_reduce((int64_t)sum, shi, OpAdd());
+    done = (uint32_t)block_reduce((int64_t)cnt, shi, OpAdd()) == f.expect;
+  }
+  if (!done) {
+    // exact extremes over every element that can reach them, then the
+    // generic encode (as fallback_row, block-wide)
+    const float lb_max = st.lb_max, ub_min = st.ub_min;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+#pragma unroll
+    for (int i = 0; i < kCtaNV; ++i) {
+      const int64_t c = tid + (int64_t)i * kCtaThreads;
+      if (c >= nvec) continue;
+      float xs[8];
+      smooth8(u[i], tab, c, xs);
+      uint32_t mmax = 0, mmin = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        mmax |= (uint32_t)(!(xs[e] + err_bound(xs[e]) < lb_max)) << e;
+        mmin |= (uint32_t)(!(xs[e] - err_bound(xs[e]) > ub_min)) << e;
+      }
+      if (mmax | mmin) {
+        const double2 e2 = exact_extremes8(u[i], srow, rrow, c, mmax, mmin);
+        mn = fmin(mn, e2.x);
+        mx = fmax(mx, e2.y);
+      }
+    }
+    mn = block_reduce(mn, shd, OpMin());
+    mx = block_reduce(mx, shd, OpMax());
+    p = affine_params(mn, mx, bits, sym);
+    const RowEncoder enc(p, mn, mx, bits, st.exact_all);
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kCtaNV; ++i) {
+      const int64_t c = tid + (int64_t)i * kCtaThreads;
+      if (c >= nvec) continue;
+      float xs[8];
+      smooth8(u[i], tab, c, xs);
+      __stcs(dst + c, enc.encode8(u[i], xs, c, srow, rrow, s));
+    }
+    sum = (int)block_reduce((int64_t)s, shi, OpAdd());
+  }
+  if (tid == 0) {
+    if (a.ep.codes_tab) {
+      const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
+      a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
+          make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
+    } else {
+      if (rowsum) rowsum[r] = sum;
+      scale[r] = p.scale;
+      if (scale_f32) scale_f32[r] = (float)p.scale;
+      zp[r] = p.zp;
+    }
+  }
+  if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
+}
+
 template <bool GIVEN>
 static cudaError_t launch_bulk(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                                uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
@@ -917,6 +1115,8 @@ static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long 
 // need their own extreme pass (x, gathered) use the register kernel, whose
 // second pass and the router's just-read rows hit L1/L2 (in the step: 222 vs
 // 258 us). MOE_B200_K1_CFG=0 / 7 forces one kernel for both (A/B runs).
+// Calls with at most MOE_TUNE_K1_SMALL_ROWS rows (decode-size batches) use
+// the CTA-per-row kernel (tools/k1_small.py).
 template <bool GIVEN>
 static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsigned long long* ext, int bits, int sym,
                               uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
@@ -925,6 +1125,12 @@ static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsign
     const char* env = getenv("MOE_B200_K1_CFG");
     return env ? atoi(env) : -1;
   }();
+  if (a.rows <= k1_small_rows() && a.cols <= (int64_t)kCtaNV * kCtaThreads * 8) {
+    act_quant_cta_kernel<GIVEN><<<(unsigned)a.rows, kCtaThreads, 0, s>>>(a, rs32, ext, bits, sym, codes, ldc, scale,
+                                                                          scale_f32, zp, rowsum);
+    count_launch();
+    return cudaGetLastError();
+  }
   const bool bulk = forced == 7 || (forced < 0 && GIVEN);
   if (bulk) return launch_bulk<GIVEN>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
   launch_cfg<GIVEN, 16, 2>(a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);

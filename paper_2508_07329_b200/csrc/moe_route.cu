@@ -321,17 +321,12 @@ __global__ void permute_scan_kernel(const int32_t* block_counts, int nblocks, in
   }
 }
 
-__global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t* idx, const float* topk_w,
-                                                                       int64_t n, int k, int E,
-                                                                       const int32_t* block_base,
-                                                                       int32_t* src_token, int32_t* row_expert,
-                                                                       float* row_weight, int32_t* token_pos) {
-  __shared__ int run[kMaxE];
-  __shared__ int wcnt[kPermThreads / 32][kMaxE];
+// stable scatter of pairs [lo, hi) given each expert's first free row (run[])
+__device__ __forceinline__ void permute_scatter_range(const int32_t* idx, const float* topk_w, int64_t lo, int64_t hi,
+                                                      int k, int E, int* run, int (*wcnt)[kMaxE],
+                                                      int32_t* src_token, int32_t* row_expert, float* row_weight,
+                                                      int32_t* token_pos) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = block_base[(int64_t)blockIdx.x * E + e];
-  const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
-  const int64_t hi = min(n, lo + kPermChunk);
   for (int64_t base = lo; base < hi; base += kPermThreads) {
     for (int i = threadIdx.x; i < (kPermThreads / 32) * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
     __syncthreads();
@@ -358,6 +353,45 @@ __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t* idx, const float* topk_w,
+                                                                       int64_t n, int k, int E,
+                                                                       const int32_t* block_base,
+                                                                       int32_t* src_token, int32_t* row_expert,
+                                                                       float* row_weight, int32_t* token_pos) {
+  __shared__ int run[kMaxE];
+  __shared__ int wcnt[kPermThreads / 32][kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = block_base[(int64_t)blockIdx.x * E + e];
+  const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
+  permute_scatter_range(idx, topk_w, lo, min(n, lo + kPermChunk), k, E, run, wcnt, src_token, row_expert, row_weight,
+                        token_pos);
+}
+
+// Batches of at most kPermChunk pairs (decode sizes): count, scan and
+// scatter in one block — one launch instead of three, same permutation.
+__global__ void __launch_bounds__(kPermThreads) permute_single_kernel(const int32_t* idx, const float* topk_w,
+                                                                      int64_t n, int k, int E, int32_t* offsets,
+                                                                      int32_t* src_token, int32_t* row_expert,
+                                                                      float* row_weight, int32_t* token_pos) {
+  __shared__ int run[kMaxE];
+  __shared__ int wcnt[kPermThreads / 32][kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&run[idx[i]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = run[e];
+      offsets[e] = s;
+      run[e] = s;
+      s += c;
+    }
+    offsets[E] = s;
+  }
+  __syncthreads();
+  permute_scatter_range(idx, topk_w, 0, n, k, E, run, wcnt, src_token, row_expert, row_weight, token_pos);
 }
 
 // ── combine ────────────────────────────────────────────────────────────────
@@ -482,6 +516,13 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
   int32_t* counts = static_cast<int32_t*>(workspace);
   int32_t* base = counts + (int64_t)nb * E;
   cudaStream_t s = as_stream(stream);
+  if (nb == 1) {
+    permute_single_kernel<<<1, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, expert_offsets, src_token,
+                                                     row_expert, row_weight, token_pos);
+    ::moe::count_launch();
+    MOE_LAUNCH_CHECK();
+    return MOE_OK;
+  }
   permute_count_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, n, E, counts); ::moe::count_launch();
   permute_scan_kernel<<<1, 64, 0, s>>>(counts, nb, E, base, expert_offsets); ::moe::count_launch();
   permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, base, src_token, row_expert,

@@ -143,7 +143,9 @@ class MoELayer:
         mark("quant_x")
         # the SwiGLU epilogue also emits each h row's (value, column) records
         # of the float32 min/max of h * RN32(1/s2), so the second K1 streams h once
-        fuse = self.d % 16 == 0 and self.d >= 128
+        # (decode-size batches go through K1's CTA-per-row kernel, whose own
+        # extreme pass is cheaper than initialising and filling the records)
+        fuse = self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS)
         ext = torch.empty((T * self.k, 2), dtype=torch.int64, device=x.device) if fuse else None
         h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,

@@ -40,3 +40,13 @@ def cuda():
     from paper_2508_07329_b200 import _lib
     _lib.load()
     return torch.device("cuda:0")
+
+
+@pytest.fixture(params=["warp", "cta"])
+def k1_kernel(request, cuda):
+    """Run a K1 test through each of the bit-identical per-token kernels:
+    the per-warp / bulk kernels ("warp") and the CTA-per-row kernel the
+    library picks for small row counts ("cta")."""
+    from paper_2508_07329_b200 import _lib
+    with _lib.tuned(_lib.TUNE_K1_SMALL_ROWS, 0 if request.param == "warp" else 1 << 40):
+        yield request.param

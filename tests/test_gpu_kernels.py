@@ -35,7 +35,7 @@ def _smooth(rng, G, d):
 
 # ── K1 ───────────────────────────────────────────────────────────────────
 @pytest.mark.parametrize("T,d", [(64, 96), (257, 1024), (1024, 4096), (33, 14336)])
-def test_act_quant_per_token_bitexact(cuda, T, d):
+def test_act_quant_per_token_bitexact(cuda, T, d, k1_kernel):
     rng = np.random.default_rng(T + d)
     x = _acts(rng, T, d)
     s = _smooth(rng, 1, d)
@@ -48,7 +48,7 @@ def test_act_quant_per_token_bitexact(cuda, T, d):
     np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
 
 
-def test_act_quant_gather_grouped_bitexact(cuda):
+def test_act_quant_gather_grouped_bitexact(cuda, k1_kernel):
     rng = np.random.default_rng(5)
     T, d, G = 300, 512, 8
     x = _acts(rng, T, d)
@@ -65,7 +65,7 @@ def test_act_quant_gather_grouped_bitexact(cuda):
 
 
 @pytest.mark.parametrize("sym", [False, True])
-def test_act_quant_one_sided_rows(cuda, sym):
+def test_act_quant_one_sided_rows(cuda, sym, k1_kernel):
     """ReLU-like rows (min exactly 0, many zeros), non-positive rows and
     symmetric codes take the general fast path (code window [0, 255] plus an
     explicit candidate check, zero extremes exempt): bit-exact vs the oracle."""
@@ -88,7 +88,7 @@ def test_act_quant_one_sided_rows(cuda, sym):
     np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), codes.astype(np.int64).sum(1))
 
 
-def test_act_quant_golden_k1(cuda, golden):
+def test_act_quant_golden_k1(cuda, golden, k1_kernel):
     x = golden["k1_x_bf16"]
     r = ops.act_quant(torch.from_numpy(x.astype(np.float32)).to(cuda).bfloat16(),
                       smooth=torch.from_numpy(golden["k1_smooth"]).to(cuda))
@@ -97,7 +97,7 @@ def test_act_quant_golden_k1(cuda, golden):
     np.testing.assert_array_equal(r["zp"].cpu().numpy(), golden["k1_zps"])
 
 
-def test_act_quant_bf16_fast_path_ties(cuda):
+def test_act_quant_bf16_fast_path_ties(cuda, k1_kernel):
     """bf16 rows whose quotients land exactly on k + 0.5 (and next to it), plus
     all-positive rows far from zero (clip saturation) — the cases where the
     float32 filter must defer to the exact float64 path."""
@@ -121,7 +121,7 @@ def test_act_quant_bf16_fast_path_ties(cuda):
         np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
 
 
-def test_act_quant_edge_values(cuda):
+def test_act_quant_edge_values(cuda, k1_kernel):
     # constant rows (scale floor), all-zero rows, exact ties at .5 of the grid,
     # negative zero
     x = np.zeros((6, 64))
@@ -156,7 +156,7 @@ def _true_records(x32, recip32):
     return np.stack([_ext_key(xs[r, cm], cm), _ext_key(xs[r, cM], cM)], 1)
 
 
-def test_act_quant_row_ext_speculation(cuda):
+def test_act_quant_row_ext_speculation(cuda, k1_kernel):
     """K1 fed (value, column) extreme records: correct records, records that
     point at the wrong element, stale values, duplicated extremes, empty
     (never-written) records and out-of-range columns all give the exact
@@ -187,7 +187,7 @@ def test_act_quant_row_ext_speculation(cuda):
             np.testing.assert_array_equal(got.cpu().numpy(), exp)
 
 
-def test_swiglu_row_ext_feeds_k1(cuda):
+def test_swiglu_row_ext_feeds_k1(cuda, k1_kernel):
     """The grouped SwiGLU epilogue's extreme records of h * RN32(1/s2) match
     the stored bf16 h, and K1 fed those records equals K1 without them."""
     rng = np.random.default_rng(22)
@@ -337,6 +337,30 @@ def test_router_gate_topk(cuda, E, k, T, d, tc):
     oidx, ow, _ = M.router_topk(lg, k)               # identical float32 logits
     np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
     np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-5, atol=1e-9)  # float32 expf
+
+
+@pytest.mark.parametrize("d", [256, 640, 1024, 4096])
+def test_router_tc_cluster_and_persistent_agree(cuda, d):
+    """The two tensor-core router kernels — K split over a thread-block
+    cluster (small batches) and the persistent multi-accumulator kernel
+    (large batches) — give bit-identical logits, ids and weights, so a
+    token's routing does not depend on its batch size."""
+    from paper_2508_07329_b200 import _lib
+    rng = np.random.default_rng(d)
+    x = torch.from_numpy(_acts(rng, 3000, d, scale=3.0)).to(cuda).bfloat16()
+    wg = torch.from_numpy((rng.normal(size=(8, d)) / np.sqrt(d)).astype(np.float32)).to(cuda)
+    gb = torch.from_numpy(rng.normal(size=8).astype(np.float32) * 0.1).to(cuda)
+    for T in (1, 100, 700, 3000):
+        outs = []
+        for tiles in (1 << 40, 0):
+            with _lib.tuned(_lib.TUNE_ROUTER_CLUSTER_TILES, tiles):
+                outs.append(ops.router_gate(x[:T], wg, 2, gate_bias=gb, tensor_cores=True))
+        for a, b in zip(*outs):
+            assert torch.equal(a, b), (d, T)
+    full = ops.router_gate(x, wg, 2, gate_bias=gb, tensor_cores=True)
+    one = ops.router_gate(x[:5], wg, 2, gate_bias=gb, tensor_cores=True)
+    for a, b in zip(full, one):
+        assert torch.equal(a[:5], b)
 
 
 def test_router_topk_ties(cuda):

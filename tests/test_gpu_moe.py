@@ -143,10 +143,11 @@ def small_layer(cuda):
 def test_moe_token_independence(cuda, small_layer):
     """Each token's output depends on that token alone, bit for bit — across
     batch sizes that take the single-CTA (M < 2048 rows) and the CTA-pair
-    GEMM paths, ragged expert groups and the host pipeline's chunking."""
+    GEMM paths, the CTA-per-row (<= 256 rows) and per-warp K1 kernels,
+    ragged expert groups and the host pipeline's chunking."""
     x = torch.from_numpy(_x(np.random.default_rng(4), 2500, 512)).to(cuda).bfloat16()
     full = small_layer.forward(x)
-    for n in (1, 7, 300, 1024):
+    for n in (1, 7, 128, 129, 300, 1024):
         assert torch.equal(small_layer.forward(x[:n].contiguous()), full[:n]), n
     part = small_layer.forward(x[1000:2100].contiguous())
     assert torch.equal(part, full[1000:2100])
