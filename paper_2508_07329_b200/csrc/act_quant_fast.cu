@@ -30,7 +30,6 @@ namespace moe {
 
 constexpr float kRelErr = 4.76837158203125e-07f;    // 2^-21
 constexpr float kAbsErr = 7.174648137343064e-43f;   // 2^-140
-constexpr int kWarpsPerCta = 16;
 constexpr int kBatch = 4;                           // 16-byte vectors in flight per lane
 
 __device__ __forceinline__ float err_bound(float v) { return fmaf(fabsf(v), kRelErr, kAbsErr); }
@@ -508,6 +507,99 @@ __device__ __forceinline__ uint2 fast_core(const float (&xs)[8], const FastRow& 
   return make_uint2(low_bytes4(t[0], t[1], t[2], t[3]), low_bytes4(t[4], t[5], t[6], t[7]));
 }
 
+// Load the lane's kBatch vectors of one batch (c = c0 + 32 b), zero past the row end.
+__device__ __forceinline__ void load_batch(const uint4* __restrict__ src, int c0, int nvec, uint4 (&u)[kBatch]) {
+#pragma unroll
+  for (int b = 0; b < kBatch; ++b) {
+    const int c = c0 + 32 * b;
+    u[b] = c < nvec ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// Pass A of one row (no producer records): float32 extremes and the first
+// column holding each. Branch-free per vector (value and vector index), the
+// element inside the winning vector is located once at the end.
+__device__ __forceinline__ RowExt row_extremes_f32(const uint4* __restrict__ src, const float* __restrict__ tab,
+                                                   int nvec, int lane) {
+  float tmax = -FLT_MAX, tmin = FLT_MAX;
+  int vM = 0, vm = 0;
+  for (int c0 = lane; c0 < nvec; c0 += 32 * kBatch) {
+    uint4 u[kBatch];
+    load_batch(src, c0, nvec, u);
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int c = c0 + 32 * b;
+      if (c >= nvec) break;
+      float xs[8];
+      smooth8(u[b], tab, c, xs);
+      const float vmax = max8(xs), vmin = min8(xs);
+      const bool um = vmax > tmax, un = vmin < tmin;
+      tmax = um ? vmax : tmax;
+      vM = um ? c : vM;
+      tmin = un ? vmin : tmin;
+      vm = un ? c : vm;
+    }
+  }
+  int64_t cM = vM, cm = vm;
+  warp_argmax(tmax, cM);
+  warp_argmin(tmin, cm);
+  auto locate = [&](int64_t vc, float val) -> int64_t {
+    float xs[8];
+    smooth8(__ldg(src + vc), tab, vc, xs);
+    int j = 0;
+#pragma unroll
+    for (int e = 7; e >= 0; --e) j = xs[e] == val ? e : j;
+    return vc * 8 + j;
+  };
+  return RowExt{tmax, tmin, locate(cM, tmax), locate(cm, tmin)};
+}
+
+// Fast encode of one row with known exact parameters (FastRow): branch-free
+// packed path per vector; vectors that need the slow path are remembered in
+// a per-lane mask and redone after each segment of 64 vector steps, so the
+// hot loop makes no calls. Returns the lane's code sum; *cnt accumulates the
+// possible-extreme counts of the slow vectors.
+template <bool GEN>
+__device__ __forceinline__ int encode_row_fast(const uint4* __restrict__ src, const float* __restrict__ tab,
+                                               const double* srow, const double* rrow, int nvec, int lane,
+                                               const FastRow& f, uint2* __restrict__ dst, uint32_t* cnt) {
+  int sum = 0;
+  constexpr int kSeg = 32 * 64;   // vectors per segment (64 per lane)
+  for (int s0 = 0; s0 < nvec; s0 += kSeg) {
+    const int s1 = min(nvec, s0 + kSeg);
+    uint64_t slow = 0;
+    for (int c0 = s0 + lane; c0 < s1; c0 += 32 * kBatch) {
+      uint4 u[kBatch];
+      load_batch(src, c0, s1, u);
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        const int c = c0 + 32 * b;
+        if (c >= s1) break;
+        float xs[8];
+        smooth8(u[b], tab, c, xs);
+        bool sl;
+        const uint2 out = fast_core<GEN>(xs, f, sl);
+        if (!sl) {
+          sum += bytesum(out);
+          __stcs(dst + c, out);
+        }
+        slow |= (uint64_t)sl << ((c - s0) >> 5);
+      }
+    }
+    while (slow) {   // rare
+      const int i = __ffsll((long long)slow) - 1;
+      slow &= slow - 1;
+      const int c = s0 + lane + 32 * i;
+      const uint4 sv = slow_vec8(__ldg(src + c), tab, c, srow, rrow, f);
+      *cnt += sv.z;
+      const uint2 o2 = make_uint2(sv.x, sv.y);
+      sum += bytesum(o2);
+      __stcs(dst + c, o2);
+    }
+  }
+  return sum;
+}
+
 template <bool GIVEN, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
@@ -515,7 +607,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                           int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t nvec = a.cols / 8;
+  const int nvec = (int)(a.cols / 8);
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
   const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
@@ -530,36 +622,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     uint2* dst = reinterpret_cast<uint2*>(out_row_ptr(a, codes, ldc, r));
 
     // (value, column) records of the float32 extremes: producer's, or pass A
-    RowExt rec;
-    if (GIVEN) {
-      const unsigned long long kmin = ext[2 * r], kmax = ext[2 * r + 1];
-      rec = given_record(row, tab, a.cols, kmax, kmin, lane);
-    } else {
-      float tmax = -FLT_MAX, tmin = FLT_MAX;
-      int64_t imax = 0, imin = 0;
-      for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
-        float xs[8];
-        smooth8(u, tab, c, xs);
-        const float vmax = max8(xs), vmin = min8(xs);
-        if (vmax > tmax) {
-          int j = 0;
-#pragma unroll
-          for (int e = 7; e >= 0; --e) j = xs[e] == vmax ? e : j;
-          tmax = vmax;
-          imax = c * 8 + j;
-        }
-        if (vmin < tmin) {
-          int j = 0;
-#pragma unroll
-          for (int e = 7; e >= 0; --e) j = xs[e] == vmin ? e : j;
-          tmin = vmin;
-          imin = c * 8 + j;
-        }
-      });
-      warp_argmax(tmax, imax);
-      warp_argmin(tmin, imin);
-      rec = RowExt{tmax, tmin, imax, imin};
-    }
+    const RowExt rec = GIVEN ? given_record(row, tab, a.cols, ext[2 * r + 1], ext[2 * r], lane)
+                             : row_extremes_f32(src, tab, nvec, lane);
     const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m)) || rec.cM >= a.cols || rec.cm >= a.cols;
 
     // speculative exact extremes: the recorded elements (verified below)
@@ -583,16 +647,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       const int mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
       if (mode) {
         uint32_t cnt = 0;
-        auto run = [&](auto gen) {
-          constexpr bool G = decltype(gen)::value;
-          for_row_batches(src, nvec, lane, [&](const uint4& u, int64_t c) {
-            const uint2 out = fast_vec8<G>(u, c, tab, srow, rrow, f, cnt);
-            sum += bytesum(out);
-            __stcs(dst + c, out);
-          });
-        };
-        if (mode == 1) run(std::false_type{});
-        else run(std::true_type{});
+        sum = mode == 1 ? encode_row_fast<false>(src, tab, srow, rrow, nvec, lane, f, dst, &cnt)
+                        : encode_row_fast<true>(src, tab, srow, rrow, nvec, lane, f, dst, &cnt);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -631,7 +687,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 constexpr int kChunkBytes = 2048;
 constexpr int kChunkVec = kChunkBytes / 16;   // 128 x 16 B: 4 vectors per lane
 constexpr int kRing = 6;
-constexpr int kBulkWarps = 16;
+constexpr int kBulkWarps = 16;       // (24 / 32 warps with smaller rings: register spills, 476 / 550 us)
 constexpr int kVecStep = 2;     // vectors per lane processed together (register budget: 16 warps)
 constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
 
