@@ -2,7 +2,7 @@
 T in {4096, 8192, 16384}, plus small serving/decode batches where the layer
 is expert-weight-stream (HBM) bound).
 
-    python tools/t_sweep.py  ->  prints JSON lines, writes profiles/tsweep_r01.json
+    python tools/t_sweep.py [out.json]  ->  prints JSON lines, writes profiles/tsweep_r01.json
 
 Per T: eager forward and CUDA-graph replay (CUDA events, mean of n steps
 after warm-up), per-stage split, int8 TOPS over the layer, and the HBM
@@ -68,8 +68,9 @@ def main():
         torch.cuda.empty_cache()
     out = {"gpu": torch.cuda.get_device_name(), "weights_bytes": wbytes, "hbm_peak_gbs": HBM,
            "int8_peak_tops": INT8, "rows": rows}
-    os.makedirs("profiles", exist_ok=True)
-    with open("profiles/tsweep_r01.json", "w") as f:
+    path = sys.argv[1] if len(sys.argv) > 1 else "profiles/tsweep_r01.json"
+    os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
+    with open(path, "w") as f:
         json.dump(out, f, indent=1)
 
 
