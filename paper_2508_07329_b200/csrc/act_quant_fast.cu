@@ -680,13 +680,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 // Same per-row algorithm as act_quant_warp_kernel, but rows are streamed
 // through a per-warp ring of kRing x 2 KB shared-memory stages filled by
 // cp.async.bulk (one elected lane issues, an mbarrier per stage completes
-// on the byte count): up to 12 KB in flight per warp regardless of register
-// pressure, so one 16-warp CTA per SM keeps ~190 KB of loads outstanding and
-// HBM saturated. Rows that fit the ring (x rows, d <= 6144) are held for the
-// second pass; longer rows without records are streamed twice.
+// on the byte count): 6 KB in flight per warp regardless of register
+// pressure, ~100 KB per 16-warp CTA. Rows that fit the ring (d <= 3072) are
+// held for the second pass; longer rows without records are streamed twice.
 constexpr int kChunkBytes = 2048;
 constexpr int kChunkVec = kChunkBytes / 16;   // 128 x 16 B: 4 vectors per lane
-constexpr int kRing = 6;
+// 3 stages (6 KB per warp, 98 KB per CTA): the rest of the SM's 256 KB stays
+// L1 and holds the expert's float32 reciprocal table (57 KB at ffn = 14336);
+// 6 stages left ~30 KB of L1 and the table loads went to L2 (368 vs 346 us)
+constexpr int kRing = 3;
 constexpr int kBulkWarps = 16;       // (24 / 32 warps with smaller rings: register spills, 476 / 550 us)
 constexpr int kVecStep = 2;     // vectors per lane processed together (register budget: 16 warps)
 constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
