@@ -80,8 +80,11 @@ moe_status moe_device_check(int dev);
  *   MOE_TUNE_ROUTER_CLUSTER_TILES: tensor-core router calls with at most
  *   this many 128-token tiles split K over a thread-block cluster; larger
  *   ones use the persistent multi-accumulator kernel (same logits;
- *   default 64 tiles). */
-enum { MOE_TUNE_K1_SMALL_ROWS = 1, MOE_TUNE_ROUTER_CLUSTER_TILES = 2 };
+ *   default 64 tiles).
+ *   MOE_TUNE_FUSED_QUANT: 1 (default) lets the MoE forward use
+ *   moe_w8a8_gemm_quant_a for its second GEMM, 0 the separate K1 + GEMM
+ *   (read by the host layer; same results). */
+enum { MOE_TUNE_K1_SMALL_ROWS = 1, MOE_TUNE_ROUTER_CLUSTER_TILES = 2, MOE_TUNE_FUSED_QUANT = 3 };
 moe_status moe_tune(int key, int64_t value, int64_t* old);
 
 /* ---- K1: smoothing + RTN affine quantization ----------------------------
@@ -291,6 +294,26 @@ moe_status moe_w8a8_gemm_scatter(const uint8_t* a, int64_t M, int64_t K, int64_t
                                  const float* bias, const float* row_weight, const int32_t* group_offsets,
                                  int num_groups, int epilogue, void* const* out_tab, const int32_t* out_rank,
                                  const int32_t* out_row, int out_dtype, int64_t ldo, moe_stream_t stream);
+/* GEMM2 with its A operand's K1 fused in (MoE second grouped GEMM; replaces
+ * moe_act_quant(row_ext=...) followed by moe_w8a8_gemm). x [M, K] bf16 (the
+ * SwiGLU output h, ld ldx) is quantized per row exactly as moe_act_quant
+ * with smoothing table rows row_group[m] and the producer records row_ext,
+ * by the GEMM's epilogue warps while they wait for accumulators; the TMA
+ * producer loads an A block once its rows are complete. Outputs: the codes
+ * a [M, lda], a_scale64 / a_scale / a_zp / a_rowsum (as moe_act_quant) and
+ * out (as moe_w8a8_gemm with the DEQUANT epilogue). Bit-identical to the
+ * two separate calls. workspace: moe_w8a8_gemm_quant_a_workspace(M) bytes
+ * (zeroed by the call). */
+int64_t moe_w8a8_gemm_quant_a_workspace(int64_t M);
+moe_status moe_w8a8_gemm_quant_a(const void* x, int64_t ldx, const double* smooth, const double* smooth_recip,
+                                 const float* smooth_recip_f32, const int32_t* row_group,
+                                 const unsigned long long* row_ext, uint8_t* a, int64_t lda, double* a_scale64,
+                                 float* a_scale, int32_t* a_zp, int32_t* a_rowsum, int64_t M, int64_t K,
+                                 const uint8_t* w, int64_t N, int64_t ldw, const float* w_scale, const int32_t* w_zp,
+                                 const int32_t* w_rowsum, const float* bias, const float* row_weight,
+                                 const int32_t* group_offsets, int num_groups, int epilogue, void* out,
+                                 int out_dtype, int64_t ldo, void* workspace, int64_t workspace_bytes,
+                                 moe_stream_t stream);
 moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
                          const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream);
 

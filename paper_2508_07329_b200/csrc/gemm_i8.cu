@@ -24,7 +24,7 @@
 // offsets, so routing never syncs with the host.
 #include <algorithm>
 
-#include "k1_common.cuh"
+#include "k1_fast.cuh"
 #include "ptx.cuh"
 
 #include <cudaTypedefs.h>
@@ -70,6 +70,18 @@ struct GemmArgs {
   const float* ns_rs32;
   int64_t ns_ld;
   unsigned long long* row_ext;  // [M, 2] (min, max) records
+  // fused K1 of the A operand (DEQUANT): the epilogue warps quantize A's
+  // rows (K1 with producer records) while they wait for accumulators; the
+  // TMA producer loads an A block once its 32-row blocks are complete
+  int fq;
+  RowArgs qa;                   // bf16 source rows of A, row -> smoothing group
+  const float* q_rs32;
+  const unsigned long long* q_ext;
+  uint8_t* q_codes;             // = A
+  int64_t q_ldc;
+  double* q_scale;
+  int* q_next;                  // next row to quantize
+  int* q_blk;                   // completed rows per 32-row block
 };
 
 template <int BN, int STAGES, int CG>
@@ -410,6 +422,35 @@ __device__ __forceinline__ void swiglu_fast(const GemmArgs& p, const TileInfo& t
   }
 }
 
+// ── fused K1 of the A operand ──────────────────────────────────────────────
+#ifndef MOE_FQ_BATCH
+#define MOE_FQ_BATCH 16     // 16-byte vectors in flight per lane (8 KB per warp)
+#endif
+// Relaxed poll / release increment: no L1 invalidation (an acquire at GPU
+// scope invalidates the SM's L1, which holds the K1 warps' reciprocal
+// tables). The polled rows are read only through L2 (TMA, ld.cg).
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// TMA producer: wait until A rows [r0, r1) are quantized (whole 32-row blocks)
+__device__ __forceinline__ void fq_wait_rows(const GemmArgs& p, int r0, int r1) {
+  r1 = min(r1, p.M);
+  for (int b = r0 >> 5; b * 32 < r1; ++b) {
+    const int need = min(32, p.M - b * 32);
+    while (ld_relaxed_s32(p.q_blk + b) < need) __nanosleep(64);
+  }
+  fence_proxy_async_global();
+}
+
 // Epilogue of one tile for one thread: TMEM lane quarter q, column half
 // `half` (8 epilogue warps split the 256 columns), output row `row`.
 template <int BN, int EPI, bool BF16>
@@ -420,10 +461,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
   float sa = 0.f, rw = 1.f;
   int32_t za = 0, rsa = 0;
   if (rvalid) {
-    za = p.a_zp[row];
-    rsa = p.a_rowsum[row];
+    // through L2 (ld.cg): with K1 fused, these rows were written by other SMs during this kernel
+    za = __ldcg(p.a_zp + row);
+    rsa = __ldcg(p.a_rowsum + row);
     if (EPI != MOE_EPI_ACC_I32) {
-      sa = p.a_scale[row];
+      sa = __ldcg(p.a_scale + row);
       if (p.row_weight) rw = p.row_weight[row];
     }
   }
@@ -541,7 +583,25 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
   }
 }
 
-template <int BN, int STAGES, int EPI, bool BF16, int CG>
+// Fused K1: drain one accumulator tile (its tfull phase already observed);
+// out of line so the K1 loop that calls it keeps its registers.
+template <int BN, bool BF16, int CG>
+static __device__ __noinline__ void fq_drain(const GemmArgs& p, const TileInfo& ti, uint32_t as, uint32_t tmem_base,
+                                             uint32_t rank, int q, int half, uint64_t* tempty,
+                                             const CUtensorMap* tmO, uint8_t* obuf, uint32_t& ob,
+                                             const uint8_t* pbuf) {
+  const int lane = threadIdx.x & 31;
+  tc_fence_after();
+  const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
+  const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+  ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
+  epilogue_tile<BN, MOE_EPI_DEQUANT, BF16>(p, ti, row, tbase, half, ext, tmO, obuf, ob, pbuf);
+  tc_fence_before();
+  if (CG == 2) mbar_arrive_leader(&tempty[as]);
+  else mbar_arrive(&tempty[as]);
+}
+
+template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, GemmArgs p) {
@@ -621,6 +681,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const int arow = ti.m0 + (int)rank * kBM;
       const int wrow = ti.g * p.N + ti.n0 + (int)rank * (BN / CG);
+      if constexpr (FQ) fq_wait_rows(p, arow, min(arow + kBM, ti.m_end));
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
@@ -678,7 +739,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t* obuf = smem + L::kOutOff + (warp - 4) * 2048;   // this warp's TMA-store staging (2 x 1 KB)
     uint32_t ob = 0;
     uint32_t tile_it = 0;
-    for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
+    constexpr bool fused = FQ && EPI == MOE_EPI_DEQUANT;
+    if constexpr (fused) {
+      // K1 of A fused in: quantize rows (claimed in order from a global
+      // counter), servicing ready accumulator tiles between 8 KB batches
+      int t = unit;
+      bool left = true;
+      auto tile_ready = [&]() {
+        int ok = 0;
+        if (lane == 0) ok = t < total_tiles && mbar_try_wait(smem_u32(&tfull[tile_it & 1]), (tile_it >> 1) & 1);
+        return __shfl_sync(0xffffffffu, ok, 0) != 0;
+      };
+      auto drain = [&]() {
+        const uint32_t as = tile_it & 1;
+        mbar_wait(&tfull[as], (tile_it >> 1) & 1);
+        const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
+        fq_drain<BN, BF16, CG>(p, ti, as, tmem_base, rank, q, half, tempty, &tmO, obuf, ob,
+                               smem + L::kParamOff + as * L::kParamBuf);
+        t += n_units;
+        ++tile_it;
+      };
+      auto poll = [&]() {
+        while (tile_ready()) drain();
+      };
+      while (t < total_tiles || left) {
+        poll();
+        if (left) {
+          int r = 0;
+          if (lane == 0) r = atomicAdd(p.q_next, 1);
+          r = __shfl_sync(0xffffffffu, r, 0);
+          if (r >= p.M) {
+            left = false;
+            continue;
+          }
+          k1_row_warp<true, MOE_FQ_BATCH>(p.qa, r, p.q_rs32, p.q_ext, 8, 0, p.q_codes, p.q_ldc, p.q_scale,
+                                          const_cast<float*>(p.a_scale), const_cast<int32_t*>(p.a_zp),
+                                          const_cast<int32_t*>(p.a_rowsum), lane, poll);
+          __syncwarp();
+          if (lane == 0) {
+            fence_proxy_async_global();   // the codes are read by TMA (async proxy)
+            red_release_add(p.q_blk + (r >> 5), 1);
+          }
+        } else if (t < total_tiles) {
+          drain();
+        }
+      }
+    }
+    for (int t = fused ? total_tiles : unit; t < total_tiles; t += n_units, ++tile_it) {
       const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
       uint8_t* pbuf = smem + L::kParamOff + (tile_it & 1) * L::kParamBuf;
@@ -802,10 +909,10 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, int EPI, bool BF16, int CG>
+template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false>
 static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const GemmArgs& p,
                             int grid, cudaStream_t s) {
-  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG>;
+  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG, FQ>;
   constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
   MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(kern), bytes));
   if (CG == 1) {
@@ -868,6 +975,9 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
   switch (epilogue) {
     case MOE_EPI_DEQUANT:
+      if (p.fq)   // K1 of A fused in (separate instantiation: the plain kernel keeps its registers)
+        return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG, true>(ta, tb, to, p, grid, s)
+                    : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG, true>(ta, tb, to, p, grid, s);
       return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG>(ta, tb, to, p, grid, s)
                   : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG>(ta, tb, to, p, grid, s);
     case MOE_EPI_SWIGLU:
@@ -889,7 +999,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
                              void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
                              const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
                              void* const* out_tab, const int32_t* out_rank, const int32_t* out_row,
-                             moe_stream_t stream) {
+                             moe_stream_t stream, const GemmArgs* fq = nullptr) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
   const bool w_corr = (epilogue & MOE_EPI_FLAG_WCORR) != 0;
   epilogue &= 0xFF;
@@ -938,6 +1048,17 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
   p.out_tab = out_tab;
   p.out_rank = out_rank;
   p.out_row = out_row;
+  if (fq) {
+    p.fq = 1;
+    p.qa = fq->qa;
+    p.q_rs32 = fq->q_rs32;
+    p.q_ext = fq->q_ext;
+    p.q_codes = fq->q_codes;
+    p.q_ldc = fq->q_ldc;
+    p.q_scale = fq->q_scale;
+    p.q_next = fq->q_next;
+    p.q_blk = fq->q_blk;
+  }
   const int esz = out_dtype == MOE_DT_BF16 ? 2 : 4;
   p.vec_ok = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((ldo * esz) % 16 == 0);
   p.acc_vec_ok = acc_out && ((reinterpret_cast<uintptr_t>(acc_out) & 15) == 0) && (ld_acc % 4 == 0) &&
@@ -955,6 +1076,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
   const bool tc_ok = (K % 16 == 0) && K >= kBK && (lda % 16 == 0) && (ldw % 16 == 0) &&
                      ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
   MOE_REQUIRE(tc_ok || !row_ext, "w8a8_gemm: row_ext needs the tensor-core path (K % 16 == 0, K >= 128)");
+  MOE_REQUIRE(tc_ok || !fq, "w8a8_gemm: fused A quantization needs the tensor-core path");
   if (tc_ok) {
     // CTA pairs once there are enough 256-row tiles to fill the machine
     const bool pair = M >= 256 * 8 && getenv("MOE_B200_NO_PAIR") == nullptr;
@@ -997,4 +1119,36 @@ extern "C" moe_status moe_w8a8_gemm_scatter(const uint8_t* a, int64_t M, int64_t
   return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, bias, row_weight,
                     group_offsets, num_groups, epilogue, const_cast<void*>(reinterpret_cast<const void*>(out_tab)),
                     out_dtype, ldo, nullptr, 0, nullptr, 0, nullptr, out_tab, out_rank, out_row, stream);
+}
+
+extern "C" int64_t moe_w8a8_gemm_quant_a_workspace(int64_t M) { return 4 * (1 + (M + 31) / 32); }
+
+extern "C" moe_status moe_w8a8_gemm_quant_a(
+    const void* x, int64_t ldx, const double* smooth, const double* smooth_recip, const float* smooth_recip_f32,
+    const int32_t* row_group, const unsigned long long* row_ext, uint8_t* a, int64_t lda, double* a_scale64,
+    float* a_scale, int32_t* a_zp, int32_t* a_rowsum, int64_t M, int64_t K, const uint8_t* w, int64_t N, int64_t ldw,
+    const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum, const float* bias, const float* row_weight,
+    const int32_t* group_offsets, int num_groups, int epilogue, void* out, int out_dtype, int64_t ldo,
+    void* workspace, int64_t workspace_bytes, moe_stream_t stream) {
+  MOE_REQUIRE(x && smooth && smooth_recip && smooth_recip_f32 && row_ext && a && a_scale64 && a_scale && a_zp &&
+                  a_rowsum,
+              "w8a8_gemm_quant_a: null operand");
+  MOE_REQUIRE((epilogue & 0xFF) == MOE_EPI_DEQUANT, "w8a8_gemm_quant_a: dequant epilogue only");
+  MOE_REQUIRE(M >= 1 && K % 8 == 0 && ldx % 8 == 0 && lda >= K && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(a) & 7) == 0 && lda % 8 == 0,
+              "w8a8_gemm_quant_a: bf16 rows with K % 8 == 0, 16-byte aligned");
+  MOE_REQUIRE(workspace && workspace_bytes >= moe_w8a8_gemm_quant_a_workspace(M), "w8a8_gemm_quant_a: workspace");
+  GemmArgs fq{};
+  fq.qa = RowArgs{x, MOE_DT_BF16, M, K, ldx, nullptr, row_group, SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, K}};
+  fq.q_rs32 = smooth_recip_f32;
+  fq.q_ext = row_ext;
+  fq.q_codes = a;
+  fq.q_ldc = lda;
+  fq.q_scale = a_scale64;
+  fq.q_next = static_cast<int*>(workspace);
+  fq.q_blk = fq.q_next + 1;
+  MOE_CUDA_TRY(cudaMemsetAsync(workspace, 0, (size_t)moe_w8a8_gemm_quant_a_workspace(M), as_stream(stream)));
+  return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, bias, row_weight,
+                    group_offsets, num_groups, epilogue, out, out_dtype, ldo, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                    nullptr, nullptr, stream, &fq);
 }

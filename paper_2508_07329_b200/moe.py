@@ -151,12 +151,22 @@ class MoELayer:
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,
                           next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_ext=ext)
         mark("gemm13_swiglu")
-        a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
-                           row_group=perm["row_expert"], row_ext=ext)
-        mark("quant_h")
-        y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
-                          group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)
-        mark("gemm2")
+        if fuse and self.F % 8 == 0 and L.tune(L.TUNE_FUSED_QUANT) > 0:
+            # K1 of h runs inside the second grouped GEMM (its epilogue warps
+            # quantize rows while the tensor cores work; bit-identical)
+            mark("quant_h")
+            y, a2 = ops.w8a8_gemm_quant_a(h, self.w2, smooth=self.s2, smooth_recip=self.s2_recip,
+                                          smooth_recip_f32=self.s2_recip32, row_group=perm["row_expert"],
+                                          row_ext=ext, group_offsets=perm["offsets"], num_groups=self.E,
+                                          n_per_group=self.d, out_dtype=y_dtype, row_weight=perm["row_weight"])
+            mark("gemm2")
+        else:
+            a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
+                               row_group=perm["row_expert"], row_ext=ext)
+            mark("quant_h")
+            y = ops.w8a8_gemm(a2, self.w2, epilogue=L.EPI_DEQUANT, out_dtype=y_dtype, row_weight=perm["row_weight"],
+                              group_offsets=perm["offsets"], num_groups=self.E, n_per_group=self.d)
+            mark("gemm2")
         out = ops.combine(y, perm["token_pos"], T, self.k, out_dtype=out_dtype, out=out)
         mark("combine")
         if return_aux:

@@ -153,6 +153,39 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
     return acc if epilogue == L.EPI_ACC_I32 else o
 
 
+def w8a8_gemm_quant_a(x: torch.Tensor, w: dict, *, smooth: torch.Tensor, smooth_recip: torch.Tensor,
+                      smooth_recip_f32: torch.Tensor, row_group: torch.Tensor, row_ext: torch.Tensor,
+                      group_offsets: torch.Tensor, num_groups: int, n_per_group: int, out_dtype=torch.bfloat16,
+                      row_weight: torch.Tensor | None = None, out: torch.Tensor | None = None) -> tuple:
+    """The MoE second grouped GEMM with K1 of its A operand fused in
+    (moe_w8a8_gemm_quant_a): x [M, K] bf16 rows with producer records ->
+    (out, a) where a is act_quant's dict for x. Same results as act_quant
+    followed by w8a8_gemm."""
+    x = _rowmajor(x, "x")
+    M, K = x.shape
+    dev = x.device
+    codes = torch.empty((M, K), dtype=torch.uint8, device=dev)
+    scale = torch.empty(M, dtype=torch.float64, device=dev)
+    scale_f32 = torch.empty(M, dtype=torch.float32, device=dev)
+    zp = torch.empty(M, dtype=torch.int32, device=dev)
+    rs = torch.empty(M, dtype=torch.int32, device=dev)
+    N = n_per_group
+    o = out if out is not None else torch.empty((M, N), dtype=out_dtype, device=dev)
+    wsb = L.load().moe_w8a8_gemm_quant_a_workspace(M)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    wc = w["codes"]
+    w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
+    L.call("moe_w8a8_gemm_quant_a", L.ptr(x), x.stride(0), L.ptr(smooth), L.ptr(smooth_recip),
+           L.ptr(smooth_recip_f32), L.ptr(row_group), L.ptr(row_ext), L.ptr(codes), codes.stride(0), L.ptr(scale),
+           L.ptr(scale_f32), L.ptr(zp), L.ptr(rs), M, K, L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")),
+           L.ptr(w["zp"]), L.ptr(w_rs), None, L.ptr(row_weight), L.ptr(group_offsets), num_groups,
+           L.EPI_DEQUANT | flags, L.ptr(o), L.DT_BF16 if o.dtype == torch.bfloat16 else L.DT_F32, o.stride(0),
+           L.ptr(ws), wsb, _s())
+    a = {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
+         "granularity": "per_token", "bits": 8}
+    return o, a
+
+
 def with_wcorr(w: dict) -> dict:
     """Add the pre-corrected weight sidecar rowsum - K * zp (int32, wrapping)
     used by the GEMM epilogue instead of rowsum (MOE_EPI_FLAG_WCORR)."""

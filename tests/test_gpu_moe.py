@@ -153,6 +153,23 @@ def test_moe_token_independence(cuda, small_layer):
     assert torch.equal(part, full[1000:2100])
 
 
+@pytest.mark.parametrize("T", [300, 1500, 2500])
+def test_moe_fused_quant_gemm2_matches(cuda, small_layer, T):
+    """K1 of h fused into the second grouped GEMM (its epilogue warps
+    quantize rows while the tensor cores run; single-CTA and CTA-pair tiles)
+    gives the same codes, row parameters and layer output as K1 + GEMM."""
+    from paper_2508_07329_b200 import _lib as L
+    x = torch.from_numpy(_x(np.random.default_rng(T), T, 512)).to(cuda).bfloat16()
+    outs = []
+    for fused in (0, 1):
+        with L.tuned(L.TUNE_FUSED_QUANT, fused):
+            outs.append(small_layer.forward(x, return_aux=True))
+    (ref, a0), (got, a1) = outs
+    for k in ("codes", "scale", "scale_f32", "zp", "rowsum"):
+        assert torch.equal(a1["a2"][k], a0["a2"][k]), k
+    assert torch.equal(got, ref)
+
+
 def test_moe_permutation_equivariance(cuda, small_layer):
     x = torch.from_numpy(_x(np.random.default_rng(5), 1500, 512)).to(cuda).bfloat16()
     perm = torch.from_numpy(np.random.default_rng(6).permutation(1500)).to(cuda)
