@@ -81,10 +81,17 @@ moe_status moe_device_check(int dev);
  *   this many 128-token tiles split K over a thread-block cluster; larger
  *   ones use the persistent multi-accumulator kernel (same logits;
  *   default 64 tiles).
- *   MOE_TUNE_FUSED_QUANT: 1 (default) lets the MoE forward use
- *   moe_w8a8_gemm_quant_a for its second GEMM, 0 the separate K1 + GEMM
- *   (read by the host layer; same results). */
-enum { MOE_TUNE_K1_SMALL_ROWS = 1, MOE_TUNE_ROUTER_CLUSTER_TILES = 2, MOE_TUNE_FUSED_QUANT = 3 };
+ *   MOE_TUNE_FUSED_QUANT: 1 lets the MoE forward use moe_w8a8_gemm_quant_a
+ *   for its second GEMM, 0 (default) the separate K1 + GEMM.
+ *   MOE_TUNE_FUSED_COMBINE: 1 (default) lets the top-2 MoE forward use
+ *   moe_w8a8_gemm_combine, 0 the separate GEMM + combine.
+ *   (Both read by the host layer; same results either way.) */
+enum {
+  MOE_TUNE_K1_SMALL_ROWS = 1,
+  MOE_TUNE_ROUTER_CLUSTER_TILES = 2,
+  MOE_TUNE_FUSED_QUANT = 3,
+  MOE_TUNE_FUSED_COMBINE = 4
+};
 moe_status moe_tune(int key, int64_t value, int64_t* old);
 
 /* ---- K1: smoothing + RTN affine quantization ----------------------------
@@ -314,6 +321,24 @@ moe_status moe_w8a8_gemm_quant_a(const void* x, int64_t ldx, const double* smoot
                                  const int32_t* group_offsets, int num_groups, int epilogue, void* out,
                                  int out_dtype, int64_t ldo, void* workspace, int64_t workspace_bytes,
                                  moe_stream_t stream);
+/* GEMM2 with the top-2 combine fused in (replaces moe_w8a8_gemm(DEQUANT,
+ * bf16) followed by moe_combine for k == 2). A rows are the M = 2T
+ * expert-sorted (token, slot) rows, src_token [M] their tokens, token_pos
+ * [T, 2] each token's two rows. Per 32-column chunk, the first of a token's
+ * two rows to finish stores its bf16 values in y [M, ldy] (scratch) and the
+ * second adds them to its own ((0 + mine) + partner in float, which is the
+ * combine kernel's sum: two-term addition commutes) and writes out [T, ldo]
+ * bf16. Bit-identical to the two separate calls; y is only partly written.
+ * workspace: moe_w8a8_gemm_combine_workspace(T, N) bytes (zeroed by the
+ * call). */
+int64_t moe_w8a8_gemm_combine_workspace(int64_t T, int64_t N);
+moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                                 const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                                 int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,
+                                 const float* row_weight, const int32_t* group_offsets, int num_groups,
+                                 int epilogue, void* y, int64_t ldy, const int32_t* src_token,
+                                 const int32_t* token_pos, int64_t T, void* out, int64_t ldo, void* workspace,
+                                 int64_t workspace_bytes, moe_stream_t stream);
 moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
                          const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream);
 

@@ -25,6 +25,7 @@ EPI_FLAG_WCORR = 0x100
 TUNE_K1_SMALL_ROWS = 1
 TUNE_ROUTER_CLUSTER_TILES = 2
 TUNE_FUSED_QUANT = 3
+TUNE_FUSED_COMBINE = 4
 ORDER_MAX_ABS, ORDER_SUM_SQUARES = 1, 2
 
 _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double
@@ -48,6 +49,9 @@ _SIGS = {
     "moe_w8a8_gemm_quant_a_workspace": (_I64, [_I64]),
     "moe_w8a8_gemm_quant_a": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I64, _P, _I64,
                                    _I64, _P, _P, _P, _P, _P, _P, _I, _I, _P, _I, _I64, _P, _I64, _P]),
+    "moe_w8a8_gemm_combine_workspace": (_I64, [_I64, _I64]),
+    "moe_w8a8_gemm_combine": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _I, _I,
+                                   _P, _I64, _P, _P, _I64, _P, _I64, _P, _I64, _P]),
     "moe_quant_sq_error": (_I, [_P, _I64, _I64, _P, _I, _P, _P, _P, _P, _I64, _P]),
     "moe_quant_sq_error_workspace": (_I64, [_I64, _I64]),
     "moe_router_gate": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),

@@ -82,6 +82,15 @@ struct GemmArgs {
   double* q_scale;
   int* q_next;                  // next row to quantize
   int* q_blk;                   // completed rows per 32-row block
+  // fused top-2 combine (DEQUANT, bf16): the second of a token's two rows
+  // to finish a 32-column chunk adds the first's stored values and writes
+  // the token's output row
+  const int32_t* comb_src;      // row -> token
+  const int32_t* comb_pos;      // [T, 2] token -> its two rows
+  int* comb_cnt;                // [T, N / 32] chunk arrival counters (zeroed)
+  int comb_chunks;
+  __nv_bfloat16* comb_out;      // [T, comb_ldo]
+  int64_t comb_ldo;
 };
 
 template <int BN, int STAGES, int CG>
@@ -451,9 +460,43 @@ __device__ __forceinline__ void fq_wait_rows(const GemmArgs& p, int r0, int r1) 
   fence_proxy_async_global();
 }
 
+// Fused combine of one 32-column chunk of row `row` (y already dequantized
+// and weighted, float): rounded to bf16 as the combine kernel would read it;
+// the first of the token's two rows to get here stores it (y scratch) and
+// publishes (+2); the second waits for that, adds ((0 + mine) + partner, the
+// combine kernel's float order up to commutation of two terms) and stores
+// the token's bf16 output.
+__device__ __forceinline__ void comb_store(const GemmArgs& p, int row, int n_lo, float (&y)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) y[j] = __bfloat162float(__float2bfloat16_rn(y[j]));
+  const int t = p.comb_src[row];
+  int* ctr = p.comb_cnt + (int64_t)t * p.comb_chunks + (n_lo >> 5);
+  if (atomicAdd(ctr, 1) == 0) {
+    store32<true>(p.out, (int64_t)row * p.ldo + n_lo, y, 32, true);
+    red_release_add(ctr, 2);
+  } else {
+    while (ld_relaxed_s32(ctr) < 4) __nanosleep(32);
+    const int r0 = p.comb_pos[2 * t], r1 = p.comb_pos[2 * t + 1];
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.out) +
+                                                      (int64_t)(r0 == row ? r1 : r0) * p.ldo + n_lo);
+    float o[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = __ldcg(src + q);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o[q * 8 + 2 * e] = (0.f + y[q * 8 + 2 * e]) + __uint_as_float(w[e] << 16);
+        o[q * 8 + 2 * e + 1] = (0.f + y[q * 8 + 2 * e + 1]) + __uint_as_float(w[e] & 0xFFFF0000u);
+      }
+    }
+    store32<true>(p.comb_out, (int64_t)t * p.comb_ldo + n_lo, o, 32, true);
+  }
+}
+
 // Epilogue of one tile for one thread: TMEM lane quarter q, column half
 // `half` (8 epilogue warps split the 256 columns), output row `row`.
-template <int BN, int EPI, bool BF16>
+template <int BN, int EPI, bool BF16, bool CB = false>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo& ti, int row, uint32_t tbase,
                                               int half, ExtRec& ext, const CUtensorMap* tmO, uint8_t* obuf,
                                               uint32_t& ob, const uint8_t* pbuf) {
@@ -575,9 +618,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& p, const TileInfo&
             y[j] = val * rw;
           }
         }
-        void* obase = p.out_tab ? p.out_tab[p.out_rank[row]] : p.out;
-        const int64_t orow = p.out_tab ? (int64_t)p.out_row[row] : (int64_t)row;
-        store32<BF16>(obase, orow * p.ldo + n_lo, y, nvalid, p.vec_ok);
+        if constexpr (CB) {
+          comb_store(p, row, n_lo, y);
+        } else {
+          void* obase = p.out_tab ? p.out_tab[p.out_rank[row]] : p.out;
+          const int64_t orow = p.out_tab ? (int64_t)p.out_row[row] : (int64_t)row;
+          store32<BF16>(obase, orow * p.ldo + n_lo, y, nvalid, p.vec_ok);
+        }
       }
     }
   }
@@ -601,7 +648,7 @@ static __device__ __noinline__ void fq_drain(const GemmArgs& p, const TileInfo& 
   else mbar_arrive(&tempty[as]);
 }
 
-template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false>
+template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false, bool CB = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, GemmArgs p) {
@@ -813,7 +860,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = ti.m0 + (int)rank * kBM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       ExtRec ext{-FLT_MAX, FLT_MAX, 0, 0};
-      epilogue_tile<BN, EPI, BF16>(p, ti, row, tbase, half, ext, &tmO, obuf, ob, pbuf);
+      epilogue_tile<BN, EPI, BF16, CB>(p, ti, row, tbase, half, ext, &tmO, obuf, ob, pbuf);
       tc_fence_before();
       if (CG == 2) mbar_arrive_leader(&tempty[as]);
       else mbar_arrive(&tempty[as]);
@@ -909,10 +956,10 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false>
+template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false, bool CB = false>
 static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const GemmArgs& p,
                             int grid, cudaStream_t s) {
-  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG, FQ>;
+  auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG, FQ, CB>;
   constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
   MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(kern), bytes));
   if (CG == 1) {
@@ -975,6 +1022,8 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
   switch (epilogue) {
     case MOE_EPI_DEQUANT:
+      if (p.comb_cnt)   // fused top-2 combine (bf16 only, checked by the entry point)
+        return launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG, false, true>(ta, tb, to, p, grid, s);
       if (p.fq)   // K1 of A fused in (separate instantiation: the plain kernel keeps its registers)
         return bf16 ? launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG, true>(ta, tb, to, p, grid, s)
                     : launch_tc<BN, ST, MOE_EPI_DEQUANT, false, CG, true>(ta, tb, to, p, grid, s);
@@ -999,7 +1048,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
                              void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
                              const float* next_smooth_recip_f32, int64_t next_ld, unsigned long long* row_ext,
                              void* const* out_tab, const int32_t* out_rank, const int32_t* out_row,
-                             moe_stream_t stream, const GemmArgs* fq = nullptr) {
+                             moe_stream_t stream, const GemmArgs* fq = nullptr, const GemmArgs* cb = nullptr) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
   const bool w_corr = (epilogue & MOE_EPI_FLAG_WCORR) != 0;
   epilogue &= 0xFF;
@@ -1048,6 +1097,14 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
   p.out_tab = out_tab;
   p.out_rank = out_rank;
   p.out_row = out_row;
+  if (cb) {
+    p.comb_src = cb->comb_src;
+    p.comb_pos = cb->comb_pos;
+    p.comb_cnt = cb->comb_cnt;
+    p.comb_chunks = cb->comb_chunks;
+    p.comb_out = cb->comb_out;
+    p.comb_ldo = cb->comb_ldo;
+  }
   if (fq) {
     p.fq = 1;
     p.qa = fq->qa;
@@ -1077,6 +1134,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
                      ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
   MOE_REQUIRE(tc_ok || !row_ext, "w8a8_gemm: row_ext needs the tensor-core path (K % 16 == 0, K >= 128)");
   MOE_REQUIRE(tc_ok || !fq, "w8a8_gemm: fused A quantization needs the tensor-core path");
+  MOE_REQUIRE(tc_ok || !cb, "w8a8_gemm: fused combine needs the tensor-core path");
   if (tc_ok) {
     // CTA pairs once there are enough 256-row tiles to fill the machine
     const bool pair = M >= 256 * 8 && getenv("MOE_B200_NO_PAIR") == nullptr;
@@ -1151,4 +1209,35 @@ extern "C" moe_status moe_w8a8_gemm_quant_a(
   return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, bias, row_weight,
                     group_offsets, num_groups, epilogue, out, out_dtype, ldo, nullptr, 0, nullptr, 0, nullptr, nullptr,
                     nullptr, nullptr, stream, &fq);
+}
+
+extern "C" int64_t moe_w8a8_gemm_combine_workspace(int64_t T, int64_t N) { return 4 * T * ((N + 31) / 32); }
+
+extern "C" moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
+                                            const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
+                                            int64_t ldw, const float* w_scale, const int32_t* w_zp,
+                                            const int32_t* w_rowsum, const float* row_weight,
+                                            const int32_t* group_offsets, int num_groups, int epilogue, void* y,
+                                            int64_t ldy, const int32_t* src_token, const int32_t* token_pos,
+                                            int64_t T, void* out, int64_t ldo, void* workspace,
+                                            int64_t workspace_bytes, moe_stream_t stream) {
+  MOE_REQUIRE(y && out && src_token && token_pos, "w8a8_gemm_combine: null pointer");
+  MOE_REQUIRE((epilogue & 0xFF) == MOE_EPI_DEQUANT, "w8a8_gemm_combine: dequant epilogue only");
+  MOE_REQUIRE(M == 2 * T, "w8a8_gemm_combine: top-2 routing (M == 2 T)");
+  MOE_REQUIRE(N % 32 == 0 && ldy % 8 == 0 && ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0,
+              "w8a8_gemm_combine: N % 32 == 0 and 16-byte aligned bf16 rows");
+  MOE_REQUIRE(workspace && workspace_bytes >= moe_w8a8_gemm_combine_workspace(T, N),
+              "w8a8_gemm_combine: workspace");
+  GemmArgs cb{};
+  cb.comb_src = src_token;
+  cb.comb_pos = token_pos;
+  cb.comb_cnt = static_cast<int*>(workspace);
+  cb.comb_chunks = (int)(N / 32);
+  cb.comb_out = static_cast<__nv_bfloat16*>(out);
+  cb.comb_ldo = ldo;
+  MOE_CUDA_TRY(cudaMemsetAsync(workspace, 0, (size_t)moe_w8a8_gemm_combine_workspace(T, N), as_stream(stream)));
+  return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, nullptr, row_weight,
+                    group_offsets, num_groups, epilogue, y, MOE_DT_BF16, ldy, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                    nullptr, nullptr, stream, nullptr, &cb);
 }

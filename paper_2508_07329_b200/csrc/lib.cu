@@ -17,6 +17,7 @@ int64_t k1_small_rows() { return g_k1_small_rows.load(std::memory_order_relaxed)
 static std::atomic<int64_t> g_router_cluster_tiles{64};   // tools/router_bench.py crossover
 int64_t router_cluster_tiles() { return g_router_cluster_tiles.load(std::memory_order_relaxed); }
 static std::atomic<int64_t> g_fused_quant{0};
+static std::atomic<int64_t> g_fused_combine{1};
 }  // namespace moe
 
 extern "C" moe_status moe_tune(int key, int64_t value, int64_t* old) {
@@ -34,6 +35,11 @@ extern "C" moe_status moe_tune(int key, int64_t value, int64_t* old) {
     }
     case MOE_TUNE_FUSED_QUANT: {
       const int64_t prev = value < 0 ? moe::g_fused_quant.load() : moe::g_fused_quant.exchange(value);
+      if (old) *old = prev;
+      return MOE_OK;
+    }
+    case MOE_TUNE_FUSED_COMBINE: {
+      const int64_t prev = value < 0 ? moe::g_fused_combine.load() : moe::g_fused_combine.exchange(value);
       if (old) *old = prev;
       return MOE_OK;
     }

@@ -186,6 +186,28 @@ def w8a8_gemm_quant_a(x: torch.Tensor, w: dict, *, smooth: torch.Tensor, smooth_
     return o, a
 
 
+def w8a8_gemm_combine(a: dict, w: dict, *, row_weight: torch.Tensor, group_offsets: torch.Tensor, num_groups: int,
+                      n_per_group: int, src_token: torch.Tensor, token_pos: torch.Tensor, T: int,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """The MoE second grouped GEMM with the top-2 combine fused in
+    (moe_w8a8_gemm_combine): returns out [T, N] bf16, equal to
+    combine(w8a8_gemm(a, w, bf16), token_pos, T, 2)."""
+    ac, wc = a["codes"], w["codes"]
+    M, K = ac.shape
+    N = n_per_group
+    dev = ac.device
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    o = out if out is not None else torch.empty((T, N), dtype=torch.bfloat16, device=dev)
+    wsb = L.load().moe_w8a8_gemm_combine_workspace(T, N)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
+    L.call("moe_w8a8_gemm_combine", L.ptr(ac), M, K, ac.stride(0), L.ptr(a["scale_f32"]), L.ptr(a["zp"]),
+           L.ptr(a["rowsum"]), L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w_rs),
+           L.ptr(row_weight), L.ptr(group_offsets), num_groups, L.EPI_DEQUANT | flags, L.ptr(y), y.stride(0),
+           L.ptr(src_token), L.ptr(token_pos), T, L.ptr(o), o.stride(0), L.ptr(ws), wsb, _s())
+    return o
+
+
 def with_wcorr(w: dict) -> dict:
     """Add the pre-corrected weight sidecar rowsum - K * zp (int32, wrapping)
     used by the GEMM epilogue instead of rowsum (MOE_EPI_FLAG_WCORR)."""

@@ -170,6 +170,20 @@ def test_moe_fused_quant_gemm2_matches(cuda, small_layer, T):
     assert torch.equal(got, ref)
 
 
+@pytest.mark.parametrize("T", [1, 100, 300, 1500, 2500])
+def test_moe_fused_combine_matches(cuda, small_layer, T):
+    """The top-2 combine fused into GEMM2's epilogue (first row of a token
+    parks its chunk, the second adds it) equals GEMM2 + combine bit for bit
+    (compared as raw bf16 bits, signed zeros included)."""
+    from paper_2508_07329_b200 import _lib as L
+    x = torch.from_numpy(_x(np.random.default_rng(T + 7), T, 512)).to(cuda).bfloat16()
+    outs = []
+    for fused in (0, 1):
+        with L.tuned(L.TUNE_FUSED_COMBINE, fused):
+            outs.append(small_layer.forward(x))
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+
+
 def test_moe_permutation_equivariance(cuda, small_layer):
     x = torch.from_numpy(_x(np.random.default_rng(5), 1500, 512)).to(cuda).bfloat16()
     perm = torch.from_numpy(np.random.default_rng(6).permutation(1500)).to(cuda)
