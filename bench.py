@@ -225,25 +225,40 @@ def main() -> None:
     ep_info = None
     model = layer
     if world > 1 or args.ep:
-        # expert parallelism: plan_two_stage over the GPU-measured routing of
-        # all ranks -> replicated residents, the rest bin-packed (ep.py)
-        from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertParallelMoE, PeerBuffers,
-                                              PeerExpertParallelMoE, plan_placement)
-        placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
-        backend = CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank))
-        if args.ep_transport == "peer":
-            # receive capacity: every rank could route all its tokens to one owner
-            bufs = (PeerBuffers.symmetric(D, world * T * TOPK, T * TOPK) if world > 1
-                    else PeerBuffers.loopback(1, D, T * TOPK, T * TOPK)[0])
-            model = PeerExpertParallelMoE(backend, placement, bufs)
-        else:
-            model = ExpertParallelMoE(backend, placement)
-        counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
-        ep_info = {"transport": args.ep_transport, "replicated": list(placement.replicated),
-                   "owner": list(placement.owner),
-                   "local_fraction_est": placement.local_fraction(counts)}
-        del layer.w13, layer.w2            # this rank keeps only its local experts' weights
-        torch.cuda.empty_cache()
+        try:
+            # expert parallelism: plan_two_stage over the GPU-measured routing of
+            # all ranks -> replicated residents, the rest bin-packed (ep.py)
+            from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertParallelMoE, PeerBuffers,
+                                                  PeerExpertParallelMoE, plan_placement)
+            placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
+            backend = CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank))
+            if args.ep_transport == "peer":
+                # receive capacity: every rank could route all its tokens to one owner
+                bufs = (PeerBuffers.symmetric(D, world * T * TOPK, T * TOPK) if world > 1
+                        else PeerBuffers.loopback(1, D, T * TOPK, T * TOPK)[0])
+                model = PeerExpertParallelMoE(backend, placement, bufs)
+            else:
+                model = ExpertParallelMoE(backend, placement)
+            counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
+            ep_info = {"transport": args.ep_transport, "replicated": list(placement.replicated),
+                       "owner": list(placement.owner),
+                       "local_fraction_est": placement.local_fraction(counts)}
+            del layer.w13, layer.w2            # this rank keeps only its local experts' weights
+            torch.cuda.empty_cache()
+            ep_error = None
+        except Exception as exc:
+            ep_error = repr(exc)[:300]
+            print(f"[bench] expert-parallel setup failed on rank {rank}: {ep_error}", file=sys.stderr)
+        ok = torch.tensor([0 if ep_error else 1], device="cuda")
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank takes the same branch
+        if int(ok.item()):
+            model.forward(x_dev)                            # one EP forward before the timing
+            torch.cuda.synchronize()
+        else:                                               # labelled fallback: independent replicas
+            model = layer if hasattr(layer, "w13") else MoELayer.random(E, D, F, top_k=TOPK, seed=1)
+            ep_info = {"fallback": "replicas (no exchange)", "error": ep_error or "failed on another rank"}
+            torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -380,7 +395,8 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
-                       "top_k": TOPK, "d": D, "ffn": F, "parallelism": f"ep{world}" if ep_info is not None else "1gpu",
+                       "top_k": TOPK, "d": D, "ffn": F, "parallelism": (f"replicas{world}" if ep_info and "fallback" in ep_info else
+                                       f"ep{world}" if ep_info is not None else "1gpu"),
                        "l2": "inputs larger than L2 (x 134 MB, expert weights 1.41 GB per layer)"},
             "int8_tops_layer": value / world * OPS_PER_TOKEN / 1e12,
             "stages_ms": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
