@@ -130,6 +130,9 @@ class MoELayer:
         y_dtype = y_dtype or (torch.float32 if out_dtype == torch.float32 else torch.bfloat16)
         mark = timer.mark if timer is not None else (lambda _n: None)
         T = x.shape[0]
+        if T == 0:
+            empty = out if out is not None else torch.empty((0, self.d), dtype=out_dtype, device=x.device)
+            return (empty, {}) if return_aux else empty
         mark("start")
         logits, idx, w = self.route(x, want_logits=return_aux)
         mark("router")

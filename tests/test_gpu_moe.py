@@ -184,6 +184,24 @@ def test_moe_fused_combine_matches(cuda, small_layer, T):
     assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
 
 
+def test_moe_edge_batches(cuda, small_layer):
+    """Empty batch, one token, a batch whose tokens all pick the same two
+    experts (six experts idle), and k = 1 / E = 1 layers."""
+    x0 = torch.empty((0, 512), dtype=torch.bfloat16, device=cuda)
+    assert small_layer.forward(x0).shape == (0, 512)
+    x = torch.from_numpy(_x(np.random.default_rng(31), 64, 512)).to(cuda).bfloat16()
+    one = small_layer.forward(x[:1].contiguous())
+    assert torch.equal(one, small_layer.forward(x)[:1])
+    same = x[:1].repeat(300, 1).contiguous()          # identical tokens -> identical routing
+    ys = small_layer.forward(same)
+    assert torch.equal(ys, one.repeat(300, 1))
+    for E, k in ((4, 1), (1, 1)):
+        lay = MoELayer.random(E, 256, 512, top_k=k, seed=E)
+        xx = x[:, :256].contiguous()
+        full = lay.forward(xx)
+        assert torch.equal(lay.forward(xx[:10].contiguous()), full[:10])
+
+
 def test_moe_permutation_equivariance(cuda, small_layer):
     x = torch.from_numpy(_x(np.random.default_rng(5), 1500, 512)).to(cuda).bfloat16()
     perm = torch.from_numpy(np.random.default_rng(6).permutation(1500)).to(cuda)
