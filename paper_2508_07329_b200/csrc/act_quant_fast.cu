@@ -145,16 +145,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         for (int b = 0; b < 4; ++b) {
           const bool ok = full || cb + 32 * b < nvec;
           u[b] = ok ? v[lane + 32 * b] : make_uint4(0u, 0u, 0u, 0u);
-          if (tab && ok) {
-            ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b));
-            tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * b) + 1);
-          }
+          const int64_t ct = ok ? cb + 32 * b : 0;
+          ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * ct);
+          tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * ct + 1);
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           if (!(full || cb + 32 * b < nvec)) continue;
           float xs[8];
-          smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
+          smooth8_pre(u[b], ta[b], tb[b], xs);
           const float vmax = max8(xs), vmin = min8(xs);
           const bool um = vmax > tmax, un = vmin < tmin;
           tmax = um ? vmax : tmax;
@@ -220,17 +219,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
 #pragma unroll
             for (int b = 0; b < kVecStep; ++b) {
               u[b] = v[lane + 32 * (hf + b)];
-              if (tab) {
-                ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)));
-                tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)) + 1);
-              }
+              ta[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)));
+              tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * (cb + 32 * (hf + b)) + 1);
             }
             uint2 out[kVecStep];
             uint32_t slowm = 0;
 #pragma unroll
             for (int b = 0; b < kVecStep; ++b) {
               float xs[8];
-              smooth8_pre(u[b], tab != nullptr, ta[b], tb[b], xs);
+              smooth8_pre(u[b], ta[b], tb[b], xs);
               bool sl;
               out[b] = fast_core<G>(xs, f, sl);
               slowm |= (uint32_t)sl << b;
@@ -514,11 +511,13 @@ static cudaError_t launch_bulk(const RowArgs& a, const float* rs32, const unsign
   return cudaGetLastError();
 }
 
+// The fast kernels need bf16 rows and the smoothing tables (float64 s and
+// RN(1/s), float32 RN32(1/s)); unsmoothed rows take the exact kernel (the
+// host layer passes a table of ones to keep them on the fast path).
 static bool eligible(const RowArgs& a, const float* rs32, uint8_t* codes, int64_t ldc) {
-  const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
   return a.dt == MOE_DT_BF16 && a.cols % 8 == 0 && a.ldx % 8 == 0 && ldc % 8 == 0 &&
          (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (reinterpret_cast<uintptr_t>(codes) & 7) == 0 &&
-         (a.sm.mode == MOE_SMOOTH_NONE || (smooth && a.sm.rs && rs32));
+         a.sm.mode == MOE_SMOOTH_DIVIDE && a.sm.s && a.sm.rs && rs32;
 }
 
 template <bool GIVEN, int WARPS, int MINB>

@@ -28,18 +28,19 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   }
 }
 
-// xs = x * RN32(1/s) for 8 consecutive elements (table through L1)
+// xs = x * RN32(1/s) for 8 consecutive elements (table through L1). The fast
+// kernels always have a table (K1 without smoothing takes the exact kernel,
+// or the host passes a table of ones), so the multiply is unconditional: a
+// conditional one made the compiler merge both versions with moves.
 __device__ __forceinline__ void smooth8(const uint4& u, const float* __restrict__ tab, int64_t c, float (&xs)[8]) {
   unpack8(u, xs);
-  if (tab) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c);
-    const float4 b = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c + 1);
-    float2 p;
-    p = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(a.x, a.y)); xs[0] = p.x; xs[1] = p.y;
-    p = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(a.z, a.w)); xs[2] = p.x; xs[3] = p.y;
-    p = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(b.x, b.y)); xs[4] = p.x; xs[5] = p.y;
-    p = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(b.z, b.w)); xs[6] = p.x; xs[7] = p.y;
-  }
+  const float4 a = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c);
+  const float4 b = __ldg(reinterpret_cast<const float4*>(tab) + 2 * c + 1);
+  float2 p;
+  p = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(a.x, a.y)); xs[0] = p.x; xs[1] = p.y;
+  p = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(a.z, a.w)); xs[2] = p.x; xs[3] = p.y;
+  p = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(b.x, b.y)); xs[4] = p.x; xs[5] = p.y;
+  p = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(b.z, b.w)); xs[6] = p.x; xs[7] = p.y;
 }
 
 // ── packed 8-bit encode (sm_100 FFMA2/FADD2 + I2IP saturating pack) ───────
@@ -471,16 +472,13 @@ __device__ __forceinline__ uint2 fast_vec8(const uint4& u, int64_t c, const floa
 }
 
 // xs = x * table for 8 elements, table slice preloaded (ta: elements 0-3, tb: 4-7)
-__device__ __forceinline__ void smooth8_pre(const uint4& u, bool has_tab, const float4& ta, const float4& tb,
-                                            float (&xs)[8]) {
+__device__ __forceinline__ void smooth8_pre(const uint4& u, const float4& ta, const float4& tb, float (&xs)[8]) {
   unpack8(u, xs);
-  if (has_tab) {
-    float2 q;
-    q = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(ta.x, ta.y)); xs[0] = q.x; xs[1] = q.y;
-    q = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(ta.z, ta.w)); xs[2] = q.x; xs[3] = q.y;
-    q = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(tb.x, tb.y)); xs[4] = q.x; xs[5] = q.y;
-    q = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(tb.z, tb.w)); xs[6] = q.x; xs[7] = q.y;
-  }
+  float2 q;
+  q = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(ta.x, ta.y)); xs[0] = q.x; xs[1] = q.y;
+  q = __fmul2_rn(make_float2(xs[2], xs[3]), make_float2(ta.z, ta.w)); xs[2] = q.x; xs[3] = q.y;
+  q = __fmul2_rn(make_float2(xs[4], xs[5]), make_float2(tb.x, tb.y)); xs[4] = q.x; xs[5] = q.y;
+  q = __fmul2_rn(make_float2(xs[6], xs[7]), make_float2(tb.z, tb.w)); xs[6] = q.x; xs[7] = q.y;
 }
 
 // branch-free fast encode of 8 smoothed values; slow = the vector must take slow_vec8

@@ -50,6 +50,17 @@ def reciprocal(s: torch.Tensor, with_f32: bool = False):
     return (out, out32) if with_f32 else out
 
 
+_ONES: dict = {}
+
+
+def _ones_table(cols: int, dev) -> tuple:
+    key = (cols, str(dev))
+    if key not in _ONES:
+        one = torch.ones((1, cols), dtype=torch.float64, device=dev)
+        _ONES[key] = (one, one.clone(), torch.ones((1, cols), dtype=torch.float32, device=dev))
+    return _ONES[key]
+
+
 def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_recip: torch.Tensor | None = None,
               smooth_recip_f32: torch.Tensor | None = None,
               smooth_mode: int = L.SMOOTH_DIVIDE, row_group: torch.Tensor | None = None,
@@ -71,6 +82,12 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
     lib = L.load()
     wsb = lib.moe_act_quant_workspace(n_rows, cols, gran)
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev) if wsb else None
+    if smooth is None and x.dtype == torch.bfloat16 and gran == L.GRAN["per_token"]:
+        # unsmoothed bf16 rows: a table of ones keeps them on the fast K1
+        # kernels (x / 1 is exact in both the float32 filter and float64)
+        smooth, smooth_recip, smooth_recip_f32 = _ones_table(cols, dev)
+        smooth_mode = L.SMOOTH_DIVIDE
+        row_group = None
     mode = L.SMOOTH_NONE if smooth is None else smooth_mode
     if smooth is not None:
         smooth = smooth.contiguous()
