@@ -339,6 +339,13 @@ moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t
                                  int epilogue, void* y, int64_t ldy, const int32_t* src_token,
                                  const int32_t* token_pos, int64_t T, void* out, int64_t ldo, void* workspace,
                                  int64_t workspace_bytes, moe_stream_t stream);
+/* MoE stack block glue (SURVEY.md C5 token path, pre-norm residual blocks):
+ * s = bf16(x + y) (y == NULL: s = x), written to x_out when y is given, and
+ * norm_out = bf16(s * rsqrt(mean(s^2) + eps)) (float32, fixed reduction
+ * order per row; norm_out may be NULL). bf16 rows [T, d], d % 8 == 0,
+ * d <= 8192, contiguous. */
+moe_status moe_rmsnorm_residual(const void* x, const void* y, void* x_out, void* norm_out, int64_t T, int64_t d,
+                                float eps, moe_stream_t stream);
 moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
                          const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream);
 

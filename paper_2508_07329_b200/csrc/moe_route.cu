@@ -432,6 +432,61 @@ __global__ void combine_bf16_vec_kernel(const __nv_bfloat16* y, const int32_t* t
   }
 }
 
+// Residual + RMSNorm of the MoE stack (pre-norm blocks, SURVEY.md C5 token
+// path): s = bf16(x + y) (y optional), norm = bf16(s * rsqrt(mean(s^2) + eps))
+// in float32, one CTA per token row, each thread 8-element vectors. The sum of
+// squares is reduced in a fixed order, so the norm of a row depends on that
+// row alone.
+__global__ void __launch_bounds__(256) rmsnorm_residual_kernel(const __nv_bfloat16* x, const __nv_bfloat16* y,
+                                                               __nv_bfloat16* x_out, __nv_bfloat16* n_out,
+                                                               int64_t d, float eps) {
+  __shared__ float red[8];
+  const int64_t t = blockIdx.x;
+  const int nv = (int)(d / 8);
+  constexpr int kMaxV = 4;   // d <= 256 * 8 * 4 = 8192
+  float v[kMaxV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxV; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c >= nv) break;
+    const uint4 ux = reinterpret_cast<const uint4*>(x + t * d)[c];
+    const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&ux);
+    uint4 uy = make_uint4(0u, 0u, 0u, 0u);
+    if (y) uy = reinterpret_cast<const uint4*>(y + t * d)[c];
+    const __nv_bfloat16* hy = reinterpret_cast<const __nv_bfloat16*>(&uy);
+    uint4 os;
+    __nv_bfloat16* ho = reinterpret_cast<__nv_bfloat16*>(&os);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float sv = y ? __bfloat162float(__float2bfloat16_rn(__bfloat162float(hx[e]) + __bfloat162float(hy[e])))
+                         : __bfloat162float(hx[e]);
+      ho[e] = __float2bfloat16_rn(sv);
+      v[i][e] = sv;
+      ss = fmaf(sv, sv, ss);
+    }
+    if (y && x_out) reinterpret_cast<uint4*>(x_out + t * d)[c] = os;
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float r = rsqrtf(tot / (float)d + eps);
+  if (!n_out) return;
+#pragma unroll
+  for (int i = 0; i < kMaxV; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c >= nv) break;
+    uint4 on;
+    __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) hn[e] = __floats2bfloat162_rn(v[i][2 * e] * r, v[i][2 * e + 1] * r);
+    reinterpret_cast<uint4*>(n_out + t * d)[c] = on;
+  }
+}
+
 __global__ void histogram_kernel(const int32_t* idx, int64_t T, int k, int E, int layer, int64_t* counts,
                                  int32_t* path_codes) {
   __shared__ unsigned long long cnt[kMaxE];
@@ -566,6 +621,21 @@ extern "C" moe_status moe_expert_histogram(const int32_t* topk_idx, int64_t T, i
   int64_t blocks = (T + 255) / 256;
   if (blocks > num_sms() * 4) blocks = num_sms() * 4;
   histogram_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(topk_idx, T, k, E, layer, counts, path_codes); ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_rmsnorm_residual(const void* x, const void* y, void* x_out, void* norm_out, int64_t T,
+                                           int64_t d, float eps, moe_stream_t stream) {
+  MOE_REQUIRE(x && T >= 1 && d >= 8 && d % 8 == 0 && d <= 8192, "rmsnorm_residual: bf16 rows, d % 8 == 0, d <= 8192");
+  MOE_REQUIRE(norm_out || (y && x_out), "rmsnorm_residual: nothing to write");
+  MOE_REQUIRE(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(x_out) |
+                reinterpret_cast<uintptr_t>(norm_out)) & 15) == 0,
+              "rmsnorm_residual: 16-byte aligned rows");
+  rmsnorm_residual_kernel<<<(unsigned)T, 256, 0, as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(x_out),
+      static_cast<__nv_bfloat16*>(norm_out), d, eps);
+  ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }

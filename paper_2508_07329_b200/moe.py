@@ -413,14 +413,23 @@ class MoEStack:
     @staticmethod
     def norm(x: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
         """RMSNorm without a learned gain (random-weight stacks): keeps the
-        residual stream's scale bounded across layers."""
-        xf = x.float()
-        return (xf * torch.rsqrt(xf.pow(2).mean(dim=-1, keepdim=True) + eps)).to(x.dtype)
+        residual stream's scale bounded across layers (moe_rmsnorm_residual)."""
+        return ops.rmsnorm_residual(x, None, eps)[1]
+
+    @staticmethod
+    def residual(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        """bf16(x + y), the block's residual add (same kernel)."""
+        return ops.rmsnorm_residual(x, y, want_norm=False)[0]
 
     def forward(self, x: torch.Tensor, stats=None) -> torch.Tensor:
+        # one fused pass per block boundary: residual add + next block's norm
+        n = self.norm(x)
         for l, layer in enumerate(self.layers):
-            y = layer.forward(self.norm(x), stats=_LayerStats(stats, l) if stats is not None else None)
-            x = (x.float() + y.float()).to(x.dtype)
+            y = layer.forward(n, stats=_LayerStats(stats, l) if stats is not None else None)
+            if l + 1 < len(self.layers):
+                x, n = ops.rmsnorm_residual(x, y)
+            else:
+                x = self.residual(x, y)
         return x
 
     __call__ = forward

@@ -225,6 +225,20 @@ def w8a8_gemm_combine(a: dict, w: dict, *, row_weight: torch.Tensor, group_offse
     return o
 
 
+def rmsnorm_residual(x: torch.Tensor, y: torch.Tensor | None = None, eps: float = 1e-5,
+                     want_sum: bool = True, want_norm: bool = True) -> tuple:
+    """(s, norm): s = bf16(x + y) (x when y is None), norm = RMSNorm(s) without
+    gain, one fused pass (moe_rmsnorm_residual). bf16 [T, d] rows."""
+    x = x.contiguous()
+    T, d = x.shape
+    s_out = torch.empty_like(x) if (y is not None and want_sum) else None
+    n_out = torch.empty_like(x) if want_norm else None
+    if T:
+        L.call("moe_rmsnorm_residual", L.ptr(x), L.ptr(y.contiguous()) if y is not None else None, L.ptr(s_out),
+               L.ptr(n_out), T, d, eps, _s())
+    return (s_out if y is not None else x), n_out
+
+
 def with_wcorr(w: dict) -> dict:
     """Add the pre-corrected weight sidecar rowsum - K * zp (int32, wrapping)
     used by the GEMM epilogue instead of rowsum (MOE_EPI_FLAG_WCORR)."""

@@ -363,6 +363,25 @@ def test_router_tc_cluster_and_persistent_agree(cuda, d):
         assert torch.equal(a[:5], b)
 
 
+@pytest.mark.parametrize("T,d", [(37, 4096), (5, 1024), (300, 256)])
+def test_rmsnorm_residual(cuda, T, d):
+    """Stack glue kernel: residual add exactly as bf16(float(x) + float(y)),
+    RMSNorm within one bf16 ulp of a float32 torch reference, rows
+    independent of the batch."""
+    rng = np.random.default_rng(T + d)
+    x = torch.from_numpy(rng.normal(size=(T, d)).astype(np.float32) * 3).to(cuda).bfloat16()
+    y = torch.from_numpy(rng.normal(size=(T, d)).astype(np.float32)).to(cuda).bfloat16()
+    s, n = ops.rmsnorm_residual(x, y)
+    assert torch.equal(s, (x.float() + y.float()).to(torch.bfloat16))
+    sf = s.float()
+    ref = sf * torch.rsqrt(sf.pow(2).mean(dim=-1, keepdim=True) + 1e-5)
+    torch.testing.assert_close(n.float(), ref, rtol=2 ** -7, atol=1e-6)
+    _, n2 = ops.rmsnorm_residual(s, None)
+    assert torch.equal(n2, n)                       # fused norm == norm of the sum
+    _, n3 = ops.rmsnorm_residual(s[: T // 2 + 1].contiguous(), None)
+    assert torch.equal(n3, n[: T // 2 + 1])
+
+
 def test_router_topk_ties(cuda):
     lg = np.array([[1, 1, 1, 1], [0, 2, 2, 0], [3, 3, 1, 3], [-1, -1, -1, -2]], dtype=np.float32)
     idx, w = ops.router_topk(torch.from_numpy(lg).to(cuda), 2)
