@@ -130,3 +130,35 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert lib.moe_abi_version() == 1
     assert lib.moe_act_quant_workspace(4, 4, 0) == 16
+
+
+def test_abi_argument_errors_without_gpu():
+    """The C ABI's error contract (status code + thread-local message) for
+    invalid arguments: checked before any device work, so it runs here."""
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("library not built (run __graft_entry__.build())")
+    lib = _lib.load_library()
+    P = None
+    # act_quant: empty matrix, unsupported bits
+    D = 16   # dummy (never dereferenced) device addresses: validation runs before any launch
+    st = lib.moe_act_quant(D, _lib.DT_BF16, 0, 8, 8, P, P, P, P, _lib.SMOOTH_NONE, P, 8, 0, 1, D, 8, D, D, D, D, P,
+                           P, 0, P)
+    assert st == _lib.EINVAL and b"non-empty" in lib.moe_last_error()
+    st = lib.moe_act_quant(P, _lib.DT_BF16, 4, 8, 8, P, P, P, P, _lib.SMOOTH_NONE, P, 8, 0, 1, D, 8, D, D, D, D, P,
+                           P, 0, P)
+    assert st == _lib.EINVAL and b"null" in lib.moe_last_error()
+    # GEMM: K beyond the exact-int32 bound
+    st = lib.moe_w8a8_gemm(1, 4, 40000, 40000, 1, 1, 1, 1, 4, 40000, 1, 1, 1, P, P, P, 1, _lib.EPI_DEQUANT, 1,
+                           _lib.DT_F32, 4, P, 0, P, 0, P, P)
+    assert st == _lib.EINVAL and b"K too large" in lib.moe_last_error()
+    # fused combine needs top-2 rows (M == 2 T)
+    st = lib.moe_w8a8_gemm_combine(1, 6, 128, 128, 1, 1, 1, 1, 64, 128, 1, 1, 1, P, P, 1, _lib.EPI_DEQUANT, 16, 64,
+                                   1, 1, 4, 16, 64, 16, 1 << 20, P)
+    assert st == _lib.EINVAL and b"top-2" in lib.moe_last_error()
+    # tuning knobs: query, set/restore, unknown key
+    import ctypes
+    old = ctypes.c_int64(0)
+    assert lib.moe_tune(_lib.TUNE_K1_SMALL_ROWS, -1, ctypes.byref(old)) == _lib.OK and old.value >= 0
+    assert lib.moe_tune(99, 1, P) == _lib.EINVAL and b"unknown key" in lib.moe_last_error()
+    # rmsnorm: d must be a multiple of 8
+    assert lib.moe_rmsnorm_residual(16, P, P, 16, 4, 12, 1e-5, P) == _lib.EINVAL
