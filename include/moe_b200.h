@@ -60,6 +60,10 @@ enum { MOE_EPI_DEQUANT = 0, MOE_EPI_SWIGLU = 1, MOE_EPI_ACC_I32 = 2 };
  * rowsum_w - K * w_zp (precomputed once per weight matrix) instead of the
  * plain code row sums; saves one integer multiply per accumulator. */
 enum { MOE_EPI_FLAG_WCORR = 0x100 };
+/* OR-ed into moe_w8a8_gemm_combine's `epilogue`: the caller zeroed the
+ * workspace already (earlier in the stream), so the call adds no memset
+ * between the previous kernel and the GEMM (keeps the PDL overlap). */
+enum { MOE_EPI_FLAG_WS_ZEROED = 0x200 };
 /* channel ordering strategies (quant.py:42-45) */
 enum { MOE_ORDER_MAX_ABS = 1, MOE_ORDER_SUM_SQUARES = 2 };
 
@@ -330,7 +334,7 @@ moe_status moe_w8a8_gemm_quant_a(const void* x, int64_t ldx, const double* smoot
  * combine kernel's sum: two-term addition commutes) and writes out [T, ldo]
  * bf16. Bit-identical to the two separate calls; y is only partly written.
  * workspace: moe_w8a8_gemm_combine_workspace(T, N) bytes (zeroed by the
- * call). */
+ * call unless MOE_EPI_FLAG_WS_ZEROED). */
 int64_t moe_w8a8_gemm_combine_workspace(int64_t T, int64_t N);
 moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
                                  const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,

@@ -22,6 +22,7 @@ GRAN = {"per_tensor": 0, "per_token": 1, "per_output_row": 2}
 SMOOTH_NONE, SMOOTH_DIVIDE, SMOOTH_MULTIPLY = 0, 1, 2
 EPI_DEQUANT, EPI_SWIGLU, EPI_ACC_I32 = 0, 1, 2
 EPI_FLAG_WCORR = 0x100
+EPI_FLAG_WS_ZEROED = 0x200
 TUNE_K1_SMALL_ROWS = 1
 TUNE_ROUTER_CLUSTER_TILES = 2
 TUNE_FUSED_QUANT = 3

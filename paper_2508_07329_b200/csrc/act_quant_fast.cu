@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     act_quant_warp_kernel(RowArgs a, const float* __restrict__ rs32_tab, const unsigned long long* __restrict__ ext,
                           int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                           int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
+  griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
                           int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                           int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint8_t* ring = smem_raw + warp * kRing * kChunkBytes;
@@ -340,6 +342,8 @@ __global__ void __launch_bounds__(kCtaThreads)
   __shared__ double shd[kCtaThreads / 32];
   __shared__ int64_t shi[kCtaThreads / 32];
   __shared__ CtaRowState st;
+  griddep_wait();                // PDL-launched: the previous kernel's outputs are visible from here
+  griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r = blockIdx.x;
   const int64_t nvec = a.cols / 8;
@@ -549,8 +553,9 @@ static cudaError_t launch_warp(const RowArgs& a, const float* rs32, const unsign
     return env ? atoi(env) : -1;
   }();
   if (a.rows <= k1_small_rows() && a.cols <= (int64_t)kCtaNV * kCtaThreads * 8) {
-    act_quant_cta_kernel<GIVEN><<<(unsigned)a.rows, kCtaThreads, 0, s>>>(a, rs32, ext, bits, sym, codes, ldc, scale,
-                                                                          scale_f32, zp, rowsum);
+    const cudaError_t e = launch_pdl(act_quant_cta_kernel<GIVEN>, dim3((unsigned)a.rows), dim3(kCtaThreads), 0, s, a,
+                                     rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum);
+    if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
   }

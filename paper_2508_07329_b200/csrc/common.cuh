@@ -134,4 +134,24 @@ __device__ __forceinline__ AffineParams affine_params(double mn, double mx, int 
   return p;
 }
 
+
+// Launch with programmatic dependent launch allowed: the kernel may start
+// while the previous kernel in the stream is still running and must call
+// griddepcontrol.wait (ptx.cuh: griddep_wait) before touching its outputs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace moe

@@ -63,6 +63,7 @@ struct GemmArgs {
   int param_vec_ok;  // W zp / rowsum / scale tables allow 16-byte vector loads
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   int band;                 // m-tiles per raster band (map_tile)
+  int pf_kb;                // k blocks of the first weight tile to prefetch into L2 before griddep_wait
   void* const* out_tab;     // DEQUANT: row m goes to out_tab[out_rank[m]] + out_row[m] * ldo (EP combine)
   const int32_t* out_rank;
   const int32_t* out_row;
@@ -675,6 +676,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int unit = (int)blockIdx.x / CG;         // scheduling unit: a CTA or a CTA pair
   const int n_units = (int)gridDim.x / CG;
 
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    // Launched with programmatic dependent launch: until griddep_wait() only
+    // work independent of the previous kernel's outputs. At decode sizes the
+    // grouped GEMM streams the weights; start pulling this unit's likely
+    // first weight tile (group unit / n_tiles, n block unit % n_tiles — the
+    // group offsets are not known yet) into L2 while the previous kernel runs.
+    if (p.pf_kb > 0) {
+      const int g = unit / n_tiles, nb = unit % n_tiles;
+      if (g < p.G)
+        for (int kb = 0; kb < p.pf_kb; ++kb)
+          tma_prefetch_2d(&tmB, kb * kBK, g * p.N + nb * BN + (int)rank * (BN / CG));
+    }
+  }
+  griddep_wait();
   if (threadIdx.x == 0) {
     if (p.offsets) {
       for (int g = 0; g <= p.G; ++g) off[g] = p.offsets[g];
@@ -697,10 +714,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[s], 32 * kEpiWarps * CG);  // all epilogue threads of the pair (leader's copy)
     }
     fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
   }
   if (warp == 2) {
     if (CG == 2) {
@@ -962,23 +975,24 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
   auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG, FQ, CB>;
   constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
   MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(kern), bytes));
-  if (CG == 1) {
-    kern<<<grid, kGemmThreads, bytes, s>>>(ta, tb, to, p);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = bytes;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, p));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see griddep_wait)
+  attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  if (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
   }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, p));
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
@@ -1017,6 +1031,9 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
     static const int64_t budget = getenv("MOE_B200_BAND_MB") ? atoll(getenv("MOE_B200_BAND_MB")) << 20 : (24LL << 20);
     p.band = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 20, budget / (TM * std::max<int64_t>(K, 1))));
   }
+  // decode sizes (weight-stream bound): L2-prefetch the first 640 KB of each
+  // unit's first weight tile during the previous kernel (PDL)
+  p.pf_kb = (M <= 1024) ? (int)std::min<int64_t>((K + kBK - 1) / kBK, (640 << 10) / ((BN / CG) * kBK)) : 0;
   const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
   const int64_t max_units = num_sms() / CG;
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
@@ -1236,8 +1253,9 @@ extern "C" moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t
   cb.comb_chunks = (int)(N / 32);
   cb.comb_out = static_cast<__nv_bfloat16*>(out);
   cb.comb_ldo = ldo;
-  MOE_CUDA_TRY(cudaMemsetAsync(workspace, 0, (size_t)moe_w8a8_gemm_combine_workspace(T, N), as_stream(stream)));
+  if (!(epilogue & MOE_EPI_FLAG_WS_ZEROED))
+    MOE_CUDA_TRY(cudaMemsetAsync(workspace, 0, (size_t)moe_w8a8_gemm_combine_workspace(T, N), as_stream(stream)));
   return gemm_entry(a, M, K, lda, a_scale, a_zp, a_rowsum, w, N, ldw, w_scale, w_zp, w_rowsum, nullptr, row_weight,
-                    group_offsets, num_groups, epilogue, y, MOE_DT_BF16, ldy, nullptr, 0, nullptr, 0, nullptr, nullptr,
-                    nullptr, nullptr, stream, nullptr, &cb);
+                    group_offsets, num_groups, epilogue & ~MOE_EPI_FLAG_WS_ZEROED, y, MOE_DT_BF16, ldy, nullptr, 0,
+                    nullptr, 0, nullptr, nullptr, nullptr, nullptr, stream, nullptr, &cb);
 }

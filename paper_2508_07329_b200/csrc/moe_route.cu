@@ -5,6 +5,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace moe {
 
@@ -376,6 +377,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_single_kernel(const int3
                                                                       float* row_weight, int32_t* token_pos) {
   __shared__ int run[kMaxE];
   __shared__ int wcnt[kPermThreads / 32][kMaxE];
+  griddep_wait();                 // PDL: the router's selections are visible from here
+  griddep_launch_dependents();
   for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = 0;
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&run[idx[i]], 1);
@@ -572,8 +575,8 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
   int32_t* base = counts + (int64_t)nb * E;
   cudaStream_t s = as_stream(stream);
   if (nb == 1) {
-    permute_single_kernel<<<1, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, expert_offsets, src_token,
-                                                     row_expert, row_weight, token_pos);
+    MOE_CUDA_TRY(launch_pdl(permute_single_kernel, dim3(1), dim3(kPermThreads), 0, s, topk_idx, topk_w, n, k, E,
+                            expert_offsets, src_token, row_expert, row_weight, token_pos));
     ::moe::count_launch();
     MOE_LAUNCH_CHECK();
     return MOE_OK;

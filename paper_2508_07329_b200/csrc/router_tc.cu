@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* done = empty + kRtStages;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_launch_dependents();   // the permutation kernel (PDL) may get ready meanwhile
   const uint32_t rank = cluster_ctarank(), nrank = cluster_nctarank();
   const int64_t row0 = (int64_t)(blockIdx.x / nrank) * kRtM;
   const int kblocks = (int)(d / kRtBK);

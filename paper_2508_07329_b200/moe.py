@@ -164,15 +164,19 @@ class MoELayer:
                                           n_per_group=self.d, out_dtype=y_dtype, row_weight=perm["row_weight"])
             mark("gemm2")
         else:
+            fused_combine = (self.k == 2 and not return_aux and y_dtype == torch.bfloat16
+                             and out_dtype == torch.bfloat16 and self.d % 32 == 0 and self.F % 16 == 0
+                             and L.tune(L.TUNE_FUSED_COMBINE) > 0)
+            # (zeroed before K1 of h, so nothing sits between K1 and the PDL-launched GEMM)
+            cws = ops.combine_workspace(T, self.d, x.device) if fused_combine else None
             a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
                                row_group=perm["row_expert"], row_ext=ext)
             mark("quant_h")
-            if (self.k == 2 and not return_aux and y_dtype == torch.bfloat16 and out_dtype == torch.bfloat16
-                    and self.d % 32 == 0 and self.F % 16 == 0 and L.tune(L.TUNE_FUSED_COMBINE) > 0):
+            if fused_combine:
                 # the top-2 combine fused into GEMM2's epilogue (bit-identical)
                 out = ops.w8a8_gemm_combine(a2, self.w2, row_weight=perm["row_weight"], group_offsets=perm["offsets"],
                                             num_groups=self.E, n_per_group=self.d, src_token=perm["src_token"],
-                                            token_pos=perm["token_pos"], T=T, out=out)
+                                            token_pos=perm["token_pos"], T=T, out=out, workspace=cws)
                 mark("gemm2")
                 mark("combine")
                 return out

@@ -203,9 +203,15 @@ def w8a8_gemm_quant_a(x: torch.Tensor, w: dict, *, smooth: torch.Tensor, smooth_
     return o, a
 
 
+def combine_workspace(T: int, N: int, device) -> torch.Tensor:
+    """Zeroed workspace for w8a8_gemm_combine (allocate it before the kernel
+    that precedes the GEMM so no memset sits between them)."""
+    return torch.zeros(L.load().moe_w8a8_gemm_combine_workspace(T, N), dtype=torch.uint8, device=device)
+
+
 def w8a8_gemm_combine(a: dict, w: dict, *, row_weight: torch.Tensor, group_offsets: torch.Tensor, num_groups: int,
                       n_per_group: int, src_token: torch.Tensor, token_pos: torch.Tensor, T: int,
-                      out: torch.Tensor | None = None) -> torch.Tensor:
+                      out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
     """The MoE second grouped GEMM with the top-2 combine fused in
     (moe_w8a8_gemm_combine): returns out [T, N] bf16, equal to
     combine(w8a8_gemm(a, w, bf16), token_pos, T, 2)."""
@@ -216,8 +222,12 @@ def w8a8_gemm_combine(a: dict, w: dict, *, row_weight: torch.Tensor, group_offse
     y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     o = out if out is not None else torch.empty((T, N), dtype=torch.bfloat16, device=dev)
     wsb = L.load().moe_w8a8_gemm_combine_workspace(T, N)
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
+    if workspace is not None:           # pre-zeroed by the caller
+        ws = workspace
+        flags |= L.EPI_FLAG_WS_ZEROED
+    else:
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     L.call("moe_w8a8_gemm_combine", L.ptr(ac), M, K, ac.stride(0), L.ptr(a["scale_f32"]), L.ptr(a["zp"]),
            L.ptr(a["rowsum"]), L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w_rs),
            L.ptr(row_weight), L.ptr(group_offsets), num_groups, L.EPI_DEQUANT | flags, L.ptr(y), y.stride(0),
