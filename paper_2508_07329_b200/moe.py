@@ -164,9 +164,11 @@ class MoELayer:
                                           n_per_group=self.d, out_dtype=y_dtype, row_weight=perm["row_weight"])
             mark("gemm2")
         else:
+            # (decode-size batches keep the separate combine: the per-chunk
+            # hand-off costs more than the 4 us kernel at a few dozen rows)
             fused_combine = (self.k == 2 and not return_aux and y_dtype == torch.bfloat16
                              and out_dtype == torch.bfloat16 and self.d % 32 == 0 and self.F % 16 == 0
-                             and L.tune(L.TUNE_FUSED_COMBINE) > 0)
+                             and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS) and L.tune(L.TUNE_FUSED_COMBINE) > 0)
             # (zeroed before K1 of h, so nothing sits between K1 and the PDL-launched GEMM)
             cws = ops.combine_workspace(T, self.d, x.device) if fused_combine else None
             a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,

@@ -179,9 +179,12 @@ def test_moe_fused_combine_matches(cuda, small_layer, T):
     x = torch.from_numpy(_x(np.random.default_rng(T + 7), T, 512)).to(cuda).bfloat16()
     outs = []
     for fused in (0, 1):
-        with L.tuned(L.TUNE_FUSED_COMBINE, fused):
+        # (small-row threshold 0: the fused path also runs at decode sizes)
+        with L.tuned(L.TUNE_FUSED_COMBINE, fused), L.tuned(L.TUNE_K1_SMALL_ROWS, 0):
             outs.append(small_layer.forward(x))
+    outs.append(small_layer.forward(x))            # default knobs
     assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
 
 
 def test_moe_edge_batches(cuda, small_layer):
