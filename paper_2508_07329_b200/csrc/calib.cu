@@ -101,63 +101,94 @@ __global__ void hessian_finalize_kernel(double* H, int64_t n, double damping, co
 // run the in-tile sequential loop. Per element the subtractions happen in
 // exactly the reference's order, so codes are bit-identical.
 constexpr int kGT = 32;      // columns per tile
-constexpr int kGRows = 64;   // rows (threads) per CTA
 constexpr int kGU = 64;      // U rows per smem stage
 
-__global__ void __launch_bounds__(kGRows) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
-                                                               const int32_t* order, const double* U,
-                                                               const double* scale, const int32_t* zp, int qmax,
-                                                               uint8_t* codes, int64_t ldc, double* err) {
+// Each row is owned by kGP adjacent lanes, lane p holding the tile columns
+// j = p, p + kGP, ... (kGT / kGP of them): the left-looking updates of a tile
+// are split kGP ways, and in the in-tile sequential part the owner of column
+// i computes its code and error and shuffles the error to the row's other
+// lanes. Every element still receives its updates one at a time, separate
+// multiply and subtract, in ascending column order (quant.py:425-430), so
+// the codes equal the reference's bit for bit.
+constexpr int kGThreads = 128;
+
+template <int kGP>   // lanes per row (8 or 32)
+__global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
+                                                                  const int32_t* order, const double* U,
+                                                                  const double* scale, const int32_t* zp, int qmax,
+                                                                  uint8_t* codes, int64_t ldc, double* err) {
+  constexpr int kGRowsCta = kGThreads / kGP;             // rows per CTA
+  constexpr int kGQ = kGT / kGP;                         // tile columns per lane
   __shared__ __align__(16) double us[kGU][kGT];
+  __shared__ __align__(16) double es[kGU][kGRowsCta];    // the CTA's rows' errors of the staged columns
   __shared__ __align__(16) double ut[kGT][kGT + 1];
-  const int64_t r = (int64_t)blockIdx.x * kGRows + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int p = threadIdx.x % kGP;                       // column phase of this lane
+  const int rl = threadIdx.x / kGP;                      // row within the CTA
+  const int64_t r0 = (int64_t)blockIdx.x * kGRowsCta;
+  const int64_t r = (int64_t)blockIdx.x * kGRowsCta + threadIdx.x / kGP;
+  const unsigned group = (lane / kGP) * kGP;             // first lane of this row's group
   const bool valid = r < R;
   const double sc = valid ? scale[r] : 1.0;
   const double rsc = __drcp_rn(sc);
   const int z = valid ? zp[r] : 0;
   for (int64_t J = 0; J < n; J += kGT) {
     const int tw = (int)((n - J) < kGT ? (n - J) : kGT);
-    double w[kGT];
+    double w[kGQ];
 #pragma unroll
-    for (int j = 0; j < kGT; ++j) {
+    for (int q = 0; q < kGQ; ++q) {
+      const int j = p + kGP * q;
       const int64_t col = J + j;
-      w[j] = (valid && j < tw) ? W[r * ldw + (order ? (int64_t)order[col] : col)] : 0.0;
+      w[q] = (valid && j < tw) ? W[r * ldw + (order ? (int64_t)order[col] : col)] : 0.0;
     }
     // updates from all previous columns, ascending
     for (int64_t i0 = 0; i0 < J; i0 += kGU) {
       const int ni = (int)((J - i0) < kGU ? (J - i0) : kGU);
       __syncthreads();
-      for (int q = threadIdx.x; q < kGU * kGT; q += kGRows) {
-        const int ii = q / kGT, jj = q % kGT;
+      for (int t = threadIdx.x; t < kGU * kGT; t += kGThreads) {
+        const int ii = t / kGT, jj = t % kGT;
         us[ii][jj] = (ii < ni && jj < tw) ? U[(i0 + ii) * n + J + jj] : 0.0;
       }
+      for (int t = threadIdx.x; t < kGU * kGRowsCta; t += kGThreads) {
+        const int ii = t / kGRowsCta, rr = t % kGRowsCta;
+        es[ii][rr] = (ii < ni && r0 + rr < R) ? err[(i0 + ii) * R + r0 + rr] : 0.0;
+      }
       __syncthreads();
+#pragma unroll 4
       for (int ii = 0; ii < ni; ++ii) {
-        const double e = valid ? err[(i0 + ii) * R + r] : 0.0;
+        const double e = es[ii][rl];
 #pragma unroll
-        for (int j = 0; j < kGT; ++j) w[j] = __dsub_rn(w[j], __dmul_rn(e, us[ii][j]));
+        for (int q = 0; q < kGQ; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(e, us[ii][p + kGP * q]));
       }
     }
     // in-tile sequential part
     __syncthreads();
-    for (int q = threadIdx.x; q < kGT * kGT; q += kGRows) {
-      const int ii = q / kGT, jj = q % kGT;
+    for (int t = threadIdx.x; t < kGT * kGT; t += kGThreads) {
+      const int ii = t / kGT, jj = t % kGT;
       ut[ii][jj] = (ii < tw && jj < tw) ? U[(J + ii) * n + J + jj] : 0.0;
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kGT; ++i) {
       if (i < tw) {
-        const int c = encode_code(w[i], sc, rsc, z, qmax);
-        const double deq = __dmul_rn((double)(c - z), sc);
-        const double e = __ddiv_rn(__dsub_rn(w[i], deq), ut[i][i]);
-        if (valid) {
-          err[(J + i) * R + r] = e;
-          const int64_t col = J + i;
-          codes[r * ldc + (order ? (int64_t)order[col] : col)] = (uint8_t)c;
+        const int owner = i % kGP, qi = i / kGP;
+        double e = 0.0;
+        if (p == owner) {
+          const int c = encode_code(w[qi], sc, rsc, z, qmax);
+          const double deq = __dmul_rn((double)(c - z), sc);
+          e = __ddiv_rn(__dsub_rn(w[qi], deq), ut[i][i]);
+          if (valid) {
+            err[(J + i) * R + r] = e;
+            const int64_t col = J + i;
+            codes[r * ldc + (order ? (int64_t)order[col] : col)] = (uint8_t)c;
+          }
         }
+        e = __shfl_sync(0xffffffffu, e, (int)group + owner);
 #pragma unroll
-        for (int j = i + 1; j < kGT; ++j) w[j] = __dsub_rn(w[j], __dmul_rn(e, ut[i][j]));
+        for (int q = 0; q < kGQ; ++q) {
+          const int j = p + kGP * q;
+          if (j > i) w[q] = __dsub_rn(w[q], __dmul_rn(e, ut[i][j]));
+        }
       }
     }
   }
@@ -249,9 +280,18 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
   MOE_REQUIRE(R >= 1 && n >= 1 && ldw >= n && ldc >= n, "gptq_columns: bad shape");
   MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
   MOE_REQUIRE(err_ws_bytes >= moe_gptq_workspace(R, n), "gptq_columns: workspace too small");
-  const unsigned blocks = (unsigned)((R + kGRows - 1) / kGRows);
-  gptq_columns_kernel<<<blocks, kGRows, 0, as_stream(stream)>>>(W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1,
-                                                               codes, ldc, static_cast<double*>(err_ws)); ::moe::count_launch();
+  // few rows (e.g. W2 of an expert, 4096): a whole warp per row so the SMs
+  // have enough independent rows; many rows: 8 lanes per row, 4 columns each
+  static const int forced = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
+  const int P = forced ? forced : (R <= 8192 ? 32 : 8);
+  const unsigned blocks = (unsigned)((R + kGThreads / P - 1) / (kGThreads / P));
+  if (P == 32)
+    gptq_columns_kernel<32><<<blocks, kGThreads, 0, as_stream(stream)>>>(
+        W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes, ldc, static_cast<double*>(err_ws));
+  else
+    gptq_columns_kernel<8><<<blocks, kGThreads, 0, as_stream(stream)>>>(
+        W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes, ldc, static_cast<double*>(err_ws));
+  ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }
