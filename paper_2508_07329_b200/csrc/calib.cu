@@ -3,6 +3,7 @@
 // (quant.py:415-434) in strict reference order, and the Frobenius-loss
 // reduction used by quant_loss / search_smoothing (quant.py:267-311).
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace moe {
 
@@ -101,7 +102,10 @@ __global__ void hessian_finalize_kernel(double* H, int64_t n, double damping, co
 // run the in-tile sequential loop. Per element the subtractions happen in
 // exactly the reference's order, so codes are bit-identical.
 constexpr int kGT = 32;      // columns per tile
-constexpr int kGU = 64;      // U rows per smem stage
+#ifndef MOE_GPTQ_STAGE
+#define MOE_GPTQ_STAGE 32
+#endif
+constexpr int kGStage = MOE_GPTQ_STAGE;   // U rows per shared-memory stage (double-buffered)
 
 // Each row is owned by kGP adjacent lanes, lane p holding the tile columns
 // j = p, p + kGP, ... (kGT / kGP of them): the left-looking updates of a tile
@@ -112,21 +116,33 @@ constexpr int kGU = 64;      // U rows per smem stage
 // the codes equal the reference's bit for bit.
 constexpr int kGThreads = 128;
 
-template <int kGP>   // lanes per row (8 or 32)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int kGP, int kGS>   // lanes per row (8 or 32; lane p owns tile columns [p * kGQ, (p + 1) * kGQ)), staged U rows
 __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
                                                                   const int32_t* order, const double* U,
                                                                   const double* scale, const int32_t* zp, int qmax,
                                                                   uint8_t* codes, int64_t ldc, double* err) {
   constexpr int kGRowsCta = kGThreads / kGP;             // rows per CTA
   constexpr int kGQ = kGT / kGP;                         // tile columns per lane
-  __shared__ __align__(16) double us[kGU][kGT];
-  __shared__ __align__(16) double es[kGU][kGRowsCta];    // the CTA's rows' errors of the staged columns
-  __shared__ __align__(16) double ut[kGT][kGT + 1];
+  constexpr int kGU = kGS;
+  extern __shared__ __align__(16) double gsm[];
+  auto us = reinterpret_cast<double (*)[kGU][kGT]>(gsm);                        // [2][kGU][kGT] U rows (double-buffered)
+  auto es = reinterpret_cast<double (*)[kGU][kGRowsCta]>(gsm + 2 * kGU * kGT);  // [2][kGU][rows] errors
+  auto ut = reinterpret_cast<double (*)[kGT + 1]>(gsm + 2 * kGU * kGT + 2 * kGU * kGRowsCta);
   const int lane = threadIdx.x & 31;
-  const int p = threadIdx.x % kGP;                       // column phase of this lane
+  const int p = threadIdx.x % kGP;                       // column block of this lane
   const int rl = threadIdx.x / kGP;                      // row within the CTA
   const int64_t r0 = (int64_t)blockIdx.x * kGRowsCta;
-  const int64_t r = (int64_t)blockIdx.x * kGRowsCta + threadIdx.x / kGP;
+  const int64_t r = r0 + rl;
   const unsigned group = (lane / kGP) * kGP;             // first lane of this row's group
   const bool valid = r < R;
   const double sc = valid ? scale[r] : 1.0;
@@ -137,32 +153,56 @@ __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W
     double w[kGQ];
 #pragma unroll
     for (int q = 0; q < kGQ; ++q) {
-      const int j = p + kGP * q;
+      const int j = p * kGQ + q;
       const int64_t col = J + j;
       w[q] = (valid && j < tw) ? W[r * ldw + (order ? (int64_t)order[col] : col)] : 0.0;
     }
-    // updates from all previous columns, ascending
-    for (int64_t i0 = 0; i0 < J; i0 += kGU) {
+    // updates from all previous columns, ascending; the next chunk of U rows
+    // and errors streams in (cp.async) while this one is applied
+    auto stage = [&](int64_t i0, int buf) {
       const int ni = (int)((J - i0) < kGU ? (J - i0) : kGU);
-      __syncthreads();
       for (int t = threadIdx.x; t < kGU * kGT; t += kGThreads) {
         const int ii = t / kGT, jj = t % kGT;
-        us[ii][jj] = (ii < ni && jj < tw) ? U[(i0 + ii) * n + J + jj] : 0.0;
+        const bool ok = ii < ni && jj < tw;
+        cp_async8(&us[buf][ii][jj], ok ? U + (i0 + ii) * n + J + jj : U, ok);
       }
       for (int t = threadIdx.x; t < kGU * kGRowsCta; t += kGThreads) {
         const int ii = t / kGRowsCta, rr = t % kGRowsCta;
-        es[ii][rr] = (ii < ni && r0 + rr < R) ? err[(i0 + ii) * R + r0 + rr] : 0.0;
+        const bool ok = ii < ni && r0 + rr < R;
+        cp_async8(&es[buf][ii][rr], ok ? err + (i0 + ii) * R + r0 + rr : err, ok);
+      }
+      cp_async_commit();
+    };
+    if (J > 0) stage(0, 0);
+    int buf = 0;
+    for (int64_t i0 = 0; i0 < J; i0 += kGU, buf ^= 1) {
+      const int ni = (int)((J - i0) < kGU ? (J - i0) : kGU);
+      if (i0 + kGU < J) {
+        stage(i0 + kGU, buf ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
 #pragma unroll 4
       for (int ii = 0; ii < ni; ++ii) {
-        const double e = es[ii][rl];
+        const double e = es[buf][ii][rl];
+        const double* u = &us[buf][ii][p * kGQ];
+        if constexpr (kGQ % 2 == 0) {
 #pragma unroll
-        for (int q = 0; q < kGQ; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(e, us[ii][p + kGP * q]));
+          for (int q = 0; q < kGQ; q += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(u + q);
+            w[q] = __dsub_rn(w[q], __dmul_rn(e, v.x));
+            w[q + 1] = __dsub_rn(w[q + 1], __dmul_rn(e, v.y));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kGQ; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(e, u[q]));
+        }
       }
+      __syncthreads();   // this buffer is restaged two chunks later
     }
     // in-tile sequential part
-    __syncthreads();
     for (int t = threadIdx.x; t < kGT * kGT; t += kGThreads) {
       const int ii = t / kGT, jj = t % kGT;
       ut[ii][jj] = (ii < tw && jj < tw) ? U[(J + ii) * n + J + jj] : 0.0;
@@ -171,7 +211,7 @@ __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W
 #pragma unroll
     for (int i = 0; i < kGT; ++i) {
       if (i < tw) {
-        const int owner = i % kGP, qi = i / kGP;
+        const int owner = i / kGQ, qi = i % kGQ;
         double e = 0.0;
         if (p == owner) {
           const int c = encode_code(w[qi], sc, rsc, z, qmax);
@@ -186,11 +226,12 @@ __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W
         e = __shfl_sync(0xffffffffu, e, (int)group + owner);
 #pragma unroll
         for (int q = 0; q < kGQ; ++q) {
-          const int j = p + kGP * q;
+          const int j = p * kGQ + q;
           if (j > i) w[q] = __dsub_rn(w[q], __dmul_rn(e, ut[i][j]));
         }
       }
     }
+    __syncthreads();   // ut and the error columns of this tile are complete before the next tile
   }
 }
 
@@ -285,12 +326,16 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
   static const int forced = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
   const int P = forced ? forced : (R <= 8192 ? 32 : 8);
   const unsigned blocks = (unsigned)((R + kGThreads / P - 1) / (kGThreads / P));
-  if (P == 32)
-    gptq_columns_kernel<32><<<blocks, kGThreads, 0, as_stream(stream)>>>(
-        W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes, ldc, static_cast<double*>(err_ws));
-  else
-    gptq_columns_kernel<8><<<blocks, kGThreads, 0, as_stream(stream)>>>(
-        W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes, ldc, static_cast<double*>(err_ws));
+  auto launch = [&](auto kern, int rows_cta) -> cudaError_t {
+    const int smem = (int)sizeof(double) * (2 * kGStage * kGT + 2 * kGStage * rows_cta + kGT * (kGT + 1));
+    const cudaError_t e = set_max_smem_once(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, kGThreads, smem, as_stream(stream)>>>(W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes,
+                                                         ldc, static_cast<double*>(err_ws));
+    return cudaGetLastError();
+  };
+  MOE_CUDA_TRY(P == 32 ? launch(gptq_columns_kernel<32, kGStage>, kGThreads / 32)
+                       : launch(gptq_columns_kernel<8, kGStage>, kGThreads / 8));
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
