@@ -982,8 +982,11 @@ static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const 
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see griddep_wait)
-  attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = getenv("MOE_B200_NO_PDL") != nullptr;   // (A/B switch)
+  if (!no_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see griddep_wait)
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   if (CG == 2) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = 2;
