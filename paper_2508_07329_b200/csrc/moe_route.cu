@@ -294,33 +294,6 @@ __global__ void permute_count_kernel(const int32_t* idx, int64_t n, int E, int32
   for (int e = threadIdx.x; e < E; e += blockDim.x) block_counts[(int64_t)blockIdx.x * E + e] = cnt[e];
 }
 
-// single block: offsets[e] and per-block bases (block-major exclusive scan)
-__global__ void permute_scan_kernel(const int32_t* block_counts, int nblocks, int E, int32_t* block_base,
-                                    int32_t* offsets) {
-  __shared__ int tot[kMaxE];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int s = 0;
-    for (int b = 0; b < nblocks; ++b) s += block_counts[(int64_t)b * E + e];
-    tot[e] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int e = 0; e < E; ++e) {
-      offsets[e] = s;
-      s += tot[e];
-    }
-    offsets[E] = s;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int s = offsets[e];
-    for (int b = 0; b < nblocks; ++b) {
-      block_base[(int64_t)b * E + e] = s;
-      s += block_counts[(int64_t)b * E + e];
-    }
-  }
-}
 
 // stable scatter of pairs [lo, hi) given each expert's first free row (run[])
 __device__ __forceinline__ void permute_scatter_range(const int32_t* idx, const float* topk_w, int64_t lo, int64_t hi,
@@ -356,14 +329,40 @@ __device__ __forceinline__ void permute_scatter_range(const int32_t* idx, const 
   }
 }
 
+// Every block derives its own bases from the per-block counts (nblocks x E
+// ints, tiny): expert offset = sum of earlier experts' totals, plus the
+// counts of earlier blocks; block 0 also writes the offsets. (No separate
+// scan launch.)
 __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t* idx, const float* topk_w,
                                                                        int64_t n, int k, int E,
-                                                                       const int32_t* block_base,
-                                                                       int32_t* src_token, int32_t* row_expert,
-                                                                       float* row_weight, int32_t* token_pos) {
+                                                                       const int32_t* block_counts, int nblocks,
+                                                                       int32_t* offsets, int32_t* src_token,
+                                                                       int32_t* row_expert, float* row_weight,
+                                                                       int32_t* token_pos) {
   __shared__ int run[kMaxE];
+  __shared__ int tot[kMaxE];
   __shared__ int wcnt[kPermThreads / 32][kMaxE];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = block_base[(int64_t)blockIdx.x * E + e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int t = 0, before = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      const int c = block_counts[(int64_t)b * E + e];
+      t += c;
+      if (b < (int)blockIdx.x) before += c;
+    }
+    tot[e] = t;
+    run[e] = before;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int e = 0; e < E; ++e) {
+      run[e] += s;
+      if (blockIdx.x == 0) offsets[e] = s;
+      s += tot[e];
+    }
+    if (blockIdx.x == 0) offsets[E] = s;
+  }
+  __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
   permute_scatter_range(idx, topk_w, lo, min(n, lo + kPermChunk), k, E, run, wcnt, src_token, row_expert, row_weight,
                         token_pos);
@@ -572,7 +571,6 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
   const int64_t n = T * k;
   const int nb = (int)((n + kPermChunk - 1) / kPermChunk);
   int32_t* counts = static_cast<int32_t*>(workspace);
-  int32_t* base = counts + (int64_t)nb * E;
   cudaStream_t s = as_stream(stream);
   if (nb == 1) {
     MOE_CUDA_TRY(launch_pdl(permute_single_kernel, dim3(1), dim3(kPermThreads), 0, s, topk_idx, topk_w, n, k, E,
@@ -582,9 +580,9 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
     return MOE_OK;
   }
   permute_count_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, n, E, counts); ::moe::count_launch();
-  permute_scan_kernel<<<1, 64, 0, s>>>(counts, nb, E, base, expert_offsets); ::moe::count_launch();
-  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, base, src_token, row_expert,
-                                                     row_weight, token_pos); ::moe::count_launch();
+  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, counts, nb, expert_offsets,
+                                                     src_token, row_expert, row_weight, token_pos);
+  ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }
