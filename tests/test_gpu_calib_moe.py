@@ -64,3 +64,51 @@ def test_calibrate_moe_layer_quality(cuda):
     e_haq, e_rtn = err(haq), err(rtn)
     assert e_haq < 0.05, e_haq
     assert e_haq < e_rtn, (e_haq, e_rtn)
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_calibrate_moe_layer_distributed_gloo_two_ranks(tmp_path):
+    """Experts calibrated on two ranks (expert e on rank e % 2; gloo
+    collectives on host tensors, both processes on GPU 0, no kernel waits on
+    the other process) and broadcast: both ranks build the layer the
+    single-process calibration builds, bit for bit."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    port = _free_port()
+    script = textwrap.dedent(f"""
+        import os, sys, numpy as np, torch
+        sys.path.insert(0, {repr(os.getcwd())})
+        import torch.distributed as dist
+        from paper_2508_07329_b200.calib_moe import calibrate_moe_layer, calibrate_moe_layer_distributed
+        rank = int(sys.argv[1])
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        rng = np.random.default_rng(0)
+        E, D, F = 4, 128, 256
+        experts = [{{"w1": rng.normal(size=(F, D)) * 0.05, "w3": rng.normal(size=(F, D)) * 0.05,
+                     "w2": rng.normal(size=(D, F)) * 0.05}} for _ in range(E)]
+        wg = (rng.normal(size=(E, D)) / np.sqrt(D)).astype(np.float32)
+        x = torch.from_numpy(rng.normal(size=(256, D)).astype(np.float32)).cuda()
+        lay, rep = calibrate_moe_layer_distributed(wg, experts, x, top_k=2, grid_steps=5)
+        ref, rrep = calibrate_moe_layer(wg, experts, x, top_k=2, grid_steps=5)
+        ok = all(torch.equal(lay.w13[k], ref.w13[k]) and torch.equal(lay.w2[k], ref.w2[k])
+                 for k in ("codes", "scale_f32", "zp")) and torch.equal(lay.s13, ref.s13) and \\
+             [r.exponent13 for r in rep] == [r.exponent13 for r in rrep]
+        dist.destroy_process_group()
+        print("EQUAL" if ok else "DIFFERENT")
+    """)
+    path = tmp_path / "calib_dist.py"
+    path.write_text(script)
+    procs = [subprocess.Popen([sys.executable, str(path), str(r)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for o, e in outs:
+        assert "EQUAL" in o, o + e[-3000:]
