@@ -142,7 +142,11 @@ def measured_peaks() -> dict:
 
 # ── CPU reference path (oracle, test infrastructure; timed, never shipped) ──
 def cpu_moe_baseline(experts_host: list, gate_w: np.ndarray, gate_b, x: np.ndarray, tokens: int,
-                     budget_s: float) -> dict:
+                     warmup: int, runs: int, budget_s: float | None = None) -> dict:
+    """The oracle's reference-style float64 fake-quant MoE layer on ``tokens``
+    tokens: ``warmup`` untimed runs, then ``runs`` timed runs (stopping early
+    once ``budget_s`` of timed CPU work is spent, if given); value = tokens /
+    mean run time."""
     from oracle import moe_ref as M
     from oracle import quant_ref as Q
 
@@ -153,19 +157,75 @@ def cpu_moe_baseline(experts_host: list, gate_w: np.ndarray, gate_b, x: np.ndarr
                        for n in ("w1", "w3", "w2")}})
     xs = x[:tokens].astype(np.float64)
     logits = (xs @ gate_w.astype(np.float64).T + (0 if gate_b is None else gate_b)).astype(np.float32)
+    for _ in range(warmup):
+        M.moe_forward_fakequant(xs, None, deq, TOPK, logits=logits)
     times = []
-    t_end = time.perf_counter() + budget_s
-    while not times or time.perf_counter() < t_end:
+    t_all = time.perf_counter()
+    while len(times) < max(1, runs):
         t0 = time.perf_counter()
         M.moe_forward_fakequant(xs, None, deq, TOPK, logits=logits)
         times.append(time.perf_counter() - t0)
-        if len(times) >= 5:
+        if budget_s is not None and time.perf_counter() - t_all > budget_s:
             break
-    best = min(times)
-    return {"value": tokens / best, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{tokens} tokens x {len(times)} runs (best), Mixtral-shape layer, all 8 experts, "
-                      f"float64 fake-quant (oracle/moe_ref.moe_forward_fakequant), weights pre-dequantized",
-            "seconds_per_run": best}
+    mean = sum(times) / len(times)
+    return {"value": tokens / mean, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{tokens} tokens per run, {warmup} warm-up + {len(times)} timed runs (mean), "
+                      f"Mixtral-shape layer, all 8 experts, float64 fake-quant (oracle/moe_ref."
+                      f"moe_forward_fakequant), weights pre-dequantized, numpy/OpenBLAS on all host threads",
+            "seconds_per_run": mean, "runs": len(times), "warmup_runs": warmup}
+
+
+def gemm_roofline(T: int, stages: dict, peaks: dict) -> dict:
+    """Roofline line of the two grouped W8A8 GEMM launches (the dominant
+    kernel). Denominators: INT8 dense = 2 x the MEASURED bf16 cuBLAS rate
+    of MEASURED_PEAKS.json (burst: the GEMMs are timed over a short run of
+    steps; the sustained fraction is reported beside it), HBM = the measured
+    copy bandwidth. Below the ridge (ops per algorithmic byte < peak ops /
+    HBM bytes/s: decode-size batches, where the 1.41 GB of expert weights
+    dominate) the GEMMs are weight-stream bound and the line reports GB/s."""
+    gemm_ms = stages.get("gemm13_swiglu", 0.0) + stages.get("gemm2", 0.0)
+    ops = T * TOPK * 6 * D * F
+    # operands + outputs each touched once: A1 (T k d) + W13 (2 E F d) + h bf16 (2 T k F)
+    # + A2 (T k F) + W2 (E d F) + y/out bf16 (2 T k d)
+    nbytes = T * TOPK * D + 2 * E * F * D + 2 * T * TOPK * F + T * TOPK * F + E * D * F + 2 * T * TOPK * D
+    src = peaks.get("source", "measured")
+    i8_burst = 2.0 * float(peaks["bf16_tflops"])
+    i8_sus = 2.0 * float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    hbm = float(peaks["hbm_gbs"])
+    ridge = i8_burst * 1e12 / (hbm * 1e9)
+    intensity = ops / nbytes
+    secs = gemm_ms / 1000.0 if gemm_ms > 0 else None
+    tops = ops / secs / 1e12 if secs else None
+    gbs = nbytes / secs / 1e9 if secs else None
+    tp = ROOT / "profiles" / "traffic.json"
+    traffic, tnote = None, "no ncu capture committed"
+    if tp.exists():
+        tj = json.loads(tp.read_text())
+        if tj.get("tokens") == T:
+            traffic = tj.get("grouped_gemm_bytes_per_step")
+            tnote = (f"ncu dram__bytes_read+write of the two grouped GEMM launches of one step at T={T} "
+                     f"(profiles/traffic.json, {tj.get('tag')}; cold-cache ncu pass of this bench command)")
+        else:
+            tnote = f"profiles/traffic.json was captured at T={tj.get('tokens')}, not {T}: not reported"
+    tensor = intensity >= ridge
+    line = {"bound": "tensor" if tensor else "hbm",
+            "kernel": "gemm_i8_tc_kernel (grouped W13+SwiGLU and W2 launches)",
+            "achieved": tops if tensor else gbs, "peak": i8_burst if tensor else hbm,
+            "unit": "TOPS (int8)" if tensor else "GB/s",
+            "traffic": traffic, "traffic_note": tnote,
+            "peak_note": (f"int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops (burst {peaks['bf16_tflops']}, "
+                          f"source={src}); HBM = MEASURED_PEAKS.json hbm_gbs" if tensor else
+                          f"MEASURED_PEAKS.json hbm_gbs (source={src}); below the int8 ridge"),
+            "algorithmic_ops_per_step": ops, "algorithmic_bytes_per_step": nbytes,
+            "intensity_ops_per_byte": intensity, "ridge_ops_per_byte": ridge,
+            "achieved_tops": tops, "achieved_gbs": gbs, "gemm_ms_per_step": gemm_ms,
+            "frac_of_sustained_int8": (tops / i8_sus) if tops else None,
+            "frac_of_spec_4500": (tops / 4500.0) if tops else None}
+    i8p = ROOT / "profiles" / "int8_peak.json"
+    if i8p.exists():
+        line["cublaslt_int8_8192cubed_tops"] = json.loads(i8p.read_text()).get("cublaslt_int8_burst")
+    line["frac"] = (line["achieved"] / line["peak"]) if line["achieved"] else None
+    return line
 
 
 def run_reference(args) -> None:
@@ -183,10 +243,12 @@ def run_reference(args) -> None:
         experts.append(ex)
     gw = (rng.normal(size=(E, D)) / np.sqrt(D)).astype(np.float32)
     x = synth_tokens(args.cpu_tokens, D, 0)
-    cb = cpu_moe_baseline(experts, gw, None, x, args.cpu_tokens, args.cpu_seconds)
+    # every step = one bounded sample (cpu_tokens tokens) of the workload: W
+    # untimed warm-up steps, then exactly K timed steps
+    cb = cpu_moe_baseline(experts, gw, None, x, args.cpu_tokens, args.warmup, args.steps)
     v = cb["value"]
     line = {"impl": "reference", "metric": "W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)", "value": v,
-            "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "unit": "tokens/s", "n_gpus": args.gpus, "steps": cb["runs"], "warmup": cb["warmup_runs"],
             "ms_per_step": 1000.0 * cb["seconds_per_run"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64 (fake-quant int8)", "data": "synthetic",
             "config": {"workload": WORKLOAD, "tokens_per_step": args.cpu_tokens, "experts": E, "top_k": TOPK,
@@ -196,11 +258,34 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def relaunch_under_torchrun(args) -> None:
+    """``--gpus N`` (N > 1) started as a plain process: re-exec under
+    torchrun with one rank per GPU (never silently measure one GPU)."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"[bench] relaunching: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
 def main() -> None:
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        relaunch_under_torchrun(args)
+    if world_env is not None and int(world_env) != args.gpus and "--gpus" in " ".join(sys.argv):
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
 
     import torch
     import torch.distributed as dist
@@ -347,45 +432,13 @@ def main() -> None:
                "h2d_gbs_raw": nbytes / c0.elapsed_time(c1) / 1e6, "d2h_gbs_raw": nbytes / c1.elapsed_time(c2) / 1e6}
 
     # ---- roofline of the dominant kernel (grouped W8A8 GEMMs) --------------
-    peaks = measured_peaks()
-    gemm_ms = stages.get("gemm13_swiglu", 0.0) + stages.get("gemm2", 0.0)
-    gemm_ops = T * TOPK * 6 * D * F
-    achieved = gemm_ops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
-    # denominator: the int8 tensor peak measured on this pool's B200s by
-    # cuBLASLt (tools/int8_peak.py -> profiles/int8_peak.json, burst figure:
-    # the larger, i.e. conservative for frac); fallback 2 x measured bf16
-    i8p = ROOT / "profiles" / "int8_peak.json"
-    i8 = json.loads(i8p.read_text()) if i8p.exists() else {}
-    if i8.get("cublaslt_int8_burst"):
-        peak_i8 = float(i8["cublaslt_int8_burst"])
-        peak_note = ("measured cuBLASLt int8 GEMM 8192^3 burst (profiles/int8_peak.json; sustained "
-                     f"{i8.get('cublaslt_int8_sustained', 0):.0f})")
-    else:
-        peak_i8 = 2.0 * float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-        peak_note = f"2 x measured bf16 sustained TFLOP/s (int8 dense rate = 2x bf16); source={peaks['source']}"
-    traffic = None
-    tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get("grouped_gemm_bytes_per_step")
-    roofline = {"bound": "tensor", "kernel": "gemm_i8_tc_kernel (grouped W13+SwiGLU and W2 launches)",
-                "achieved": achieved, "peak": peak_i8, "unit": "TOPS (int8)",
-                "frac": (achieved / peak_i8) if achieved else None, "traffic": traffic,
-                "peak_note": peak_note,
-                "algorithmic_ops_per_step": gemm_ops,
-                # operands + outputs each touched once: A1 (T k d) + W13 (2 E F d) + h (2 T k F)
-                # + A2 (T k F) + W2 (E d F) + y (2 T k d) bytes
-                "algorithmic_bytes_per_step": (T * TOPK * D + 2 * E * F * D + 2 * T * TOPK * F
-                                               + T * TOPK * F + E * D * F + 2 * T * TOPK * D),
-                "traffic_note": "traffic = ncu dram__bytes_read+write of the two grouped GEMM launches per step "
-                                "(profiles/traffic.json)",
-                "frac_of_spec_4500": (achieved / 4500.0) if achieved else None}
-
+    roofline = gemm_roofline(T, stages, measured_peaks())
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         experts_host = [layer.expert_host(e) for e in range(E)]
         cpu = cpu_moe_baseline(experts_host, layer.gate_w.cpu().numpy(),
                                None if layer.gate_b is None else layer.gate_b.cpu().numpy(),
-                               x_host.float().numpy(), args.cpu_tokens, args.cpu_seconds)
+                               x_host.float().numpy(), args.cpu_tokens, 1, 50, args.cpu_seconds)
 
     if rank == 0:
         value = T * world / (ms / 1000.0)

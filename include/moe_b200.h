@@ -89,12 +89,24 @@ moe_status moe_device_check(int dev);
  *   for its second GEMM, 0 (default) the separate K1 + GEMM.
  *   MOE_TUNE_FUSED_COMBINE: 1 (default) lets the top-2 MoE forward use
  *   moe_w8a8_gemm_combine, 0 the separate GEMM + combine.
- *   (Both read by the host layer; same results either way.) */
+ *   MOE_TUNE_K1_TOKENS: 1 (default) lets the MoE forward quantize x with
+ *   moe_act_quant_tokens (x read once per token), 0 the gathered
+ *   moe_act_quant. (These three are read by the host layer; same results
+ *   either way.)
+ *   MOE_TUNE_GPTQ_LANES: lanes per weight row of the moe_gptq_columns loop
+ *   (0 = automatic: 8 above 8192 rows, else 32; 8 or 32 forced).
+ *   MOE_TUNE_BAND_MB: grouped-GEMM raster band — MB of activation rows kept
+ *   L2-resident while the weight blocks stream past them (default 24; env
+ *   MOE_B200_BAND_MB sets the initial value). */
 enum {
   MOE_TUNE_K1_SMALL_ROWS = 1,
   MOE_TUNE_ROUTER_CLUSTER_TILES = 2,
   MOE_TUNE_FUSED_QUANT = 3,
-  MOE_TUNE_FUSED_COMBINE = 4
+  MOE_TUNE_FUSED_COMBINE = 4,
+  MOE_TUNE_K1_TOKENS = 5,
+  MOE_TUNE_GPTQ_LANES = 6,
+  MOE_TUNE_BAND_MB = 7,
+  MOE_TUNE_COUNT = 8
 };
 moe_status moe_tune(int key, int64_t value, int64_t* old);
 
@@ -135,6 +147,23 @@ moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols,
                          int granularity, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                          int32_t* zp, int32_t* rowsum, const unsigned long long* row_ext, void* workspace,
                          int64_t workspace_bytes, moe_stream_t stream);
+
+/* Token-major K1 for the MoE dispatch (rtn_quantize per_token of
+ * apply_smoothing's X / s, quant.py:214-231 / 314-324, as moe_act_quant):
+ * output row r = token_pos[t * k + j] (t < T, j < k) holds token t of x
+ * divided by smoothing row row_group[r]; every output row gets codes, scale,
+ * scale_f32, zp and rowsum exactly as moe_act_quant(gather_rows = the
+ * inverse of token_pos) would give. x is read once per token (all k rows
+ * are encoded from registers). Requires bf16 x, cols % 8 == 0, cols <= 4096,
+ * 16-byte aligned rows and the three smoothing tables; MOE_EINVAL otherwise.
+ * PDL-launched: x must not be written by the immediately preceding kernel
+ * of the stream when that kernel triggers its dependents early (none of
+ * this library's kernels that do write activations). */
+moe_status moe_act_quant_tokens(const void* x, int x_dtype, int64_t T, int64_t cols, int64_t ldx, int k,
+                                const int32_t* token_pos, const int32_t* row_group, const double* smooth,
+                                const double* smooth_recip, const float* smooth_recip_f32, int bits, int symmetric,
+                                uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                                int32_t* rowsum, moe_stream_t stream);
 
 /* out[i] = RN(1 / s[i]) (float64) and optionally out_f32[i] = RN32(out[i]);
  * feed smooth_recip / smooth_recip_f32. */

@@ -27,6 +27,9 @@ TUNE_K1_SMALL_ROWS = 1
 TUNE_ROUTER_CLUSTER_TILES = 2
 TUNE_FUSED_QUANT = 3
 TUNE_FUSED_COMBINE = 4
+TUNE_K1_TOKENS = 5
+TUNE_GPTQ_LANES = 6
+TUNE_BAND_MB = 7
 ORDER_MAX_ABS, ORDER_SUM_SQUARES = 1, 2
 
 _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double
@@ -41,6 +44,8 @@ _SIGS = {
     "moe_act_quant_workspace": (_I64, [_I64, _I64, _I]),
     "moe_act_quant": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _I64, _P, _P,
                            _P, _P, _P, _P, _I64, _P]),
+    "moe_act_quant_tokens": (_I, [_P, _I, _I64, _I64, _I64, _I, _P, _P, _P, _P, _P, _I, _I, _P, _I64, _P, _P, _P,
+                                  _P, _P]),
     "moe_reciprocal_f64": (_I, [_P, _I64, _P, _P, _P]),
     "moe_dequantize": (_I, [_P, _I64, _I64, _I64, _P, _P, _I, _P, _P]),
     "moe_apply_smoothing": (_I, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),

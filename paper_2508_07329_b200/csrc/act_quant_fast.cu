@@ -298,6 +298,169 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
 }
 
+// ── token-major variant for the MoE dispatch (K1 on x) ─────────────────────
+// The MoE layer quantizes each token once per selected expert (top-k rows,
+// each with its expert's smoothing). Row-major K1 over the permuted rows
+// reads a token's x row k times from unrelated warps (expert-sorted order),
+// so the second read usually misses L2 (measured: 222 MB of DRAM reads for
+// 134 MB of x). Here one warp owns a token: its x row is loaded once into
+// registers (NV 16-byte vectors per lane, rows up to 256 * NV bf16), and
+// for each of the token's k rows (output row token_pos[t, j], smoothing
+// group group[row]) the float32 extremes, the speculative exact extremes
+// and the packed encode run from those registers. Per-row arithmetic and
+// fallbacks are k1_row_warp's, so the codes are identical.
+// (NV = 16 holds 64 registers of x per lane: 12 warps per CTA leave it 168
+// registers, no spills; 16 warps capped it at 128 and spilled)
+template <int NV>
+constexpr int tok_warps() { return NV > 8 ? 12 : 16; }
+
+template <int NV, bool GEN>
+__device__ __forceinline__ int encode_regs(const uint4 (&u)[NV], const uint4* __restrict__ src,
+                                           const float* __restrict__ tab, const double* srow, const double* rrow,
+                                           int nvec, int lane, const FastRow& f, uint2* __restrict__ dst,
+                                           uint32_t* cnt) {
+  int sum = 0;
+  uint32_t slow = 0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nvec) {
+      float xs[8];
+      smooth8(u[i], tab, c, xs);
+      bool sl;
+      const uint2 out = fast_core<GEN>(xs, f, sl);
+      if (!sl) {
+        sum += bytesum(out);
+        __stcs(dst + c, out);
+      }
+      slow |= (uint32_t)sl << i;
+    }
+  }
+  while (slow) {   // rare: the generic float32 encode / exact redo, from the (L1-resident) row
+    const int i = __ffs(slow) - 1;
+    slow &= slow - 1;
+    const int c = lane + 32 * i;
+    const uint4 sv = slow_vec8(__ldg(src + c), tab, c, srow, rrow, f);
+    *cnt += sv.z;
+    const uint2 o2 = make_uint2(sv.x, sv.y);
+    sum += bytesum(o2);
+    __stcs(dst + c, o2);
+  }
+  return sum;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(tok_warps<NV>() * 32, 1)
+    act_quant_token_kernel(RowArgs a, const int32_t* __restrict__ token_pos, int k, int64_t T,
+                           const float* __restrict__ rs32_tab, int bits, int sym, uint8_t* codes, int64_t ldc,
+                           double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum) {
+  constexpr int kTokWarps = tok_warps<NV>();
+  const int lane = threadIdx.x & 31;
+  const int nvec = (int)(a.cols / 8);
+  const int64_t warps = (int64_t)gridDim.x * kTokWarps;
+  int64_t t = (int64_t)blockIdx.x * kTokWarps + (threadIdx.x >> 5);
+  uint4 u[NV];
+  auto load_row = [&](int64_t tt) {
+    const uint4* s0 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x) + tt * a.ldx);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + 32 * i;
+      u[i] = c < nvec ? __ldg(s0 + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  // PDL-launched behind the permutation: x is older than the router (whose
+  // completion the permutation kernel waited for before letting this grid
+  // launch), so the first row streams in while the permutation finishes;
+  // token_pos / group are read only after griddep_wait
+  if (t < T) load_row(t);
+  griddep_wait();
+  griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
+  for (; t < T; t += warps) {
+    const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + t * a.ldx;
+    const uint4* src = reinterpret_cast<const uint4*>(row);
+    if (t != (int64_t)blockIdx.x * kTokWarps + (threadIdx.x >> 5)) load_row(t);
+    for (int j = 0; j < k; ++j) {
+      const int64_t r = token_pos[t * k + j];
+      const int64_t gbase = a.group ? (int64_t)a.group[r] * a.sm.cols : 0;
+      const float* tab = rs32_tab + gbase;
+      const double* srow = a.sm.s + gbase;
+      const double* rrow = a.sm.rs + gbase;
+      uint2* dst = reinterpret_cast<uint2*>(out_row_ptr(a, codes, ldc, r));
+      // pass A from registers: float32 extremes and the vector holding them
+      float tmax = -FLT_MAX, tmin = FLT_MAX;
+      int vM = 0, vm = 0;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nvec) {
+          float xs[8];
+          smooth8(u[i], tab, c, xs);
+          const float vmax = max8(xs), vmin = min8(xs);
+          const bool um = vmax > tmax, un = vmin < tmin;
+          tmax = um ? vmax : tmax;
+          vM = um ? c : vM;
+          tmin = un ? vmin : tmin;
+          vm = un ? c : vm;
+        }
+      }
+      int64_t cM = vM, cm = vm;
+      warp_argmax(tmax, cM);
+      warp_argmin(tmin, cm);
+      auto locate = [&](int64_t vc, float val) -> int64_t {
+        float xs[8];
+        smooth8(__ldg(src + vc), tab, vc, xs);
+        int e0 = 0;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) e0 = xs[e] == val ? e : e0;
+        return vc * 8 + e0;
+      };
+      const RowExt rec{tmax, tmin, locate(cM, tmax), locate(cm, tmin)};
+      const bool exact_all = !(isfinite(rec.M) && isfinite(rec.m));
+      bool spec = !exact_all;
+      double mn = DBL_MAX, mx = -DBL_MAX;
+      if (spec) {
+        mx = exact_at(row, tab, srow, rrow, rec.cM, rec.M, spec);
+        mn = exact_at(row, tab, srow, rrow, rec.cm, rec.m, spec);
+      }
+      const float lb_max = spec ? rec.M - err_bound(rec.M) : -FLT_MAX;
+      const float ub_min = spec ? rec.m + err_bound(rec.m) : FLT_MAX;
+      AffineParams p{};
+      int sum = 0;
+      bool done = false;
+      if (spec) {
+        p = affine_params(mn, mx, bits, sym);
+        FastRow f;
+        const int mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
+        if (mode) {
+          uint32_t cnt = 0;
+          sum = mode == 1 ? encode_regs<NV, false>(u, src, tab, srow, rrow, nvec, lane, f, dst, &cnt)
+                          : encode_regs<NV, true>(u, src, tab, srow, rrow, nvec, lane, f, dst, &cnt);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+          }
+          done = cnt == f.expect;
+        }
+      }
+      if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
+      if (lane == 0) {
+        if (a.ep.codes_tab) {
+          const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
+          a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
+              make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
+        } else {
+          if (rowsum) rowsum[r] = sum;
+          scale[r] = p.scale;
+          if (scale_f32) scale_f32[r] = (float)p.scale;
+          zp[r] = p.zp;
+        }
+      }
+    }
+  }
+  if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
+}
+
 // ── CTA-per-row variant for small row counts ───────────────────────────────
 // Decode-size batches have a few dozen rows: one warp per row leaves most
 // SMs idle and runs each row as one long dependent chain (~25 us for 32
@@ -579,6 +742,25 @@ bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sy
                            cudaError_t* err) {
   if (!eligible(a, rs32, codes, ldc)) return false;
   *err = launch_warp<false>(a, rs32, nullptr, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+  return true;
+}
+
+bool launch_act_quant_tokens(const RowArgs& a, const int32_t* token_pos, int k, int64_t T, const float* rs32,
+                             int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                             int32_t* zp, int32_t* rowsum, cudaStream_t s, cudaError_t* err) {
+  if (!eligible(a, rs32, codes, ldc) || a.gather || k < 1 || a.cols > 256 * 16) return false;
+  const int nvec32 = (int)((a.cols / 8 + 31) / 32);
+  // one warp per token; one CTA per SM (grid-stride over the tokens)
+  auto go = [&](auto kern, int warps) {
+    const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((T + warps - 1) / warps, (int64_t)num_sms()));
+    *err = launch_pdl(kern, dim3((unsigned)ctas), dim3(warps * 32), 0, s, a, token_pos, k, T, rs32, bits, sym,
+                      codes, ldc, scale, scale_f32, zp, rowsum);
+  };
+  if (nvec32 <= 4) go(act_quant_token_kernel<4>, tok_warps<4>());
+  else if (nvec32 <= 8) go(act_quant_token_kernel<8>, tok_warps<8>());
+  else go(act_quant_token_kernel<16>, tok_warps<16>());
+  count_launch();
+  if (*err == cudaSuccess) *err = cudaGetLastError();
   return true;
 }
 

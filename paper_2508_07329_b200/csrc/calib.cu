@@ -107,8 +107,8 @@ constexpr int kGT = 32;      // columns per tile
 #endif
 constexpr int kGStage = MOE_GPTQ_STAGE;   // U rows per shared-memory stage (double-buffered)
 
-// Each row is owned by kGP adjacent lanes, lane p holding the tile columns
-// j = p, p + kGP, ... (kGT / kGP of them): the left-looking updates of a tile
+// Each row is owned by kGP adjacent lanes, lane p holding the contiguous
+// tile columns [p * kGQ, (p + 1) * kGQ): the left-looking updates of a tile
 // are split kGP ways, and in the in-tile sequential part the owner of column
 // i computes its code and error and shuffles the error to the row's other
 // lanes. Every element still receives its updates one at a time, separate
@@ -323,7 +323,10 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
   MOE_REQUIRE(err_ws_bytes >= moe_gptq_workspace(R, n), "gptq_columns: workspace too small");
   // few rows (e.g. W2 of an expert, 4096): a whole warp per row so the SMs
   // have enough independent rows; many rows: 8 lanes per row, 4 columns each
-  static const int forced = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
+  static const int env_p = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
+  const int64_t knob = tune_value(MOE_TUNE_GPTQ_LANES);
+  const int forced = knob ? (int)knob : env_p;
+  MOE_REQUIRE(forced == 0 || forced == 8 || forced == 32, "gptq_columns: lanes per row must be 8 or 32");
   const int P = forced ? forced : (R <= 8192 ? 32 : 8);
   const unsigned blocks = (unsigned)((R + kGThreads / P - 1) / (kGThreads / P));
   auto launch = [&](auto kern, int rows_cta) -> cudaError_t {

@@ -20,6 +20,7 @@ namespace moe {
 void set_error(const std::string& msg);
 void count_launch();  // every kernel launch of the library is counted (moe_launch_count)
 int64_t k1_small_rows();         // MOE_TUNE_K1_SMALL_ROWS
+int64_t tune_value(int key);     // any MOE_TUNE_* knob
 int64_t router_cluster_tiles();  // MOE_TUNE_ROUTER_CLUSTER_TILES
 
 #define MOE_REQUIRE(cond, msg)         \

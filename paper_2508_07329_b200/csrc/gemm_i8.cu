@@ -1031,7 +1031,7 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   const int64_t n_tiles = (N + BN - 1) / BN;
   // raster band: keep ~24 MB of activations L2-resident per band
   {
-    static const int64_t budget = getenv("MOE_B200_BAND_MB") ? atoll(getenv("MOE_B200_BAND_MB")) << 20 : (24LL << 20);
+    const int64_t budget = std::max<int64_t>(1, tune_value(MOE_TUNE_BAND_MB)) << 20;
     p.band = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 20, budget / (TM * std::max<int64_t>(K, 1))));
   }
   // decode sizes (weight-stream bound): L2-prefetch the first 640 KB of each

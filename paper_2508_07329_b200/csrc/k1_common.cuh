@@ -103,6 +103,13 @@ bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sy
                            double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum, cudaStream_t s,
                            cudaError_t* err);
 
+// Token-major K1 for the MoE dispatch: output row token_pos[t * k + j] (j <
+// k) = token t of x smoothed with group[row]; x read once per token. False
+// if not eligible (bf16, cols % 8 == 0, cols <= 4096, divide smoothing).
+bool launch_act_quant_tokens(const RowArgs& a, const int32_t* token_pos, int k, int64_t T, const float* rs32,
+                             int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
+                             int32_t* zp, int32_t* rowsum, cudaStream_t s, cudaError_t* err);
+
 // K1 for rows whose float32 (min, max) records of the smoothed values were
 // produced upstream (grouped GEMM SwiGLU epilogue) as (order key << 32 | col)
 // `ext` [rows, 2]: a single speculative encode pass. False if not eligible.

@@ -9,44 +9,36 @@ static std::atomic<unsigned long long> g_launches{0};
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-static std::atomic<int64_t> g_k1_small_rows{[] {
-  const char* env = getenv("MOE_B200_K1_SMALL");
-  return env ? (int64_t)atoll(env) : (int64_t)256;
-}()};
-int64_t k1_small_rows() { return g_k1_small_rows.load(std::memory_order_relaxed); }
-static std::atomic<int64_t> g_router_cluster_tiles{64};   // tools/router_bench.py crossover
-int64_t router_cluster_tiles() { return g_router_cluster_tiles.load(std::memory_order_relaxed); }
-static std::atomic<int64_t> g_fused_quant{0};
-static std::atomic<int64_t> g_fused_combine{1};
+// process-wide knobs (MOE_TUNE_*), indexed by key
+static std::atomic<int64_t> g_tune[MOE_TUNE_COUNT] = {
+    {0},
+    {[] {
+      const char* env = getenv("MOE_B200_K1_SMALL");
+      return env ? (int64_t)atoll(env) : (int64_t)256;
+    }()},
+    {64},   // router cluster tiles: tools/router_bench.py crossover
+    {0},    // fused K1 in GEMM2 (off)
+    {1},    // fused top-2 combine (on)
+    {1},    // token-major K1 on x (on)
+    {0},    // GPTQ lanes per row (0: automatic)
+    {[] {
+      const char* env = getenv("MOE_B200_BAND_MB");
+      return env ? (int64_t)atoll(env) : (int64_t)24;
+    }()},   // grouped-GEMM raster band budget (MB of A rows kept L2-resident)
+};
+int64_t tune_value(int key) { return g_tune[key].load(std::memory_order_relaxed); }
+int64_t k1_small_rows() { return tune_value(MOE_TUNE_K1_SMALL_ROWS); }
+int64_t router_cluster_tiles() { return tune_value(MOE_TUNE_ROUTER_CLUSTER_TILES); }
 }  // namespace moe
 
 extern "C" moe_status moe_tune(int key, int64_t value, int64_t* old) {
-  switch (key) {
-    case MOE_TUNE_K1_SMALL_ROWS: {
-      const int64_t prev = value < 0 ? moe::g_k1_small_rows.load() : moe::g_k1_small_rows.exchange(value);
-      if (old) *old = prev;
-      return MOE_OK;
-    }
-    case MOE_TUNE_ROUTER_CLUSTER_TILES: {
-      const int64_t prev =
-          value < 0 ? moe::g_router_cluster_tiles.load() : moe::g_router_cluster_tiles.exchange(value);
-      if (old) *old = prev;
-      return MOE_OK;
-    }
-    case MOE_TUNE_FUSED_QUANT: {
-      const int64_t prev = value < 0 ? moe::g_fused_quant.load() : moe::g_fused_quant.exchange(value);
-      if (old) *old = prev;
-      return MOE_OK;
-    }
-    case MOE_TUNE_FUSED_COMBINE: {
-      const int64_t prev = value < 0 ? moe::g_fused_combine.load() : moe::g_fused_combine.exchange(value);
-      if (old) *old = prev;
-      return MOE_OK;
-    }
-    default:
-      moe::set_error("moe_tune: unknown key " + std::to_string(key));
-      return MOE_EINVAL;
+  if (key <= 0 || key >= MOE_TUNE_COUNT) {
+    moe::set_error("moe_tune: unknown key " + std::to_string(key));
+    return MOE_EINVAL;
   }
+  const int64_t prev = value < 0 ? moe::g_tune[key].load() : moe::g_tune[key].exchange(value);
+  if (old) *old = prev;
+  return MOE_OK;
 }
 
 extern "C" const char* moe_last_error(void) { return moe::g_last_error.c_str(); }

@@ -214,6 +214,26 @@ extern "C" moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, in
   return MOE_OK;
 }
 
+extern "C" moe_status moe_act_quant_tokens(const void* x, int x_dtype, int64_t T, int64_t cols, int64_t ldx, int k,
+                                           const int32_t* token_pos, const int32_t* row_group, const double* smooth,
+                                           const double* smooth_recip, const float* smooth_recip_f32, int bits,
+                                           int symmetric, uint8_t* codes, int64_t ldc, double* scale,
+                                           float* scale_f32, int32_t* zp, int32_t* rowsum, moe_stream_t stream) {
+  MOE_REQUIRE(x && token_pos && smooth && smooth_recip && smooth_recip_f32 && codes && scale && zp,
+              "act_quant_tokens: null pointer");
+  MOE_REQUIRE(T >= 1 && k >= 1 && cols >= 1 && ldx >= cols && ldc >= cols, "act_quant_tokens: bad shape");
+  MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
+  const RowArgs a{x, x_dtype, T * k, cols, ldx, nullptr, row_group,
+                  SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, cols}};
+  cudaError_t err = cudaSuccess;
+  MOE_REQUIRE(launch_act_quant_tokens(a, token_pos, k, T, smooth_recip_f32, bits, symmetric, codes, ldc, scale,
+                                      scale_f32, zp, rowsum, as_stream(stream), &err),
+              "act_quant_tokens: needs bf16 x with cols % 8 == 0, cols <= 4096, 16-byte aligned rows");
+  MOE_CUDA_TRY(err);
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
 extern "C" moe_status moe_reciprocal_f64(const double* sv, int64_t n, double* out, float* out_f32,
                                          moe_stream_t stream) {
   MOE_REQUIRE(sv && out && n >= 1, "reciprocal: bad arguments");

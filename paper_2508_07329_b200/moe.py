@@ -121,9 +121,16 @@ class MoELayer:
         return logits, idx, w
 
     def forward(self, x: torch.Tensor, out_dtype=None, y_dtype=None, return_aux: bool = False, stats=None,
-                timer=None, out: torch.Tensor | None = None):
+                timer=None, out: torch.Tensor | None = None, h_dtype=torch.bfloat16):
         """x [T, d] (bf16) on device -> [T, d]. ``timer`` (optional) gets a
-        ``mark(stage)`` call after every kernel stage (CUDA events)."""
+        ``mark(stage)`` call after every kernel stage (CUDA events).
+
+        ``h_dtype=torch.float32`` is the precise mode: the SwiGLU output h is
+        stored in float32 (not bf16) before K1 re-quantizes it, so h's codes
+        follow the float64 oracle's except where float32 SwiGLU arithmetic
+        lands within ~1e-6 of a rounding boundary (measured flip rate in
+        DESIGN.md); K1 on h then takes the exact kernel and GEMM2 / combine
+        run in float32. The default bf16 h is the serving path."""
         if x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"expected input [T, {self.d}], got {tuple(x.shape)}")
         out_dtype = out_dtype or self.out_dtype
@@ -140,21 +147,30 @@ class MoELayer:
             stats.record(idx)
         perm = ops.route_permute(idx, w, self.E)
         mark("permute")
-        a1 = ops.act_quant(x, smooth=self.s13, smooth_recip=self.s13_recip, smooth_recip_f32=self.s13_recip32,
-                           row_group=perm["row_expert"],
-                           gather=perm["src_token"], rows=T * self.k)
+        if ops.act_quant_tokens_ok(x) and L.tune(L.TUNE_K1_TOKENS) > 0 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS):
+            # token-major K1: each token's x row read once for its k expert rows
+            a1 = ops.act_quant_tokens(x, perm["token_pos"], perm["row_expert"], smooth=self.s13,
+                                      smooth_recip=self.s13_recip, smooth_recip_f32=self.s13_recip32)
+        else:
+            a1 = ops.act_quant(x, smooth=self.s13, smooth_recip=self.s13_recip, smooth_recip_f32=self.s13_recip32,
+                               row_group=perm["row_expert"], gather=perm["src_token"], rows=T * self.k)
         mark("quant_x")
         # the SwiGLU epilogue also emits each h row's (value, column) records
         # of the float32 min/max of h * RN32(1/s2), so the second K1 streams h once
         # (decode-size batches go through K1's CTA-per-row kernel, whose own
         # extreme pass is cheaper than initialising and filling the records)
-        fuse = self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS)
+        precise = h_dtype == torch.float32
+        if not precise and h_dtype != torch.bfloat16:
+            raise ValueError("h_dtype must be torch.bfloat16 or torch.float32")
+        if precise and y_dtype != torch.float32:
+            y_dtype = torch.float32
+        fuse = (not precise and self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS))
         ext = torch.empty((T * self.k, 2), dtype=torch.int64, device=x.device) if fuse else None
-        h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16,
+        h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=h_dtype,
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,
                           next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_ext=ext)
         mark("gemm13_swiglu")
-        if fuse and self.F % 8 == 0 and L.tune(L.TUNE_FUSED_QUANT) > 0:
+        if fuse and self.F % 8 == 0 and L.tune(L.TUNE_FUSED_QUANT) > 0 and y_dtype == torch.bfloat16:
             # K1 of h runs inside the second grouped GEMM (its epilogue warps
             # quantize rows while the tensor cores work; bit-identical)
             mark("quant_h")

@@ -105,6 +105,34 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
             "granularity": granularity, "bits": bits}
 
 
+def act_quant_tokens_ok(x: torch.Tensor) -> bool:
+    """Whether moe_act_quant_tokens takes x (bf16, d % 8 == 0, d <= 4096, aligned rows)."""
+    return (x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1 and x.shape[1] % 8 == 0
+            and x.shape[1] <= 4096 and x.stride(0) % 8 == 0 and x.data_ptr() % 16 == 0)
+
+
+def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.Tensor, *, smooth: torch.Tensor,
+                     smooth_recip: torch.Tensor, smooth_recip_f32: torch.Tensor, bits: int = 8,
+                     symmetric: bool = False) -> dict:
+    """Token-major K1 for the MoE dispatch: row token_pos[t, j] = x[t] /
+    smooth[row_group[row]], per-token RTN; x is read once per token. Same
+    result as act_quant(x, gather=src_token, row_group=row_group, ...)."""
+    T, cols = x.shape
+    k = token_pos.numel() // max(T, 1)
+    rows = T * k
+    dev = x.device
+    codes = torch.empty((rows, cols), dtype=torch.uint8, device=dev)
+    scale = torch.empty(rows, dtype=torch.float64, device=dev)
+    scale_f32 = torch.empty(rows, dtype=torch.float32, device=dev)
+    zp = torch.empty(rows, dtype=torch.int32, device=dev)
+    rs = torch.empty(rows, dtype=torch.int32, device=dev)
+    L.call("moe_act_quant_tokens", L.ptr(x), _dt(x), T, cols, x.stride(0), k, L.ptr(token_pos.contiguous()),
+           L.ptr(row_group), L.ptr(smooth), L.ptr(smooth_recip), L.ptr(smooth_recip_f32), bits, int(bool(symmetric)),
+           L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp), L.ptr(rs), _s())
+    return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
+            "granularity": "per_token", "bits": bits}
+
+
 def dequantize(codes: torch.Tensor, scale: torch.Tensor, zp: torch.Tensor, granularity: str) -> torch.Tensor:
     codes = _rowmajor(codes, "codes")
     out = torch.empty(codes.shape, dtype=torch.float64, device=codes.device)

@@ -141,6 +141,42 @@ def test_act_quant_edge_values(cuda, k1_kernel):
                 np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
 
 
+@pytest.mark.parametrize("T,d,k,G", [(1, 8, 1, 1), (300, 512, 2, 8), (257, 1024, 4, 16), (1000, 4096, 2, 8),
+                                      (70, 2056, 3, 5), (5, 4096, 8, 8)])
+def test_act_quant_tokens_bitexact(cuda, T, d, k, G):
+    """Token-major K1 (x read once per token, all k expert rows encoded from
+    registers) == the oracle on the gathered rows, bit for bit, with
+    per-row smoothing groups, ragged d (not a multiple of 256), tie rows,
+    constant / zero / one-sided / tiny / huge rows."""
+    rng = np.random.default_rng(T * 7 + d + k)
+    x = _acts(rng, T, d)
+    special = [np.zeros(d), np.full(d, 5.0), np.abs(x[0]) + 1.0, -np.abs(x[0]),
+               rng.normal(size=d) * 1e-30, rng.normal(size=d) * 3e4,
+               np.r_[0.0, 255 / 8, (np.arange(d - 2) % 255 + 0.5) / 8]]
+    for i, row in enumerate(special[: T]):
+        x[i] = bf16_round(np.asarray(row, np.float32))
+    s = _smooth(rng, G, d)
+    s[0] = 1.0                                     # exact-tie rows survive group 0
+    # token_pos: a random permutation of the T*k rows; groups per row
+    pos = rng.permutation(T * k).astype(np.int32).reshape(T, k)
+    grp = rng.integers(0, G, size=T * k).astype(np.int32)
+    grp[pos[: len(special), 0]] = 0
+    sd = torch.from_numpy(s).to(cuda)
+    rec, rec32 = ops.reciprocal(sd, with_f32=True)
+    xd = torch.from_numpy(x).to(cuda).bfloat16()
+    assert ops.act_quant_tokens_ok(xd)
+    r = ops.act_quant_tokens(xd, torch.from_numpy(pos).to(cuda), torch.from_numpy(grp).to(cuda), smooth=sd,
+                             smooth_recip=rec, smooth_recip_f32=rec32)
+    src = np.empty(T * k, np.int64)
+    src[pos.ravel()] = np.repeat(np.arange(T), k)
+    codes, sc, zp, rs = M.quantize_rows_grouped(x.astype(np.float64)[src], grp, s)
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), sc)
+    np.testing.assert_array_equal(r["scale_f32"].cpu().numpy(), sc.astype(np.float32))
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+    np.testing.assert_array_equal(r["rowsum"].cpu().numpy(), rs)
+
+
 def _ext_key(v32, col):
     """(order-preserving key of a float32 << 32) | column, as int64 bits."""
     i = np.asarray(v32, np.float32).view(np.int32).astype(np.int64)

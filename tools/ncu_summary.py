@@ -23,6 +23,9 @@ def short(name: str) -> str:
     return n[:70]
 
 
+TOKENS = 16384   # bench --tokens of the captured command (argv[4] overrides)
+
+
 def launches(path: str, tag: str):
     lines = [ln for ln in open(path) if ln.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
@@ -48,7 +51,7 @@ def launches(path: str, tag: str):
                    f"{k.get('dram__bytes_read.sum', 0) / 1e6:.1f} | {k.get('dram__bytes_write.sum', 0) / 1e6:.1f} |")
     (PROF / f"launches_{tag}.md").write_text("\n".join(out) + "\n")
     gem = [k for k in step if "gemm_i8_tc" in k["name"]]
-    traffic = {"tag": tag, "grouped_gemm_bytes_per_step": sum(k.get("dram__bytes_read.sum", 0) +
+    traffic = {"tag": tag, "tokens": TOKENS, "grouped_gemm_bytes_per_step": sum(k.get("dram__bytes_read.sum", 0) +
                                                                 k.get("dram__bytes_write.sum", 0) for k in gem),
                "per_kernel": [{"kernel": short(k["name"]), "us": k["gpu__time_duration.sum"] / 1e3,
                                "dram_read": k.get("dram__bytes_read.sum", 0),
@@ -96,4 +99,6 @@ def full(path: str, tag: str):
 
 if __name__ == "__main__":
     mode, path, tag = sys.argv[1:4]
+    if len(sys.argv) > 4:
+        TOKENS = int(sys.argv[4])
     (launches if mode == "launches" else full)(path, tag)
