@@ -51,6 +51,12 @@ def _silu(g: torch.Tensor) -> torch.Tensor:
     return g / (1.0 + torch.exp(-g))
 
 
+def swiglu_calib_acts(xe: torch.Tensor, w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """The float64 SwiGLU activation h = silu(x W1^T) * (x W3^T) [tokens, F]
+    that calibrates W2 (oracle/calib_moe_ref.swiglu_acts)."""
+    return _silu(xe @ w1.T) * (xe @ w3.T)
+
+
 def _route_calib(gate_weight, x_calib, top_k, gate_bias, E):
     x = x_calib.cuda()
     if x.dim() != 2:
@@ -77,7 +83,7 @@ def _calibrate_expert(e: int, ex: dict, xf: torch.Tensor, idx: torch.Tensor, cfg
     # stacked [W1; W3] with one smoothing vector (shared input)
     r13 = quantize_layer(torch.cat([w1, w3], 0), xe.T.contiguous(), cfg, grid_steps, ordering)
     # W2 sees the expert's float SwiGLU activation of the same tokens
-    h = _silu(xe @ w1.T) * (xe @ w3.T)
+    h = swiglu_calib_acts(xe, w1, w3)
     r2 = quantize_layer(w2, h.T.contiguous(), cfg, grid_steps, ordering)
     q13 = r13.quantized
     codes13, sc13, zp13 = (np.asarray(q13.codes), np.asarray(q13.scales), np.asarray(q13.zero_points))

@@ -96,10 +96,10 @@ __global__ void hessian_finalize_kernel(double* H, int64_t n, double damping, co
 }
 
 // ── K8: left-looking strict-order GPTQ column loop ─────────────────────────
-// One thread per weight row. For column tile [J, J+32): start from the
-// original weights, apply the updates of columns i < J in ascending i
-// (err_i read from the workspace, U[i, J:J+32] broadcast from smem), then
-// run the in-tile sequential loop. Per element the subtractions happen in
+// Each weight row is owned by kGP lanes (below). For column tile [J, J+32):
+// start from the original weights, apply the updates of columns i < J in
+// ascending i (err_i read from the workspace, U[i, J:J+32] staged in shared
+// memory), then run the in-tile sequential loop. Per element the subtractions happen in
 // exactly the reference's order, so codes are bit-identical.
 constexpr int kGT = 32;      // columns per tile
 #ifndef MOE_GPTQ_STAGE

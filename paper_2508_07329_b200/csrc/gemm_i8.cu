@@ -447,6 +447,7 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -458,6 +459,7 @@ __device__ __forceinline__ void fq_wait_rows(const GemmArgs& p, int r0, int r1) 
     const int need = min(32, p.M - b * 32);
     while (ld_relaxed_s32(p.q_blk + b) < need) __nanosleep(64);
   }
+  fence_acq_rel_gpu();           // acquire: order the polled flags before the TMA reads
   fence_proxy_async_global();
 }
 
@@ -477,6 +479,7 @@ __device__ __forceinline__ void comb_store(const GemmArgs& p, int row, int n_lo,
     red_release_add(ctr, 2);
   } else {
     while (ld_relaxed_s32(ctr) < 4) __nanosleep(32);
+    fence_acq_rel_gpu();         // acquire: the partner's row is read after its release
     const int r0 = p.comb_pos[2 * t], r1 = p.comb_pos[2 * t + 1];
     const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.out) +
                                                       (int64_t)(r0 == row ? r1 : r0) * p.ldo + n_lo);

@@ -282,6 +282,7 @@ __global__ void router_topk_kernel(const float* logits, int64_t T, int E, int k,
 // ── stable counting sort ───────────────────────────────────────────────────
 constexpr int kPermThreads = 256;
 constexpr int kPermChunk = 1024;  // (token, slot) pairs per block
+constexpr int kPermScanBlocks = 64;  // above this many blocks: separate scan launch
 
 __global__ void permute_count_kernel(const int32_t* idx, int64_t n, int E, int32_t* block_counts) {
   __shared__ int cnt[kMaxE];
@@ -329,13 +330,46 @@ __device__ __forceinline__ void permute_scatter_range(const int32_t* idx, const 
   }
 }
 
-// Every block derives its own bases from the per-block counts (nblocks x E
-// ints, tiny): expert offset = sum of earlier experts' totals, plus the
-// counts of earlier blocks; block 0 also writes the offsets. (No separate
-// scan launch.)
+// Large batches: one block per expert turns the per-block counts into
+// exclusive per-block bases (bases[b * E + e]) and the expert total
+// (bases[nblocks * E + e]), so the scatter blocks read O(E) values each
+// instead of re-reading the whole nblocks x E table.
+__global__ void __launch_bounds__(kPermThreads) permute_scan_kernel(const int32_t* block_counts, int nblocks, int E,
+                                                                    int32_t* bases) {
+  __shared__ int wsum[kPermThreads / 32];
+  __shared__ int carry;
+  const int e = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nblocks; b0 += kPermThreads) {
+    const int b = b0 + threadIdx.x;
+    const int c = b < nblocks ? block_counts[(int64_t)b * E + e] : 0;
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    int before = carry;
+    for (int w2 = 0; w2 < warp; ++w2) before += wsum[w2];
+    if (b < nblocks) bases[(int64_t)b * E + e] = before + v - c;
+    __syncthreads();
+    if (threadIdx.x == kPermThreads - 1) carry = before + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bases[(int64_t)nblocks * E + e] = carry;
+}
+
+// Every block derives its own bases: from the scanned table when `bases` is
+// given, else from the per-block counts (nblocks x E ints, fine for small
+// nblocks): expert offset = sum of earlier experts' totals, plus the counts
+// of earlier blocks; block 0 also writes the offsets.
 __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t* idx, const float* topk_w,
                                                                        int64_t n, int k, int E,
                                                                        const int32_t* block_counts, int nblocks,
+                                                                       const int32_t* bases,
                                                                        int32_t* offsets, int32_t* src_token,
                                                                        int32_t* row_expert, float* row_weight,
                                                                        int32_t* token_pos) {
@@ -343,6 +377,11 @@ __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int
   __shared__ int tot[kMaxE];
   __shared__ int wcnt[kPermThreads / 32][kMaxE];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    if (bases) {
+      tot[e] = bases[(int64_t)nblocks * E + e];
+      run[e] = bases[(int64_t)blockIdx.x * E + e];
+      continue;
+    }
     int t = 0, before = 0;
     for (int b = 0; b < nblocks; ++b) {
       const int c = block_counts[(int64_t)b * E + e];
@@ -557,7 +596,7 @@ extern "C" moe_status moe_router_topk(const float* logits, int64_t T, int E, int
 
 extern "C" int64_t moe_route_permute_workspace(int64_t T, int k, int E) {
   const int64_t nb = (T * k + kPermChunk - 1) / kPermChunk;
-  return 2 * nb * E * (int64_t)sizeof(int32_t);
+  return (2 * nb + 1) * E * (int64_t)sizeof(int32_t);
 }
 
 extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* topk_w, int64_t T, int k, int E,
@@ -580,7 +619,14 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
     return MOE_OK;
   }
   permute_count_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, n, E, counts); ::moe::count_launch();
-  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, counts, nb, expert_offsets,
+  // beyond kPermScanBlocks blocks the per-block rescan (O(nb^2 E) reads) would
+  // dominate: scan once in a separate launch
+  int32_t* bases = nullptr;
+  if (nb > kPermScanBlocks) {
+    bases = counts + (int64_t)nb * E;
+    permute_scan_kernel<<<E, kPermThreads, 0, s>>>(counts, nb, E, bases); ::moe::count_launch();
+  }
+  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, counts, nb, bases, expert_offsets,
                                                      src_token, row_expert, row_weight, token_pos);
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();

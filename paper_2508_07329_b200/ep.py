@@ -290,7 +290,25 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         off = self.be.to_host(perm["offsets"]).astype(np.int64)
         return DispatchState(x.shape[0], perm, [x], np.diff(off).reshape(W, E))
 
+    def check_capacity(self, C: np.ndarray, rows_home: int) -> None:
+        """Every rank holds the global C, so every rank raises together
+        (before any peer write) if some receive buffer or this rank's yhome
+        would overflow. Receive buffers are allocated with the same capacity
+        on every rank (symmetric memory)."""
+        recv = C.sum(axis=(0, 2))
+        cap = self.bufs.codes.shape[0]
+        if recv.max(initial=0) > cap:
+            r = int(np.argmax(recv))
+            raise RuntimeError(f"expert-parallel receive buffer overflow: rank {r} would receive {int(recv[r])} "
+                               f"rows, capacity {cap} (PeerBuffers cap)")
+        home = C.sum(axis=(1, 2))           # rows each rank routes = its yhome rows
+        caph = self.bufs.yhome.shape[0]
+        if max(int(home.max(initial=0)), rows_home) > caph:
+            r = int(np.argmax(home))
+            raise RuntimeError(f"expert-parallel yhome overflow: rank {r} routes {int(home[r])} rows, capacity {caph}")
+
     def peer_send(self, st: DispatchState, C: np.ndarray):
+        self.check_capacity(C, st.perm["src_token"].numel())
         rank_of, base = peer_send_layout(C, self.rank, self.pl)
         n = st.perm["src_token"].numel()
         if n == 0:

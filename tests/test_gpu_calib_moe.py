@@ -112,3 +112,63 @@ def test_calibrate_moe_layer_distributed_gloo_two_ranks(tmp_path):
     outs = [p.communicate(timeout=600) for p in procs]
     for o, e in outs:
         assert "EQUAL" in o, o + e[-3000:]
+
+
+def test_calibrate_moe_layer_matches_oracle(cuda):
+    """f1 parity against the oracle restatement (oracle/calib_moe_ref.py,
+    quant.py:437-490 per expert as in PAPER.md:209-285) at a C2-like shape
+    (8 experts, top-2, d=512, ffn=1024, 2048 calibration tokens, full
+    21-point smoothing grid), stage by stage on identical inputs:
+    routing ids from the GPU router's float32 logits; per expert the routed
+    token set, the stacked W1||W3 codes / scales / zero points / smoothing
+    factors / exponent BIT-EXACT; the float SwiGLU activation h within
+    rtol 1e-12 of the oracle's; W2 calibrated on the GPU's h bit-exact; and
+    W2 calibrated on the oracle's own h: same exponent, codes within a
+    tiny flip rate (the float64 sums of h differ in the last bits)."""
+    from oracle import calib_moe_ref as CR
+    from oracle import quant_ref as Q
+    from paper_2508_07329_b200.calib_moe import swiglu_calib_acts
+
+    rng = np.random.default_rng(11)
+    E8, d, ffn, T, k = 8, 512, 1024, 2048, 2
+    experts = [{"w1": rng.normal(size=(ffn, d)) * 0.05, "w3": rng.normal(size=(ffn, d)) * 0.05,
+                "w2": rng.normal(size=(d, ffn)) * 0.03} for _ in range(E8)]
+    wg = (rng.normal(size=(E8, d)) / np.sqrt(d)).astype(np.float32)
+    x = rng.normal(size=(T, d)).astype(np.float32)
+    x[:, rng.choice(d, 6, replace=False)] *= 40.0
+    xd = torch.from_numpy(x).cuda().bfloat16().float()            # bf16-representable tokens
+    layer, rep = calibrate_moe_layer(wg, experts, xd, top_k=k, out_dtype=torch.float32)
+    logits, idx_gpu, _ = ops.router_gate(xd.bfloat16().contiguous(), torch.from_numpy(wg).cuda(), k)
+    xf = xd.double().cpu().numpy()
+    c = Q.cfg(8, False, Q.PER_TOKEN)
+    idx, _, _ = M_router(logits.cpu().numpy(), k)
+    np.testing.assert_array_equal(idx, idx_gpu.cpu().numpy())
+    flips = []
+    for e in range(E8):
+        tok, used_all = CR.expert_tokens(idx, e, 16)
+        assert rep[e].tokens == int((idx == e).any(axis=1).sum()) and rep[e].used_all_tokens == used_all
+        xe = torch.from_numpy(xf[tok]).cuda()
+        h_gpu = swiglu_calib_acts(xe, *(torch.from_numpy(experts[e][n]).cuda() for n in ("w1", "w3")))
+        h_gpu = h_gpu.cpu().numpy()
+        want = CR.calibrate_expert(xf, tok, experts[e], c, 21, "none", h=h_gpu)
+        got = layer.host_experts[e]
+        for n in ("w1", "w3", "w2"):
+            np.testing.assert_array_equal(np.asarray(got[n].codes), want[n][0], err_msg=f"expert {e} {n} codes")
+            np.testing.assert_array_equal(np.asarray(got[n].scales), want[n][1])
+            np.testing.assert_array_equal(np.asarray(got[n].zero_points), want[n][2])
+        np.testing.assert_array_equal(got["s13"], want["s13"])
+        np.testing.assert_array_equal(got["s2"], want["s2"])
+        assert rep[e].exponent13 == want["exponent13"] and rep[e].exponent2 == want["exponent2"]
+        assert rep[e].mse13 == pytest.approx(want["mse13"], rel=1e-9)
+        # the oracle's own float h (numpy float64 GEMMs)
+        h_np = CR.swiglu_acts(xf[tok], experts[e]["w1"], experts[e]["w3"])
+        np.testing.assert_allclose(h_gpu, h_np, rtol=1e-12, atol=1e-13 * np.abs(h_np).max())
+        own = Q.quantize_layer(experts[e]["w2"], h_np.T, c, 21)
+        assert own["exponent"] == want["exponent2"]
+        flips.append(float(np.mean(own["codes"] != want["w2"][0])))
+    assert max(flips) < 1e-4, flips
+
+
+def M_router(logits, k):
+    from oracle import moe_ref as M
+    return M.router_topk(logits, k)

@@ -425,7 +425,7 @@ def test_router_topk_ties(cuda):
     np.testing.assert_allclose(w.cpu().numpy(), 0.5, rtol=1e-7)
 
 
-@pytest.mark.parametrize("T,k,E", [(4096, 2, 8), (1, 2, 8), (5000, 4, 16), (777, 1, 3)])
+@pytest.mark.parametrize("T,k,E", [(4096, 2, 8), (1, 2, 8), (5000, 4, 16), (777, 1, 3), (70000, 2, 8), (20000, 4, 64)])
 def test_route_permute(cuda, T, k, E):
     rng = np.random.default_rng(T + k + E)
     idx = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
@@ -491,4 +491,42 @@ def test_gptq_columns_bitexact_given_u(cuda, R, n, bits, permute):
     got = ops.gptq_columns(torch.from_numpy(w).to(cuda), torch.from_numpy(U).to(cuda),
                            torch.from_numpy(sc).to(cuda), torch.from_numpy(zp).to(cuda), bits,
                            torch.from_numpy(order).to(cuda) if permute else None)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def _gptq_case(rng, R, n, bits, cuda):
+    """W [R, n] and the given U from a real (GPU, float64) damped Hessian
+    inverse factor; the oracle column loop runs on the same U."""
+    x = torch.from_numpy(rng.normal(size=(n, n + 64))).to(cuda)
+    H = 2.0 * x @ x.T
+    H += 0.01 * H.diagonal().mean() * torch.eye(n, device=cuda, dtype=torch.float64)
+    U = torch.linalg.cholesky(torch.cholesky_inverse(torch.linalg.cholesky(H))).T.contiguous()
+    w = rng.normal(size=(R, n)) * 0.02
+    sc, zp = Q.affine(w.min(axis=1), w.max(axis=1), Q.cfg(bits))
+    return w, U, sc, zp
+
+
+@pytest.mark.parametrize("n", [4096, 14336])
+@pytest.mark.parametrize("lanes", [8, 32])
+def test_gptq_columns_bitexact_mixtral_shapes(cuda, n, lanes):
+    """K8 at the Mixtral expert shapes (W1||W3: n = d = 4096; W2: n = ffn =
+    14336) on a 64-row slice (rows are independent, quant.py:423-430), with
+    both lane splits forced: 8 lanes per row (4 contiguous tile columns each,
+    the double2 path used for R > 8192, i.e. the stacked W1||W3) and 32."""
+    rng = np.random.default_rng(n + lanes)
+    w, U, sc, zp = _gptq_case(rng, 64, n, 8, cuda)
+    want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
+    with L.tuned(L.TUNE_GPTQ_LANES, lanes):
+        got = ops.gptq_columns(torch.from_numpy(w).to(cuda), U, torch.from_numpy(sc).to(cuda),
+                               torch.from_numpy(zp).to(cuda), 8)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_gptq_columns_bitexact_many_rows(cuda):
+    """More than 8192 rows: the automatic choice is 8 lanes per row."""
+    rng = np.random.default_rng(9)
+    w, U, sc, zp = _gptq_case(rng, 8200, 96, 8, cuda)
+    want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
+    got = ops.gptq_columns(torch.from_numpy(w).to(cuda), U, torch.from_numpy(sc).to(cuda),
+                           torch.from_numpy(zp).to(cuda), 8)
     np.testing.assert_array_equal(got.cpu().numpy(), want)
