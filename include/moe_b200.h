@@ -159,6 +159,16 @@ moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols,
  * PDL-launched: x must not be written by the immediately preceding kernel
  * of the stream when that kernel triggers its dependents early (none of
  * this library's kernels that do write activations). */
+/* K1 with producer records (row_ext, as moe_act_quant(row_ext=...)) whose
+ * row count lives on the device: rows r < *rows_dev of the capacity
+ * rows_cap are quantized (the expert-parallel receiver, whose row count
+ * comes from the device-side exchange plan). bf16 rows, cols % 8 == 0. */
+moe_status moe_act_quant_given_dev(const void* x, int x_dtype, int64_t rows_cap, const int32_t* rows_dev,
+                                   int64_t cols, int64_t ldx, const double* smooth, const double* smooth_recip,
+                                   const float* smooth_recip_f32, const int32_t* row_group, int bits, int symmetric,
+                                   uint8_t* codes, int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                                   int32_t* rowsum, const unsigned long long* row_ext, moe_stream_t stream);
+
 moe_status moe_act_quant_tokens(const void* x, int x_dtype, int64_t T, int64_t cols, int64_t ldx, int k,
                                 const int32_t* token_pos, const int32_t* row_group, const double* smooth,
                                 const double* smooth_recip, const float* smooth_recip_f32, int bits, int symmetric,
@@ -302,15 +312,16 @@ moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, int64_t ldw, 
  *   of row_bytes bytes (16-byte vectors when aligned).
  * ep_pack_params: params[n, 4] int32 = (scale_f32 bits, zp, rowsum, weight
  *   bits; weight NULL -> 1.0f), the per-row sidecar of dispatched codes.
- * ep_unpack_params: SoA scale_f32/zp/rowsum/weight of params[index[r]]. */
+ * ep_unpack_params: SoA scale_f32/zp/rowsum/weight of params[index[r]] for
+ *   r < n (r < min(n, *n_dev) with a device row count). */
 moe_status moe_route_keys(const int32_t* topk_idx, int64_t n, const int32_t* dest_rank, int E, int32_t* keys,
                           moe_stream_t stream);
 moe_status moe_gather_rows(const void* src, int64_t src_ld_bytes, const int32_t* index, int64_t n,
                            int64_t row_bytes, void* dst, int64_t dst_ld_bytes, moe_stream_t stream);
 moe_status moe_ep_pack_params(const float* scale_f32, const int32_t* zp, const int32_t* rowsum,
                               const float* weight, int64_t n, int32_t* params, moe_stream_t stream);
-moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, float* scale_f32,
-                                int32_t* zp, int32_t* rowsum, float* weight, moe_stream_t stream);
+moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, const int32_t* n_dev,
+                                float* scale_f32, int32_t* zp, int32_t* rowsum, float* weight, moe_stream_t stream);
 
 /* Fused expert-parallel transport (peer memory over NVLink instead of an
  * NCCL all-to-all; buffers from torch symmetric memory):
@@ -320,14 +331,37 @@ moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int
  *   (scale_f32, zp, rowsum, routing weight) into params_tab[...][dst_row[r]].
  * w8a8_gemm_scatter: moe_w8a8_gemm (DEQUANT) whose output row m is stored at
  *   out_tab[out_rank[m]] + out_row[m] * ldo (the combine's home buffers).
+ *   With token_pos (output row of token t's j-th selection, rows = T * k)
+ *   x is read once per token (token-major K1, as moe_act_quant_tokens);
+ *   rows whose dst_rank is negative (refused plan) are skipped.
  * block_map: for rows in contiguous blocks [block_start[b], block_start[b+1]),
- *   out0[i] = val0[b], out1[i] = val1[b] + i - block_start[b] (the
- *   destination rank / row of every dispatched or returned row). */
+ *   out0[i] = val0[b], out1[i] = val1[b] + i - block_start[b], out2[i] =
+ *   val2[b] (optional): the destination rank / row (and local expert) of
+ *   every dispatched or returned row; i < n, or i < min(n, *n_dev) with a
+ *   device row count; valid (optional, device): *valid == 0 makes every
+ *   out0 -1.
+ * ep_peer_plan: the exchange plan of one peer-memory EP forward computed on
+ *   the device (no host round trip): from every rank's route_permute
+ *   offsets over its W*E keys (offsets_all [W, W*E+1], key r*E + e = rows
+ *   for expert e served by rank r, gathered by one all-gather), this
+ *   rank's (me) send bases, receive blocks and grouped-GEMM offsets of its
+ *   G local experts (local, ascending). plan (moe_ep_peer_plan_size ints):
+ *   [valid, R, send_base[W*E], starts[G*W+1], ranks[G*W], homes[G*W],
+ *   group[G*W], goff[G+1]]; valid = 0 (and R = 0) when some rank would
+ *   receive more than cap rows, route more than cap_home rows, or this rank
+ *   receives rows for an expert it does not hold. */
 moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
-                                  const int32_t* gather_rows, const double* smooth, const double* smooth_recip,
+                                  const int32_t* gather_rows, const int32_t* token_pos, int k,
+                                  const double* smooth, const double* smooth_recip,
                                   const float* smooth_recip_f32, const int32_t* row_group, int bits, int symmetric,
                                   void* const* codes_tab, void* const* params_tab, const int32_t* dst_rank,
                                   const int32_t* dst_row, const float* row_weight, int64_t ldc, moe_stream_t stream);
+int64_t moe_ep_peer_plan_size(int W, int E, int G);
+moe_status moe_ep_peer_plan(const int32_t* offsets_all, int W, int E, int me, const int32_t* local, int G,
+                            int64_t cap, int64_t cap_home, int32_t* plan, moe_stream_t stream);
+moe_status moe_block_map(int64_t n, const int32_t* n_dev, int nblocks, const int32_t* block_start,
+                         const int32_t* val0, const int32_t* val1, const int32_t* val2, const int32_t* valid,
+                         int32_t* out0, int32_t* out1, int32_t* out2, moe_stream_t stream);
 moe_status moe_w8a8_gemm_scatter(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
                                  const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
                                  int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,
@@ -379,8 +413,6 @@ moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t
  * d <= 8192, contiguous. */
 moe_status moe_rmsnorm_residual(const void* x, const void* y, void* x_out, void* norm_out, int64_t T, int64_t d,
                                 float eps, moe_stream_t stream);
-moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
-                         const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
-  const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
+  int64_t r_lo, r_hi;
+  cta_row_range(a, rows_per_cta, r_lo, r_hi);
   for (int64_t r = r_lo + warp; r < r_hi; r += WARPS)
     k1_row_warp<GIVEN>(a, r, rs32_tab, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, lane);
   if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   const bool hold = !GIVEN && nchunks <= kRing;
   const int items_per_row = (GIVEN || hold) ? nchunks : 2 * nchunks;
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
-  const int64_t r_lo = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t r_hi = min(a.rows, r_lo + rows_per_cta);
+  int64_t r_lo, r_hi;
+  cta_row_range(a, rows_per_cta, r_lo, r_hi);
   const uint64_t pol = policy_evict_first();
 
   // producer: the warp's item stream (row, chunk) in consumption order
@@ -268,11 +268,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
       };
       if (mode == 1) run(std::false_type{});
       else run(std::true_type{});
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      }
+      warp_sum2(sum, cnt);
       done = cnt == f.expect;
     } else {
       for (int k = 0; k < nchunks; ++k) {   // keep the ring in step
@@ -356,9 +352,19 @@ __global__ void __launch_bounds__(tok_warps<NV>() * 32, 1)
                            double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum) {
   constexpr int kTokWarps = tok_warps<NV>();
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int nvec = (int)(a.cols / 8);
+  const uint32_t row_bytes = (uint32_t)(a.cols * 2);
   const int64_t warps = (int64_t)gridDim.x * kTokWarps;
-  int64_t t = (int64_t)blockIdx.x * kTokWarps + (threadIdx.x >> 5);
+  // the warp's next token row is prefetched into L2 (bulk prefetch, no
+  // shared memory: L1 keeps the experts' float32 reciprocal tables)
+#ifndef MOE_K1_TOK_PREFETCH
+#define MOE_K1_TOK_PREFETCH 1
+#endif
+  auto prefetch = [&](int64_t tt) {
+    if (MOE_K1_TOK_PREFETCH && lane == 0 && tt < T) bulk_prefetch_l2(static_cast<const __nv_bfloat16*>(a.x) + tt * a.ldx, row_bytes);
+  };
+  int64_t t = (int64_t)blockIdx.x * kTokWarps + warp;
   uint4 u[NV];
   auto load_row = [&](int64_t tt) {
     const uint4* s0 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x) + tt * a.ldx);
@@ -373,14 +379,19 @@ __global__ void __launch_bounds__(tok_warps<NV>() * 32, 1)
   // launch), so the first row streams in while the permutation finishes;
   // token_pos / group are read only after griddep_wait
   if (t < T) load_row(t);
+  prefetch(t + warps);
   griddep_wait();
   griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
   for (; t < T; t += warps) {
     const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + t * a.ldx;
     const uint4* src = reinterpret_cast<const uint4*>(row);
-    if (t != (int64_t)blockIdx.x * kTokWarps + (threadIdx.x >> 5)) load_row(t);
+    if (t != (int64_t)blockIdx.x * kTokWarps + warp) {
+      load_row(t);
+      prefetch(t + warps);
+    }
     for (int j = 0; j < k; ++j) {
       const int64_t r = token_pos[t * k + j];
+      if (ep_row_dropped(a, r)) continue;
       const int64_t gbase = a.group ? (int64_t)a.group[r] * a.sm.cols : 0;
       const float* tab = rs32_tab + gbase;
       const double* srow = a.sm.s + gbase;
@@ -435,11 +446,7 @@ __global__ void __launch_bounds__(tok_warps<NV>() * 32, 1)
           uint32_t cnt = 0;
           sum = mode == 1 ? encode_regs<NV, false>(u, src, tab, srow, rrow, nvec, lane, f, dst, &cnt)
                           : encode_regs<NV, true>(u, src, tab, srow, rrow, nvec, lane, f, dst, &cnt);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-          }
+          warp_sum2(sum, cnt);
           done = cnt == f.expect;
         }
       }
@@ -509,6 +516,7 @@ __global__ void __launch_bounds__(kCtaThreads)
   griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r = blockIdx.x;
+  if ((a.rows_dev && r >= *a.rows_dev) || ep_row_dropped(a, r)) return;
   const int64_t nvec = a.cols / 8;
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
   const RowView rv = row_view(a, r);

@@ -40,8 +40,9 @@ __global__ void pack_params_kernel(const float* scale, const int32_t* zp, const 
     params[i] = make_int4(__float_as_int(scale[i]), zp[i], rowsum[i], weight ? __float_as_int(weight[i]) : 0x3F800000);
 }
 
-__global__ void unpack_params_kernel(const int4* params, const int32_t* index, int64_t n, float* scale, int32_t* zp,
-                                     int32_t* rowsum, float* weight) {
+__global__ void unpack_params_kernel(const int4* params, const int32_t* index, int64_t n, const int32_t* n_dev,
+                                     float* scale, int32_t* zp, int32_t* rowsum, float* weight) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int4 p = params[index ? index[i] : i];
     scale[i] = __int_as_float(p.x);
@@ -52,9 +53,15 @@ __global__ void unpack_params_kernel(const int4* params, const int32_t* index, i
 }
 
 // rows grouped in contiguous blocks [start[b], start[b+1]): out0[i] = val0[b],
-// out1[i] = val1[b] + (i - start[b])   (binary search over nb blocks)
-__global__ void block_map_kernel(int64_t n, int nb, const int32_t* start, const int32_t* val0, const int32_t* val1,
-                                 int32_t* out0, int32_t* out1) {
+// out1[i] = val1[b] + (i - start[b]), out2[i] = val2[b] (optional), for
+// i < n (or i < *n_dev when given; binary search over nb blocks). With
+// `valid` given and *valid == 0 every out0 is -1 (a refused exchange plan:
+// consumers skip such rows instead of writing anywhere).
+__global__ void block_map_kernel(int64_t n, const int32_t* n_dev, int nb, const int32_t* start, const int32_t* val0,
+                                 const int32_t* val1, const int32_t* val2, const int32_t* valid, int32_t* out0,
+                                 int32_t* out1, int32_t* out2) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);
+  const bool ok = !valid || *valid != 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = nb;   // last b with start[b] <= i
     while (hi - lo > 1) {
@@ -62,8 +69,84 @@ __global__ void block_map_kernel(int64_t n, int nb, const int32_t* start, const 
       if (start[mid] <= i) lo = mid;
       else hi = mid;
     }
-    out0[i] = val0[lo];
+    out0[i] = ok ? val0[lo] : -1;
     out1[i] = val1[lo] + (int32_t)(i - start[lo]);
+    if (out2) out2[i] = val2[lo];
+  }
+}
+
+// ── device-side exchange plan of the peer-memory EP forward ───────────────
+// offs[s] = rank s's route_permute offsets over its W*E sort keys (key
+// r*E + e = rows of s for expert e served by rank r), gathered from every
+// rank: C[s][r][e] = offs[s][key+1] - offs[s][key]. Every receive buffer is
+// expert-major, sender-minor. Writes (int32):
+//   plan[0]            1 = plan valid, 0 = refused (buffer overflow or rows
+//                      for an expert this rank does not hold)
+//   plan[1]            R = rows this rank receives
+//   send_base[W*E]     first receive-buffer row of this rank's block for key
+//   starts[G*W+1], ranks[G*W], homes[G*W], group[G*W]: receive blocks
+//                      (local expert g ascending, sender s), each block's
+//                      home rank / first home row / local expert index
+//   goff[G+1]          grouped-GEMM offsets of the local experts
+// Single CTA; W*E <= 4096 keys.
+__global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, const int32_t* local, int G,
+                                    int64_t cap, int64_t cap_home, int32_t* plan) {
+  __shared__ int bad;
+  const int KE = W * E, ld = KE + 1;
+  auto C = [&](int s, int r, int e) { return offs[s * ld + r * E + e + 1] - offs[s * ld + r * E + e]; };
+  int32_t* send_base = plan + 2;
+  int32_t* starts = send_base + KE;
+  int32_t* ranks = starts + G * W + 1;
+  int32_t* homes = ranks + G * W;
+  int32_t* group = homes + G * W;
+  int32_t* goff = group + G * W;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  // sender side: one thread per (r, e)
+  for (int key = threadIdx.x; key < KE; key += blockDim.x) {
+    const int r = key / E, e = key % E;
+    int64_t base = 0;
+    for (int e2 = 0; e2 < e; ++e2)
+      for (int s = 0; s < W; ++s) base += C(s, r, e2);
+    for (int s = 0; s < me; ++s) base += C(s, r, e);
+    send_base[key] = (int32_t)base;
+  }
+  // capacity checks (every rank evaluates the same global counts)
+  for (int r = threadIdx.x; r < W; r += blockDim.x) {
+    int64_t recv = 0, home = 0;
+    for (int s = 0; s < W; ++s)
+      for (int e = 0; e < E; ++e) recv += C(s, r, e);
+    home = offs[r * ld + KE] - offs[r * ld];
+    if (recv > cap || home > cap_home) atomicOr(&bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // rows for an expert this rank does not hold
+    for (int e = 0; e < E; ++e) {
+      bool mine = false;
+      for (int g = 0; g < G; ++g) mine |= local[g] == e;
+      if (!mine)
+        for (int s = 0; s < W; ++s) if (C(s, me, e) != 0) bad = 1;
+    }
+    int64_t pos = 0;
+    for (int g = 0; g < G; ++g) {
+      goff[g] = (int32_t)pos;
+      const int e = local[g];
+      for (int s = 0; s < W; ++s) {
+        const int b = g * W + s;
+        starts[b] = (int32_t)pos;
+        ranks[b] = s;
+        homes[b] = offs[s * ld + me * E + e];
+        group[b] = g;
+        pos += C(s, me, e);
+      }
+    }
+    if (bad) pos = 0;
+    starts[G * W] = (int32_t)pos;
+    goff[G] = (int32_t)pos;
+    if (bad) for (int g = 0; g < G; ++g) goff[g] = 0;
+    plan[0] = bad ? 0 : 1;
+    plan[1] = (int32_t)pos;
   }
 }
 
@@ -120,23 +203,43 @@ extern "C" moe_status moe_ep_pack_params(const float* scale_f32, const int32_t* 
   return MOE_OK;
 }
 
-extern "C" moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, float* scale_f32,
-                                           int32_t* zp, int32_t* rowsum, float* weight, moe_stream_t stream) {
+extern "C" moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int64_t n, const int32_t* n_dev,
+                                           float* scale_f32, int32_t* zp, int32_t* rowsum, float* weight,
+                                           moe_stream_t stream) {
   MOE_REQUIRE(params && scale_f32 && zp && rowsum && n >= 0, "ep_unpack_params: bad arguments");
   MOE_REQUIRE((reinterpret_cast<uintptr_t>(params) & 15) == 0, "ep_unpack_params: params must be 16-byte aligned");
   if (n == 0) return MOE_OK;
   unpack_params_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(reinterpret_cast<const int4*>(params), index,
-                                                                         n, scale_f32, zp, rowsum, weight);
+                                                                         n, n_dev, scale_f32, zp, rowsum, weight);
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }
 
-extern "C" moe_status moe_block_map(int64_t n, int nblocks, const int32_t* block_start, const int32_t* val0,
-                                    const int32_t* val1, int32_t* out0, int32_t* out1, moe_stream_t stream) {
+extern "C" int64_t moe_ep_peer_plan_size(int W, int E, int G) {
+  return 2 + (int64_t)W * E + 4 * (int64_t)G * W + 1 + G + 1;
+}
+
+extern "C" moe_status moe_ep_peer_plan(const int32_t* offsets_all, int W, int E, int me, const int32_t* local,
+                                       int G, int64_t cap, int64_t cap_home, int32_t* plan, moe_stream_t stream) {
+  MOE_REQUIRE(offsets_all && plan && (local || G == 0), "ep_peer_plan: null pointer");
+  MOE_REQUIRE(W >= 1 && E >= 1 && W * E <= 4096 && me >= 0 && me < W && G >= 0 && G <= E,
+              "ep_peer_plan: bad sizes");
+  ep_peer_plan_kernel<<<1, 256, 0, as_stream(stream)>>>(offsets_all, W, E, me, local, G, cap, cap_home, plan);
+  ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_block_map(int64_t n, const int32_t* n_dev, int nblocks, const int32_t* block_start,
+                                    const int32_t* val0, const int32_t* val1, const int32_t* val2,
+                                    const int32_t* valid, int32_t* out0, int32_t* out1, int32_t* out2,
+                                    moe_stream_t stream) {
   MOE_REQUIRE(n >= 0 && nblocks >= 1 && block_start && val0 && val1 && out0 && out1, "block_map: bad arguments");
+  MOE_REQUIRE(!out2 || val2, "block_map: out2 needs val2");
   if (n == 0) return MOE_OK;
-  block_map_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, nblocks, block_start, val0, val1, out0, out1);
+  block_map_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, n_dev, nblocks, block_start, val0, val1, val2,
+                                                                     valid, out0, out1, out2);
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;

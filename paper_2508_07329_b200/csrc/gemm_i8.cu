@@ -64,6 +64,8 @@ struct GemmArgs {
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   int band;                 // m-tiles per raster band (map_tile)
   int pf_kb;                // k blocks of the first weight tile to prefetch into L2 before griddep_wait
+  int l2pol;                // L2 eviction priority of the A (bits 0-1) and W (bits 2-3) tile loads:
+                            // 0 evict_last, 1 evict_normal, 2 evict_first
   void* const* out_tab;     // DEQUANT: row m goes to out_tab[out_rank[m]] + out_row[m] * ldo (EP combine)
   const int32_t* out_rank;
   const int32_t* out_row;
@@ -142,6 +144,14 @@ __device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start
     m_tile = full * bs + (w - n_tile * rm);
   }
   return TileInfo{g, off[g] + m_tile * TM, off[g + 1], n_tile * BN};
+}
+
+__device__ __forceinline__ uint64_t l2_policy(int which) {
+  uint64_t pol;
+  if (which == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (which == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 __device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
@@ -448,6 +458,16 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int atom_add_acquire_s32(int* p, int v) {
+  int old;
+  asm volatile("atom.acquire.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -474,12 +494,15 @@ __device__ __forceinline__ void comb_store(const GemmArgs& p, int row, int n_lo,
   for (int j = 0; j < 32; ++j) y[j] = __bfloat162float(__float2bfloat16_rn(y[j]));
   const int t = p.comb_src[row];
   int* ctr = p.comb_cnt + (int64_t)t * p.comb_chunks + (n_lo >> 5);
-  if (atomicAdd(ctr, 1) == 0) {
+  // acquire on the arrival (and on the rare poll): when the partner has
+  // already released (+2), its row is visible to the reads below
+  const int old = atom_add_acquire_s32(ctr, 1);
+  if (old == 0) {
     store32<true>(p.out, (int64_t)row * p.ldo + n_lo, y, 32, true);
     red_release_add(ctr, 2);
   } else {
-    while (ld_relaxed_s32(ctr) < 4) __nanosleep(32);
-    fence_acq_rel_gpu();         // acquire: the partner's row is read after its release
+    if (old < 3)
+      while (ld_acquire_s32(ctr) < 4) __nanosleep(32);
     const int r0 = p.comb_pos[2 * t], r1 = p.comb_pos[2 * t + 1];
     const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.out) +
                                                       (int64_t)(r0 == row ? r1 : r0) * p.ldo + n_lo);
@@ -736,8 +759,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0 && lane == 0) {
     // ===== TMA producer (both CTAs of a pair load their own halves) =====
-    const uint64_t pol_a = policy_evict_last();
-    const uint64_t pol_b = policy_evict_last();
+    const uint64_t pol_a = l2_policy(p.l2pol & 3);
+    const uint64_t pol_b = l2_policy((p.l2pol >> 2) & 3);
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0;
     for (int t = unit; t < total_tiles; t += n_units) {
@@ -1039,6 +1062,10 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   }
   // decode sizes (weight-stream bound): L2-prefetch the first 640 KB of each
   // unit's first weight tile during the previous kernel (PDL)
+  {
+    static const int env_pol = getenv("MOE_B200_GEMM_L2POL") ? atoi(getenv("MOE_B200_GEMM_L2POL")) : -1;
+    p.l2pol = env_pol >= 0 ? env_pol : 0;
+  }
   p.pf_kb = (M <= 1024) ? (int)std::min<int64_t>((K + kBK - 1) / kBK, (640 << 10) / ((BN / CG) * kBK)) : 0;
   const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
   const int64_t max_units = num_sms() / CG;

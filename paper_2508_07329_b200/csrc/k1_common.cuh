@@ -34,7 +34,26 @@ struct RowArgs {
   const int32_t* group;   // output row -> smoothing table row (optional)
   SmoothArgs sm;
   EpOut ep;               // optional (zero: local output arrays)
+  const int32_t* rows_dev = nullptr;  // optional: the row count lives on the device (<= rows, the capacity)
 };
+
+// Rows [lo, hi) of this CTA: `rows_per_cta` from the host, or, with a device
+// row count, an even split of *rows_dev over the grid (launched for the
+// capacity `rows`).
+__device__ __forceinline__ void cta_row_range(const RowArgs& a, int64_t rows_per_cta, int64_t& lo, int64_t& hi) {
+  int64_t rows = a.rows, rpc = rows_per_cta;
+  if (a.rows_dev) {
+    rows = min(rows, (int64_t)*a.rows_dev);
+    rpc = (rows + gridDim.x - 1) / gridDim.x;
+  }
+  lo = (int64_t)blockIdx.x * rpc;
+  hi = min(rows, lo + rpc);
+}
+
+// EP dispatch rows refused by the exchange plan (dst_rank < 0) are skipped.
+__device__ __forceinline__ bool ep_row_dropped(const RowArgs& a, int64_t r) {
+  return a.ep.codes_tab && a.ep.dst_rank[r] < 0;
+}
 
 __device__ __forceinline__ uint8_t* out_row_ptr(const RowArgs& a, uint8_t* codes, int64_t ldc, int64_t r) {
   return a.ep.codes_tab ? a.ep.codes_tab[a.ep.dst_rank[r]] + (int64_t)a.ep.dst_row[r] * ldc : codes + r * ldc;

@@ -228,16 +228,45 @@ __device__ __forceinline__ void for_row_batches(const uint4* src, int64_t nvec, 
   }
 }
 
-// warp arg-reduce: larger value wins, ties to the lower column
+// warp arg-reduce: larger value wins, ties to the lower column. Two REDUX
+// instructions on order-preserving keys instead of five shuffle rounds
+// (-0 is keyed as +0, so signed zeros tie like in a float compare; the
+// returned value is then +0, which every caller treats like -0).
+__device__ __forceinline__ uint32_t fkey32(float v) {
+  const uint32_t b = __float_as_uint(v + 0.0f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey32(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+#ifndef MOE_K1_REDUX
+#define MOE_K1_REDUX 1
+#endif
+#if MOE_K1_REDUX
+__device__ __forceinline__ void warp_argmax(float& v, int64_t& col) {
+  const uint32_t k = fkey32(v);
+  const uint32_t km = __reduce_max_sync(0xffffffffu, k);
+  col = (int64_t)__reduce_min_sync(0xffffffffu, k == km ? (uint32_t)col : 0xFFFFFFFFu);
+  v = funkey32(km);
+}
+__device__ __forceinline__ void warp_argmin(float& v, int64_t& col) {
+  const uint32_t k = fkey32(v);
+  const uint32_t km = __reduce_min_sync(0xffffffffu, k);
+  col = (int64_t)__reduce_min_sync(0xffffffffu, k == km ? (uint32_t)col : 0xFFFFFFFFu);
+  v = funkey32(km);
+}
+// warp sums of the code sum and the candidate count (REDUX)
+__device__ __forceinline__ void warp_sum2(int& sum, uint32_t& cnt) {
+  sum = (int)__reduce_add_sync(0xffffffffu, (unsigned)sum);
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+}
+#else   // shuffle trees (A/B reference)
 __device__ __forceinline__ void warp_argmax(float& v, int64_t& col) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
     const int64_t c2 = __shfl_xor_sync(0xffffffffu, col, o);
-    if (v2 > v || (v2 == v && c2 < col)) {
-      v = v2;
-      col = c2;
-    }
+    if (v2 > v || (v2 == v && c2 < col)) { v = v2; col = c2; }
   }
 }
 __device__ __forceinline__ void warp_argmin(float& v, int64_t& col) {
@@ -245,12 +274,17 @@ __device__ __forceinline__ void warp_argmin(float& v, int64_t& col) {
   for (int o = 16; o > 0; o >>= 1) {
     const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
     const int64_t c2 = __shfl_xor_sync(0xffffffffu, col, o);
-    if (v2 < v || (v2 == v && c2 < col)) {
-      v = v2;
-      col = c2;
-    }
+    if (v2 < v || (v2 == v && c2 < col)) { v = v2; col = c2; }
   }
 }
+__device__ __forceinline__ void warp_sum2(int& sum, uint32_t& cnt) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+}
+#endif
 
 // exact float64 value of element j of the row, and whether its float32
 // evaluation matches the recorded extreme (record consistency check)
@@ -427,8 +461,7 @@ static __device__ __noinline__ int fallback_row(const uint4* src, int64_t nvec, 
     smooth8(u, tab, c, xs);
     __stcs(dst + c, enc.encode8(u, xs, c, srow, rrow, sum));
   });
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  sum = (int)__reduce_add_sync(0xffffffffu, (unsigned)sum);
   *out = p;
   return sum;
 }
@@ -597,6 +630,7 @@ __device__ __forceinline__ void k1_row_warp(const RowArgs& a, int64_t r, const f
                                             const unsigned long long* __restrict__ ext, int bits, int sym,
                                             uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                                             int32_t* zp, int32_t* rowsum, int lane, Poll poll = Poll()) {
+  if (ep_row_dropped(a, r)) return;
   const int nvec = (int)(a.cols / 8);
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
   const RowView rv = row_view(a, r);
@@ -635,11 +669,7 @@ __device__ __forceinline__ void k1_row_warp(const RowArgs& a, int64_t r, const f
       uint32_t cnt = 0;
       sum = mode == 1 ? encode_row_fast<false, NB>(src, tab, srow, rrow, nvec, lane, f, dst, &cnt, poll)
                       : encode_row_fast<true, NB>(src, tab, srow, rrow, nvec, lane, f, dst, &cnt, poll);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      }
+      warp_sum2(sum, cnt);
       // exactly the expected possible extremes (the recorded elements):
       // they are the exact extremes and the codes stand
       done = cnt == f.expect;

@@ -100,6 +100,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a global range (TMA engine; 16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
 // order this thread's (and, after a warp/CTA barrier, its peers') generic-proxy
 // shared-memory accesses before subsequent async-proxy (TMA) accesses
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -278,24 +278,59 @@ extern "C" moe_status moe_channel_stats(const double* x, int64_t n, int64_t T, i
 }
 
 extern "C" moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
-                                             const int32_t* gather_rows, const double* smooth,
-                                             const double* smooth_recip, const float* smooth_recip_f32,
-                                             const int32_t* row_group, int bits, int symmetric,
-                                             void* const* codes_tab, void* const* params_tab,
+                                             const int32_t* gather_rows, const int32_t* token_pos, int k,
+                                             const double* smooth, const double* smooth_recip,
+                                             const float* smooth_recip_f32, const int32_t* row_group, int bits,
+                                             int symmetric, void* const* codes_tab, void* const* params_tab,
                                              const int32_t* dst_rank, const int32_t* dst_row, const float* row_weight,
                                              int64_t ldc, moe_stream_t stream) {
-  MOE_REQUIRE(x && gather_rows && codes_tab && params_tab && dst_rank && dst_row, "act_quant_dispatch: null pointer");
+  MOE_REQUIRE(x && (gather_rows || token_pos) && codes_tab && params_tab && dst_rank && dst_row,
+              "act_quant_dispatch: null pointer");
   MOE_REQUIRE(rows >= 1 && cols >= 1 && ldx >= cols && ldc >= cols, "act_quant_dispatch: bad sizes");
   MOE_REQUIRE(x_dtype == MOE_DT_BF16 && smooth && smooth_recip && smooth_recip_f32,
               "act_quant_dispatch: bf16 rows with divide-smoothing tables (f64, RN(1/s) and its f32 copy)");
   MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
-  RowArgs a{x, x_dtype, rows, cols, ldx, gather_rows, row_group, SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, cols}};
+  MOE_REQUIRE(!token_pos || (k >= 1 && rows % k == 0), "act_quant_dispatch: rows must be T * k");
+  RowArgs a{x, x_dtype, rows, cols, ldx, token_pos ? nullptr : gather_rows, row_group,
+            SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, cols}};
   a.ep = EpOut{reinterpret_cast<uint8_t* const*>(codes_tab), reinterpret_cast<int4* const*>(params_tab), dst_rank,
                dst_row, row_weight};
   cudaError_t err = cudaSuccess;
+  // token-major (x read once per token) when token_pos is given and x fits
+  // the register-resident kernel; else one warp per gathered row
+  if (token_pos && launch_act_quant_tokens(a, token_pos, k, rows / k, smooth_recip_f32, bits, symmetric, nullptr,
+                                           ldc, nullptr, nullptr, nullptr, nullptr, as_stream(stream), &err)) {
+    MOE_CUDA_TRY(err);
+    return MOE_OK;
+  }
+  MOE_REQUIRE(gather_rows, "act_quant_dispatch: token-major K1 not eligible and no gather_rows given");
+  a.gather = gather_rows;
   MOE_REQUIRE(launch_act_quant_fast(a, smooth_recip_f32, bits, symmetric, nullptr, ldc, nullptr, nullptr, nullptr,
                                     nullptr, as_stream(stream), &err),
               "act_quant_dispatch: needs cols % 8 == 0 and 16-byte aligned rows");
   MOE_CUDA_TRY(err);
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_act_quant_given_dev(const void* x, int x_dtype, int64_t rows_cap, const int32_t* rows_dev,
+                                              int64_t cols, int64_t ldx, const double* smooth,
+                                              const double* smooth_recip, const float* smooth_recip_f32,
+                                              const int32_t* row_group, int bits, int symmetric, uint8_t* codes,
+                                              int64_t ldc, double* scale, float* scale_f32, int32_t* zp,
+                                              int32_t* rowsum, const unsigned long long* row_ext,
+                                              moe_stream_t stream) {
+  MOE_REQUIRE(x && rows_dev && row_ext && codes && scale && zp && smooth && smooth_recip && smooth_recip_f32,
+              "act_quant_given_dev: null pointer");
+  MOE_REQUIRE(rows_cap >= 1 && cols >= 1 && ldx >= cols && ldc >= cols, "act_quant_given_dev: bad sizes");
+  MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
+  RowArgs a{x, x_dtype, rows_cap, cols, ldx, nullptr, row_group,
+            SmoothArgs{smooth, smooth_recip, MOE_SMOOTH_DIVIDE, cols}};
+  a.rows_dev = rows_dev;
+  cudaError_t err = cudaSuccess;
+  MOE_REQUIRE(launch_act_quant_given(a, smooth_recip_f32, row_ext, bits, symmetric, codes, ldc, scale, scale_f32, zp,
+                                     rowsum, as_stream(stream), &err),
+              "act_quant_given_dev: needs bf16 rows (cols % 8 == 0, 16-byte aligned) and float32 reciprocals");
+  MOE_CUDA_TRY(err);
+  MOE_LAUNCH_CHECK();
   return MOE_OK;
 }

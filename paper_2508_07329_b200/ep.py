@@ -51,11 +51,19 @@ class ExpertPlacement:
     """Where each expert of one layer lives in a world of ``world`` ranks.
 
     replicated: experts held by every rank (served where the token is).
-    owner[e]:   rank holding sharded expert e, -1 for replicated experts."""
+    owner[e]:   rank holding non-replicated expert e (its primary holder
+                when the expert is split), -1 for replicated experts.
+    routes:     optional [W][E] table: routes[s][e] = the rank that serves
+                expert e for the tokens of source rank s. Empty = every
+                source sends expert e to owner[e]. A sharded expert may be
+                split over several ranks this way (``balanced``); the ranks
+                appearing in its column are its holders.
+    """
     world: int
     experts: int
     replicated: tuple
     owner: tuple
+    routes: tuple = ()
 
     def __post_init__(self):
         if self.world < 1 or self.experts < 1:
@@ -71,6 +79,18 @@ class ExpertPlacement:
                 raise ValueError(f"expert {e} has owner {o} outside [0, {self.world})")
         if any(not 0 <= e < self.experts for e in rep):
             raise ValueError("replicated expert id out of range")
+        if self.routes:
+            if len(self.routes) != self.world or any(len(r) != self.experts for r in self.routes):
+                raise ValueError("routes must be [world][experts]")
+            for s_, row in enumerate(self.routes):
+                for e, d in enumerate(row):
+                    if e in rep and d != s_:
+                        raise ValueError(f"replicated expert {e}: source {s_} must route to itself")
+                    if not 0 <= d < self.world:
+                        raise ValueError(f"route ({s_}, {e}) -> {d} outside the world")
+            for e in range(self.experts):
+                if e not in rep and self.owner[e] not in self.holders(e):
+                    raise ValueError(f"expert {e}: owner {self.owner[e]} serves no source")
 
     @classmethod
     def sharded(cls, experts: int, world: int) -> "ExpertPlacement":
@@ -99,29 +119,108 @@ class ExpertPlacement:
         return cls(world, E, rep, tuple(owner))
 
     @classmethod
-    def from_plan(cls, plan: PlacementPlan, layer: int, freq: ExpertFreq, world: int) -> "ExpertPlacement":
+    def balanced(cls, counts, world: int, replicated=(), per_source=None) -> "ExpertPlacement":
+        """Load-split placement for few experts per rank (E <= W, e.g.
+        Mixtral's 8 experts on 8 GPUs, where one rank per expert makes the
+        hottest expert's rank the straggler). The unit of assignment is one
+        source rank's rows for one expert (``per_source[s][e]``, default
+        counts[e] / W). Non-replicated experts, hottest first (ties -> lower
+        id), are laid end to end and cut into W consecutive runs of about
+        the average load (McNaughton's wrap-around rule, quantised to whole
+        units: a unit goes to the rank whose slot [r, r + 1) x average holds
+        the unit's centre). So each rank's sharded load is the average within
+        one unit and at most W - 1 experts are split.
+        Inside a split expert every holder takes its own source's unit
+        first (served locally), the remaining sources go in ascending order.
+        Replicated experts serve their own tokens everywhere (equal load)."""
+        counts = np.asarray(counts, dtype=np.float64).reshape(-1)
+        E = counts.size
+        ps = (np.tile(counts / world, (world, 1)) if per_source is None
+              else np.asarray(per_source, dtype=np.float64).reshape(world, E))
+        rep = tuple(sorted(set(int(e) for e in replicated)))
+        nonrep = [int(e) for e in np.lexsort((np.arange(E), -counts)) if int(e) not in rep]
+        target = ps[:, nonrep].sum() / world if nonrep else 0.0
+        routes = [[s_ if e in rep else -1 for e in range(E)] for s_ in range(world)]
+        owner = [-1] * E
+        cum = 0.0
+        for e in nonrep:
+            n_units = {}                                   # rank -> number of e's units it serves
+            for s_ in sorted(range(world), key=lambda s_: -ps[s_, e]):
+                u = ps[s_, e]
+                # the unit goes to the rank whose cumulative slot holds its centre
+                r = min(world - 1, int((cum + 0.5 * u) // target)) if target > 0 else 0
+                n_units[r] = n_units.get(r, 0) + 1
+                cum += u
+            # which sources each holder serves: own source first, then ascending
+            free = [s_ for s_ in range(world) if s_ not in n_units]
+            need = dict(n_units)
+            for h in n_units:
+                routes[h][e] = h
+                need[h] -= 1
+            for h in sorted(n_units):
+                while need[h] > 0:
+                    routes[free.pop(0)][e] = h
+                    need[h] -= 1
+            owner[e] = max(n_units, key=lambda h: (n_units[h], -h))
+        split = cls(world, E, rep, tuple(owner), tuple(tuple(row) for row in routes))
+        # whole experts may already balance (e.g. many experts per rank):
+        # keep the unsplit packing unless splitting lowers the busiest rank
+        whole = cls.from_counts(counts, world, rep)
+        def peak(pl):
+            return np.bincount(pl.dest_table_all().ravel(), weights=ps.ravel(), minlength=world).max()
+        return split if peak(split) < peak(whole) * (1 - 1e-9) else whole
+
+    def dest_table_all(self) -> np.ndarray:
+        """[W, E]: dest_table of every source rank."""
+        return np.stack([self.dest_table(r) for r in range(self.world)])
+
+    @classmethod
+    def from_plan(cls, plan: PlacementPlan, layer: int, freq: ExpertFreq, world: int,
+                  balance: bool = True) -> "ExpertPlacement":
         """Residents of ``plan`` (plan_two_stage / plan_frequency / plan_path)
-        at ``layer`` are replicated; the rest are bin-packed on freq counts."""
-        return cls.from_counts(freq.counts[layer], world, plan.residents[layer])
+        at ``layer`` are replicated; the rest are placed on freq counts
+        (``balanced`` load split, or ``from_counts`` one rank each)."""
+        build = cls.balanced if balance else cls.from_counts
+        return build(freq.counts[layer], world, plan.residents[layer])
 
     def dest_table(self, rank: int) -> np.ndarray:
         """dest[e] = the rank that serves expert e for tokens of ``rank``."""
+        if self.routes:
+            return np.asarray(self.routes[rank], dtype=np.int32)
         return np.array([rank if o == -1 else o for o in self.owner], dtype=np.int32)
 
+    def holders(self, e: int) -> tuple:
+        """Ranks holding expert e's weights (every rank if replicated)."""
+        if self.owner[e] == -1:
+            return tuple(range(self.world))
+        if self.routes:
+            return tuple(sorted({row[e] for row in self.routes}))
+        return (self.owner[e],)
+
     def local_experts(self, rank: int) -> tuple:
-        return tuple(e for e in range(self.experts) if self.owner[e] == -1 or self.owner[e] == rank)
+        return tuple(e for e in range(self.experts) if rank in self.holders(e))
 
     def local_fraction(self, counts) -> float:
         """Fraction of activations served without leaving the home rank, for
-        tokens spread evenly over ranks: replicated experts always, a sharded
-        expert for the 1/W of tokens that live on its owner."""
+        tokens spread evenly over ranks (each source holds 1/W of expert e's
+        activations; they stay local when the source serves e itself)."""
         counts = np.asarray(counts, dtype=np.float64).reshape(-1)
         tot = counts.sum()
         if tot == 0:
             return 1.0
-        rep = np.zeros(self.experts, dtype=bool)
-        rep[list(self.replicated)] = True
-        return float((counts[rep].sum() + counts[~rep].sum() / self.world) / tot)
+        local = sum(counts[e] / self.world for s_ in range(self.world)
+                    for e, d in enumerate(self.dest_table(s_)) if d == s_)
+        return float(local / tot)
+
+    def rank_loads(self, counts) -> np.ndarray:
+        """Predicted rows each rank computes per forward, for global routed
+        counts ``counts`` [E] with tokens spread evenly over the ranks."""
+        counts = np.asarray(counts, dtype=np.float64).reshape(-1)
+        load = np.zeros(self.world)
+        for s_ in range(self.world):
+            for e, d in enumerate(self.dest_table(s_)):
+                load[d] += counts[e] / self.world
+        return load
 
 
 # ── exchange ──────────────────────────────────────────────────────────────
@@ -225,10 +324,10 @@ class ExpertParallelMoE:
         index, group_counts = regroup_index(recv_counts, self.local)
         return self.be.experts(recv_payload, index, group_counts, mark or (lambda _n: None))
 
-    def finish(self, st: DispatchState, y_home: torch.Tensor) -> torch.Tensor:
-        return self.be.combine(y_home, st.perm, st.T)
+    def finish(self, st: DispatchState, y_home: torch.Tensor, out=None) -> torch.Tensor:
+        return self.be.combine(y_home, st.perm, st.T, out=out)
 
-    def forward(self, x: torch.Tensor, timer=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
         """x [T, d] on this rank's device -> [T, d]. ``timer`` (optional) gets
         ``mark(stage)`` calls between phases (CUDA events)."""
         mark = timer.mark if timer is not None else (lambda _n: None)
@@ -242,11 +341,18 @@ class ExpertParallelMoE:
         y_recv = self.compute(recv, recv_counts, mark)
         y_home = self.ex.rows(y_recv, recv_splits, st.send_splits)
         mark("all_to_all_combine")
-        out = self.finish(st, y_home)
+        y = self.finish(st, y_home, out)
         mark("combine")
-        return out
+        return y
 
     __call__ = forward
+
+    def forward_host_stream(self, batches: list, depth: int = 2) -> list:
+        """Serving loop over host batches (hostio.stream_batches). The NCCL
+        transport's split sizes come back to the host every forward, so this
+        pipelines only the copies, not the host round trips."""
+        from .hostio import stream_batches
+        return stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth)
 
     def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
         """Pinned host tokens in, host tokens out (the end-to-end call)."""
@@ -259,106 +365,158 @@ class ExpertParallelMoE:
         return out_host
 
 
-def _peer_counts_all(ex, send_counts: np.ndarray) -> np.ndarray:
-    """All ranks' [W, E] send counts -> C[s, r, e] (one small all-gather)."""
+def _gather_offsets(ex, offsets: torch.Tensor) -> torch.Tensor:
+    """Every rank's route_permute offsets [W*E+1] -> [W, W*E+1] on the
+    device (one small all-gather; no host round trip)."""
     if getattr(ex, "world", 1) == 1 or ex.dist is None:
-        return send_counts[None]
-    t = torch.as_tensor(send_counts, dtype=torch.int64, device="cuda").contiguous()
-    out = torch.empty((ex.world,) + tuple(t.shape), dtype=torch.int64, device="cuda")
-    ex.dist.all_gather_into_tensor(out, t, group=ex.group)
-    return out.cpu().numpy()
+        return offsets.reshape(1, -1)
+    out = torch.empty((ex.world, offsets.numel()), dtype=offsets.dtype, device=offsets.device)
+    ex.dist.all_gather_into_tensor(out, offsets.contiguous(), group=ex.group)
+    return out
 
 
 class PeerExpertParallelMoE(ExpertParallelMoE):
-    """Expert-parallel forward over peer memory (no bulk NCCL traffic):
-    K1 writes every dispatched row straight into its owner's receive buffer
-    (already expert-contiguous, so no regroup), the owner's GEMM2 epilogue
-    writes each output row straight into the home rank's ``yhome`` slot, and
-    the home rank combines locally. Per forward: one small all-gather of the
-    [W, E] counts and two cross-rank barriers."""
+    """Expert-parallel forward over peer memory (no bulk NCCL traffic and no
+    host round trip): the routing offsets of all ranks are all-gathered on
+    the device, one small kernel (``moe_ep_peer_plan``) derives every send
+    base, receive block and grouped-GEMM offset from them, K1 writes each
+    dispatched row straight into its owner's receive buffer (already
+    expert-contiguous, so no regroup), the owner's GEMM2 epilogue writes
+    each output row straight into the home rank's ``yhome`` slot, and the
+    home rank combines locally. The receiver's row count stays on the device
+    (the K1 and GEMM launches are sized for the buffer capacity and read it),
+    so the host never waits inside a forward; per forward: one all-gather of
+    W*E+1 ints and two device-side cross-rank barriers.
+
+    A plan that would overflow a receive / home buffer (or route rows to a
+    rank that does not hold the expert) is refused on the device by every
+    rank alike: nothing is written to peer memory, and the refusal is raised
+    as ``RuntimeError`` by ``check()`` — at the latest by the next forward,
+    and by ``forward_host`` / ``forward_host_stream`` right away."""
 
     def __init__(self, backend, placement: ExpertPlacement, buffers: PeerBuffers, exchange=None,
                  rank: int | None = None):
         super().__init__(backend, placement, exchange, rank)
+        if getattr(backend, "d", 0) % 16 or getattr(backend, "d", 0) < 128:
+            raise ValueError("the peer transport needs d % 16 == 0 and d >= 128 (fused K1 records)")
         self.bufs = buffers
+        W, E = placement.world, placement.experts
+        self._rank_of = backend.to_index_tensor(np.repeat(np.arange(W, dtype=np.int32), E))
+        self._local_t = backend.to_index_tensor(np.asarray(self.local, dtype=np.int32))
+        self._flags = []             # (event, pinned valid flag) of forwards not checked yet
 
+    def migrate(self, placement: ExpertPlacement) -> None:
+        super().migrate(placement)
+        self._local_t = self.be.to_index_tensor(np.asarray(self.local, dtype=np.int32))
+
+    # phases (separate so one process can drive several ranks: run_loopback_peer)
     def peer_prepare(self, x):
         W, E = self.pl.world, self.pl.experts
         idx, w = self.be.route(x)
         keys = self.be.route_keys(idx, self.dest, E)
         perm = self.be.permute(keys, w, W * E)
-        off = self.be.to_host(perm["offsets"]).astype(np.int64)
-        return DispatchState(x.shape[0], perm, [x], np.diff(off).reshape(W, E))
+        return DispatchState(x.shape[0], perm, [x], None)
 
-    def check_capacity(self, C: np.ndarray, rows_home: int) -> None:
-        """Every rank holds the global C, so every rank raises together
-        (before any peer write) if some receive buffer or this rank's yhome
-        would overflow. Receive buffers are allocated with the same capacity
-        on every rank (symmetric memory)."""
-        recv = C.sum(axis=(0, 2))
-        cap = self.bufs.codes.shape[0]
-        if recv.max(initial=0) > cap:
-            r = int(np.argmax(recv))
-            raise RuntimeError(f"expert-parallel receive buffer overflow: rank {r} would receive {int(recv[r])} "
-                               f"rows, capacity {cap} (PeerBuffers cap)")
-        home = C.sum(axis=(1, 2))           # rows each rank routes = its yhome rows
-        caph = self.bufs.yhome.shape[0]
-        if max(int(home.max(initial=0)), rows_home) > caph:
-            r = int(np.argmax(home))
-            raise RuntimeError(f"expert-parallel yhome overflow: rank {r} routes {int(home[r])} rows, capacity {caph}")
+    def peer_plan(self, offsets_all: torch.Tensor) -> torch.Tensor:
+        plan = ops.ep_peer_plan(offsets_all, self.rank, self._local_t, self.bufs.codes.shape[0],
+                                self.bufs.yhome.shape[0])
+        flag = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        flag.copy_(plan[:1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._flags.append((ev, flag))
+        return plan
 
-    def peer_send(self, st: DispatchState, C: np.ndarray):
-        self.check_capacity(C, st.perm["src_token"].numel())
-        rank_of, base = peer_send_layout(C, self.rank, self.pl)
+    def check(self, wait: bool = False) -> None:
+        """Raise if an earlier forward's exchange plan was refused (buffer
+        overflow / placement mismatch). Non-blocking unless ``wait``."""
+        keep = []
+        for ev, flag in self._flags:
+            if wait:
+                ev.synchronize()
+            if ev.query():
+                if int(flag[0]) == 0:
+                    self._flags = []
+                    raise RuntimeError(
+                        "expert-parallel exchange refused: a receive buffer (PeerBuffers cap "
+                        f"{self.bufs.codes.shape[0]} rows) or home buffer ({self.bufs.yhome.shape[0]} rows) "
+                        "would overflow, or rows were routed to a rank that does not hold the expert")
+            else:
+                keep.append((ev, flag))
+        self._flags = keep
+
+    def peer_send(self, st: DispatchState, plan: torch.Tensor):
+        W, E, G = self.pl.world, self.pl.experts, len(self.local)
+        v = ops.plan_views(plan, W, E, G)
         n = st.perm["src_token"].numel()
         if n == 0:
             return
-        dst_rank, dst_row = ops.block_map(n, st.perm["offsets"], self.be.to_index_tensor(rank_of),
-                                          self.be.to_index_tensor(base))
-        self.be.dispatch_send(st.payload[0], st.perm, self.pl.experts, self.bufs, dst_rank, dst_row)
+        dst_rank, dst_row = ops.block_map(n, st.perm["offsets"], self._rank_of, v["send_base"], valid=v["valid"])
+        self.be.dispatch_send(st.payload[0], st.perm, E, self.bufs, dst_rank, dst_row)
 
-    def peer_compute(self, C: np.ndarray, mark=None):
-        starts, ranks, homes, counts = peer_recv_layout(C, self.rank, self.local)
-        R = int(starts[-1])
-        if R == 0:
+    def peer_compute(self, plan: torch.Tensor, mark=None):
+        W, E, G = self.pl.world, self.pl.experts, len(self.local)
+        if G == 0:
             return
-        out_rank, out_row = ops.block_map(R, self.be.to_index_tensor(starts), self.be.to_index_tensor(ranks),
-                                          self.be.to_index_tensor(homes))
-        self.be.experts_peer(self.bufs, R, counts, out_rank, out_row, mark or (lambda _n: None))
+        v = ops.plan_views(plan, W, E, G)
+        cap = self.bufs.codes.shape[0]
+        out_rank, out_row, row_group = ops.block_map(cap, v["starts"], v["ranks"], v["homes"], val2=v["group"],
+                                                     n_dev=v["R"], nblocks=G * W)
+        self.be.experts_peer_dev(self.bufs, v["R"], v["goff"], row_group, out_rank, out_row,
+                                 mark or (lambda _n: None))
 
-    def peer_finish(self, st: DispatchState):
-        return self.be.combine(self.bufs.yhome[: st.perm["src_token"].numel()], st.perm, st.T)
+    def peer_finish(self, st: DispatchState, out=None):
+        return self.be.combine(self.bufs.yhome[: st.perm["src_token"].numel()], st.perm, st.T, out=out)
 
-    def forward(self, x: torch.Tensor, timer=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        self.check()
         mark = timer.mark if timer is not None else (lambda _n: None)
         mark("start")
         st = self.peer_prepare(x)
-        C = _peer_counts_all(self.ex, st.send_counts)
+        plan = self.peer_plan(_gather_offsets(self.ex, st.perm["offsets"]))
         mark("dispatch_prepare")
-        self.peer_send(st, C)
+        self.peer_send(st, plan)
         self.bufs.barrier()
         mark("dispatch_k1_peer")
-        self.peer_compute(C, mark)
+        self.peer_compute(plan, mark)
         self.bufs.barrier()
         mark("gemm2_peer_barrier")
-        out = self.peer_finish(st)
+        y = self.peer_finish(st, out)
         mark("combine")
-        return out
+        return y
 
     __call__ = forward
 
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        out = super().forward_host(x_host, out_host)
+        self.check(wait=True)
+        return out
+
+    def forward_host_stream(self, batches: list, depth: int = 2) -> list:
+        """Serving loop over host batches (hostio.stream_batches): the H2D of
+        batch b+1 and the D2H of batch b-1 overlap batch b's EP forward."""
+        from .hostio import stream_batches
+        outs = stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth)
+        self.check(wait=True)
+        return outs
+
 
 def run_loopback_peer(ranks: list, xs: list) -> list:
-    """``run_loopback`` for the peer transport: every rank's K1 writes into
-    the other ranks' buffers, then every rank's experts write their outputs
-    into the home ranks' buffers, then every rank combines."""
+    """``run_loopback`` for the peer transport: the offsets of all ranks are
+    stacked (the all-gather), every rank's plan kernel runs, every rank's K1
+    writes into the other ranks' buffers, then every rank's experts write
+    their outputs into the home ranks' buffers, then every rank combines."""
     sts = [m.peer_prepare(x) for m, x in zip(ranks, xs)]
-    C = np.stack([st.send_counts for st in sts])
-    for m, st in zip(ranks, sts):
-        m.peer_send(st, C)
+    offs = torch.stack([st.perm["offsets"] for st in sts])
+    plans = [m.peer_plan(offs) for m in ranks]
+    for m, st, pl in zip(ranks, sts, plans):
+        m.peer_send(st, pl)
+    for m, pl in zip(ranks, plans):
+        m.peer_compute(pl)
+    outs = [m.peer_finish(st) for m, st in zip(ranks, sts)]
     for m in ranks:
-        m.peer_compute(C)
-    return [m.peer_finish(st) for m, st in zip(ranks, sts)]
+        m.check(wait=True)
+    return outs
 
 
 def run_loopback(ranks: list, xs: list) -> list:
@@ -430,7 +588,9 @@ class PeerBuffers:
 
 
 def peer_send_layout(C: np.ndarray, me: int, placement: ExpertPlacement) -> tuple[np.ndarray, np.ndarray]:
-    """Sender side. C[s, r, e] = rows rank s sends to rank r for expert e.
+    """Host restatement of the send half of ``moe_ep_peer_plan`` (the device
+    plan the forward uses; tests compare the two). Sender side. C[s, r, e] =
+    rows rank s sends to rank r for expert e.
     Rank r's receive buffer is expert-major (its local experts ascending),
     sender-minor. Returns per sort key (r, e) (r-major): destination rank and
     the first receive-buffer row of this sender's block."""
@@ -446,7 +606,8 @@ def peer_send_layout(C: np.ndarray, me: int, placement: ExpertPlacement) -> tupl
 
 
 def peer_recv_layout(C: np.ndarray, me: int, local: tuple) -> tuple:
-    """Receiver side: block starts of the (expert, sender) blocks in the
+    """Host restatement of the receive half of ``moe_ep_peer_plan``.
+    Receiver side: block starts of the (expert, sender) blocks in the
     receive buffer, each block's home rank and home row (the sender's sorted
     row of its first element), and the per-local-expert row counts."""
     W, _, E = C.shape
@@ -571,36 +732,37 @@ class CudaExpertBackend:
         inv[index] = np.arange(n, dtype=np.int32)
         return ops.gather_rows(y, self.to_index_tensor(inv))
 
-    def combine(self, y_home, perm, T):
-        return ops.combine(y_home, perm["token_pos"], T, self.k, out_dtype=self.out_dtype)
+    def combine(self, y_home, perm, T, out=None):
+        return ops.combine(y_home, perm["token_pos"], T, self.k, out_dtype=self.out_dtype, out=out)
 
     # peer transport
     def dispatch_send(self, x, perm, E, bufs, dst_rank, dst_row):
         W = perm["offsets"].numel() // E
         s, sr, sr32 = self._smooth_tables(W)
+        # token-major K1 (x read once per token) when x fits its registers
+        tok = perm["token_pos"] if ops.act_quant_tokens_ok(x) else None
         ops.act_quant_dispatch(x, perm["src_token"], perm["row_expert"], smooth=s, smooth_recip=sr,
                                smooth_recip_f32=sr32, codes_tab=bufs.codes_tab, params_tab=bufs.params_tab,
                                dst_rank=dst_rank, dst_row=dst_row, row_weight=perm["row_weight"],
-                               ldc=bufs.codes.stride(0))
+                               ldc=bufs.codes.stride(0), token_pos=tok, k=self.k)
 
-    def experts_peer(self, bufs, R, group_counts, out_rank, out_row, mark=lambda _n: None):
+    def experts_peer_dev(self, bufs, R_dev, goff, row_group, out_rank, out_row, mark=lambda _n: None):
+        """Receiver compute with the row count on the device: kernels are
+        sized for the buffer capacity and read R / the group offsets."""
         b = self.bank
         G = len(self.local_experts)
-        prm = ops.ep_unpack_params(bufs.params[:R], None)
-        a1 = {"codes": bufs.codes[:R], "scale_f32": prm["scale_f32"], "zp": prm["zp"], "rowsum": prm["rowsum"]}
-        offs = self.to_index_tensor(np.concatenate([[0], np.cumsum(group_counts)]))
-        row_group = self.to_index_tensor(np.repeat(np.arange(G), group_counts))
-        fuse = b.d % 16 == 0 and b.d >= 128
-        ext = torch.empty((R, 2), dtype=torch.int64, device="cuda") if fuse else None
-        h = ops.w8a8_gemm(a1, b.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16, group_offsets=offs,
-                          num_groups=G, n_per_group=2 * b.F, next_smooth_recip_f32=b.s2_recip32 if fuse else None,
-                          row_ext=ext)
+        cap = bufs.codes.shape[0]
+        prm = ops.ep_unpack_params(bufs.params, None, cap, n_dev=R_dev)
+        a1 = {"codes": bufs.codes, "scale_f32": prm["scale_f32"], "zp": prm["zp"], "rowsum": prm["rowsum"]}
+        ext = torch.empty((cap, 2), dtype=torch.int64, device="cuda")
+        h = ops.w8a8_gemm(a1, b.w13, epilogue=L.EPI_SWIGLU, out_dtype=torch.bfloat16, group_offsets=goff,
+                          num_groups=G, n_per_group=2 * b.F, next_smooth_recip_f32=b.s2_recip32, row_ext=ext)
         mark("gemm13_swiglu")
-        a2 = ops.act_quant(h, smooth=b.s2, smooth_recip=b.s2_recip, smooth_recip_f32=b.s2_recip32,
-                           row_group=row_group, row_ext=ext)
+        a2 = ops.act_quant_given_dev(h, R_dev, row_group, ext, smooth=b.s2, smooth_recip=b.s2_recip,
+                                     smooth_recip_f32=b.s2_recip32)
         mark("quant_h")
         ops.w8a8_gemm_scatter(a2, b.w2, out_tab=bufs.y_tab, out_rank=out_rank, out_row=out_row,
-                              ldo=bufs.yhome.stride(0), row_weight=prm["weight"], group_offsets=offs, num_groups=G,
+                              ldo=bufs.yhome.stride(0), row_weight=prm["weight"], group_offsets=goff, num_groups=G,
                               n_per_group=b.d)
         mark("gemm2")
 

@@ -299,46 +299,8 @@ class MoELayer:
         forwarded whole (no per-chunk weight re-streaming); the staging ring
         keeps the allocator out of the loop (no cross-stream frees).
         Returns the out_host tensors after the last D2H."""
-        if not batches:
-            return []
-        T = max(x.shape[0] for x, _ in batches)
-        cur = torch.cuda.current_stream()
-        io = getattr(self, "_stream_io", None)
-        if io is None or io["bufs"][0].shape[0] < T or len(io["bufs"]) < depth:
-            io = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
-                  "bufs": [torch.empty((T, self.d), dtype=batches[0][0].dtype, device="cuda") for _ in range(depth)],
-                  "outs": [torch.empty((T, self.d), dtype=self.out_dtype, device="cuda") for _ in range(depth)]}
-            self._stream_io = io
-        h2d, d2h, bufs, obufs = io["h2d"], io["d2h"], io["bufs"], io["outs"]
-        h2d.wait_stream(cur)
-        done = [None] * len(batches)          # forward of batch i finished (its input slot is free)
-        copied = [None] * len(batches)        # D2H of batch i finished (its output slot is free)
-        outs = []
-        for i, (xh, oh) in enumerate(batches):
-            slot, oslot = bufs[i % depth], obufs[i % depth]
-            n = xh.shape[0]
-            if oh is None:
-                oh = torch.empty((n, self.d), dtype=self.out_dtype, pin_memory=True)
-            with torch.cuda.stream(h2d):
-                if i >= depth:
-                    h2d.wait_event(done[i - depth])
-                slot[:n].copy_(xh, non_blocking=True)
-                loaded = torch.cuda.Event()
-                loaded.record(h2d)
-            cur.wait_event(loaded)
-            if i >= depth:
-                cur.wait_event(copied[i - depth])
-            self.forward(slot[:n], out=oslot[:n])
-            done[i] = torch.cuda.Event()
-            done[i].record(cur)
-            with torch.cuda.stream(d2h):
-                d2h.wait_event(done[i])
-                oh.copy_(oslot[:n], non_blocking=True)
-                copied[i] = torch.cuda.Event()
-                copied[i].record(d2h)
-            outs.append(oh)
-        d2h.synchronize()
-        return outs
+        from .hostio import stream_batches
+        return stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth)
 
     # ------------------------------------------------------------------
     def save(self, out_dir) -> None:

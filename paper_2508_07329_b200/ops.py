@@ -446,40 +446,101 @@ def ep_pack_params(a: dict, weight: torch.Tensor | None) -> torch.Tensor:
     return params
 
 
-def ep_unpack_params(params: torch.Tensor, index: torch.Tensor | None) -> dict:
-    n = index.numel() if index is not None else params.shape[0]
+def ep_unpack_params(params: torch.Tensor, index: torch.Tensor | None, n: int | None = None,
+                     n_dev: torch.Tensor | None = None) -> dict:
+    """SoA (scale_f32, zp, rowsum, weight) of params[index[r]] (or params[r]),
+    r < n; with ``n_dev`` (device int32) only r < min(n, n_dev[0])."""
+    if n is None:
+        n = index.numel() if index is not None else params.shape[0]
     dev = params.device
     out = {"scale_f32": torch.empty(n, dtype=torch.float32, device=dev),
            "zp": torch.empty(n, dtype=torch.int32, device=dev),
            "rowsum": torch.empty(n, dtype=torch.int32, device=dev),
            "weight": torch.empty(n, dtype=torch.float32, device=dev)}
-    L.call("moe_ep_unpack_params", L.ptr(params.contiguous()), L.ptr(index), n, L.ptr(out["scale_f32"]),
+    L.call("moe_ep_unpack_params", L.ptr(params.contiguous()), L.ptr(index), n, L.ptr(n_dev), L.ptr(out["scale_f32"]),
            L.ptr(out["zp"]), L.ptr(out["rowsum"]), L.ptr(out["weight"]), _s())
     return out
 
 
 # ── fused expert-parallel transport (peer memory) ──────────────────────────
-def block_map(n: int, block_start: torch.Tensor, val0: torch.Tensor, val1: torch.Tensor):
-    """Rows in blocks [start[b], start[b+1]) -> (val0[b], val1[b] + i - start[b])."""
+def block_map(n: int, block_start: torch.Tensor, val0: torch.Tensor, val1: torch.Tensor,
+              val2: torch.Tensor | None = None, valid: torch.Tensor | None = None,
+              n_dev: torch.Tensor | None = None, nblocks: int | None = None):
+    """Rows in blocks [start[b], start[b+1]) -> (val0[b], val1[b] + i - start[b]
+    [, val2[b]]) for i < n (i < min(n, n_dev[0]) with a device count);
+    ``valid`` (device int32, optional): 0 makes every val0 output -1."""
     dev = block_start.device
     o0 = torch.empty(n, dtype=torch.int32, device=dev)
     o1 = torch.empty(n, dtype=torch.int32, device=dev)
-    L.call("moe_block_map", n, val0.numel(), L.ptr(block_start.contiguous()), L.ptr(val0.contiguous()),
-           L.ptr(val1.contiguous()), L.ptr(o0), L.ptr(o1), _s())
-    return o0, o1
+    o2 = torch.empty(n, dtype=torch.int32, device=dev) if val2 is not None else None
+    L.call("moe_block_map", n, L.ptr(n_dev), nblocks if nblocks is not None else val0.numel(),
+           L.ptr(block_start.contiguous()), L.ptr(val0.contiguous()), L.ptr(val1.contiguous()),
+           L.ptr(val2), L.ptr(valid), L.ptr(o0), L.ptr(o1), L.ptr(o2), _s())
+    return (o0, o1) if o2 is None else (o0, o1, o2)
 
 
-def act_quant_dispatch(x: torch.Tensor, gather: torch.Tensor, row_group: torch.Tensor, *, smooth, smooth_recip,
+def ep_peer_plan(offsets_all: torch.Tensor, me: int, local: torch.Tensor, cap: int, cap_home: int,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device-side exchange plan of a peer-memory EP forward (moe_ep_peer_plan):
+    offsets_all [W, W*E+1] int32 (every rank's route_permute offsets over
+    its W*E keys) -> int32 plan [valid, R, send_base[W*E], starts[G*W+1],
+    ranks[G*W], homes[G*W], group[G*W], goff[G+1]]."""
+    W = offsets_all.shape[0]
+    E = (offsets_all.shape[1] - 1) // W
+    G = local.numel()
+    size = L.load().moe_ep_peer_plan_size(W, E, G)
+    plan = out if out is not None else torch.empty(size, dtype=torch.int32, device=offsets_all.device)
+    L.call("moe_ep_peer_plan", L.ptr(offsets_all.contiguous()), W, E, me, L.ptr(local), G, cap, cap_home,
+           L.ptr(plan), _s())
+    return plan
+
+
+def plan_views(plan: torch.Tensor, W: int, E: int, G: int) -> dict:
+    """Named slices of an ep_peer_plan buffer (device views, no copies)."""
+    o = 2
+    views = {"valid": plan[0:1], "R": plan[1:2]}
+    for name, n in (("send_base", W * E), ("starts", G * W + 1), ("ranks", G * W), ("homes", G * W),
+                    ("group", G * W), ("goff", G + 1)):
+        views[name] = plan[o:o + n]
+        o += n
+    return views
+
+
+def act_quant_dispatch(x: torch.Tensor, gather: torch.Tensor | None, row_group: torch.Tensor, *, smooth, smooth_recip,
                        smooth_recip_f32, codes_tab: torch.Tensor, params_tab: torch.Tensor, dst_rank: torch.Tensor,
                        dst_row: torch.Tensor, row_weight: torch.Tensor | None, ldc: int, bits: int = 8,
-                       symmetric: bool = False) -> None:
-    """K1 per token whose rows land directly in the destination ranks' receive buffers."""
+                       symmetric: bool = False, token_pos: torch.Tensor | None = None, k: int = 1) -> None:
+    """K1 whose rows land directly in the destination ranks' receive buffers:
+    token-major (x read once per token) when ``token_pos`` is given, else
+    one warp per gathered row."""
     x = _rowmajor(x, "x")
-    n = gather.numel()
-    L.call("moe_act_quant_dispatch", L.ptr(x), _dt(x), n, x.shape[1], x.stride(0), L.ptr(gather.contiguous()),
+    n = token_pos.numel() if token_pos is not None else gather.numel()
+    L.call("moe_act_quant_dispatch", L.ptr(x), _dt(x), n, x.shape[1], x.stride(0),
+           L.ptr(gather.contiguous() if gather is not None else None),
+           L.ptr(token_pos.contiguous() if token_pos is not None else None), k,
            L.ptr(smooth), L.ptr(smooth_recip), L.ptr(smooth_recip_f32), L.ptr(row_group.contiguous()), bits,
            int(bool(symmetric)), L.ptr(codes_tab), L.ptr(params_tab), L.ptr(dst_rank), L.ptr(dst_row),
            L.ptr(row_weight), ldc, _s())
+
+
+def act_quant_given_dev(h: torch.Tensor, rows_dev: torch.Tensor, row_group: torch.Tensor, row_ext: torch.Tensor, *,
+                        smooth, smooth_recip, smooth_recip_f32, bits: int = 8, symmetric: bool = False) -> dict:
+    """K1 with producer records over rows r < rows_dev[0] of h (capacity
+    h.shape[0] rows; the count stays on the device)."""
+    h = _rowmajor(h, "h")
+    n, cols = h.shape
+    dev = h.device
+    out = {"codes": torch.empty((n, cols), dtype=torch.uint8, device=dev),
+           "scale": torch.empty(n, dtype=torch.float64, device=dev),
+           "scale_f32": torch.empty(n, dtype=torch.float32, device=dev),
+           "zp": torch.empty(n, dtype=torch.int32, device=dev),
+           "rowsum": torch.empty(n, dtype=torch.int32, device=dev),
+           "granularity": "per_token", "bits": bits}
+    L.call("moe_act_quant_given_dev", L.ptr(h), _dt(h), n, L.ptr(rows_dev), cols, h.stride(0), L.ptr(smooth),
+           L.ptr(smooth_recip), L.ptr(smooth_recip_f32), L.ptr(row_group), bits, int(bool(symmetric)),
+           L.ptr(out["codes"]), out["codes"].stride(0), L.ptr(out["scale"]), L.ptr(out["scale_f32"]),
+           L.ptr(out["zp"]), L.ptr(out["rowsum"]), L.ptr(row_ext), _s())
+    return out
 
 
 def w8a8_gemm_scatter(a: dict, w: dict, *, out_tab: torch.Tensor, out_rank: torch.Tensor, out_row: torch.Tensor,

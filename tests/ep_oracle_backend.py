@@ -87,10 +87,13 @@ class OracleBackend:
         out[index] = y
         return torch.from_numpy(out)
 
-    def combine(self, y_home, perm, T):
+    def combine(self, y_home, perm, T, out=None):
         y = y_home.numpy()
         pos = perm["token_pos"].numpy()
-        out = np.zeros((T, y.shape[1]))
+        acc = np.zeros((T, y.shape[1]))
         for j in range(self.k):
-            out = out + y[pos[:, j]]
-        return torch.from_numpy(out)
+            acc = acc + y[pos[:, j]]
+        if out is not None:
+            out.copy_(torch.from_numpy(acc))
+            return out
+        return torch.from_numpy(acc)

@@ -191,3 +191,84 @@ def test_peer_layouts_agree():
                 assert base[r * E + e] == starts[b]
                 assert homes[b] == C[s].reshape(-1)[: r * E + e].sum()
                 b += 1
+
+
+# ── load-split placement (E <= W) ─────────────────────────────────────────
+def test_balanced_placement_splits_hot_experts():
+    """8 experts on 8 ranks with skewed routing: one holder per expert makes
+    the hottest expert's rank the straggler; the split placement keeps every
+    rank within one source unit of the average and at most W - 1 experts
+    are split."""
+    counts = np.array([400, 90, 80, 120, 60, 100, 70, 80])
+    W = 8
+    whole = ExpertPlacement.from_counts(counts, W)
+    pl = ExpertPlacement.balanced(counts, W)
+    lw, lb = whole.rank_loads(counts), pl.rank_loads(counts)
+    assert lw.max() / lw.mean() > 3.0
+    unit = counts.max() / W
+    assert lb.max() - lb.mean() <= unit + 1e-9
+    assert sum(len(pl.holders(e)) - 1 for e in range(8)) <= W - 1
+    assert lb.sum() == pytest.approx(counts.sum())
+    for s in range(W):                     # every source routes each expert to one of its holders
+        d = pl.dest_table(s)
+        assert all(d[e] in pl.holders(e) for e in range(8))
+        for e in range(8):                 # a holder serves its own tokens
+            if s in pl.holders(e):
+                assert d[e] == s
+
+
+def test_balanced_equals_from_counts_when_whole_experts_balance():
+    counts = [50, 10, 40, 40, 5, 30]
+    assert ExpertPlacement.balanced(counts, 2) == ExpertPlacement.from_counts(counts, 2)
+
+
+def test_balanced_keeps_replicated_local():
+    counts = np.array([300, 50, 50, 200, 60, 40])
+    pl = ExpertPlacement.balanced(counts, 4, replicated=(0,))
+    for s in range(4):
+        assert pl.dest_table(s)[0] == s
+    assert pl.holders(0) == (0, 1, 2, 3)
+    with pytest.raises(ValueError):
+        ExpertPlacement(2, 2, (0,), (-1, 0), routes=((1, 0), (1, 0)))   # replicated routed away
+
+
+@pytest.mark.parametrize("W,T", [(3, (20, 33, 7)), (4, (16, 16, 16, 16))])
+def test_ep_loopback_balanced_split_matches_moe_forward(W, T):
+    wg, experts = _layer(3)
+    rng = np.random.default_rng(8)
+    xs = [_tokens(rng, t) for t in T]
+    counts = np.bincount(M.router_topk(M.gate_logits(np.concatenate(xs), wg).astype(np.float32), K)[0].ravel(),
+                         minlength=E)
+    pl = ExpertPlacement.balanced(counts * 4, W)
+    ranks = [ExpertParallelMoE(OracleBackend(wg, experts, pl.local_experts(r), K), pl, rank=r,
+                               exchange=_NoExchange(W, r)) for r in range(W)]
+    for x, o in zip(xs, run_loopback(ranks, [torch.from_numpy(x) for x in xs])):
+        want, _, _ = M.moe_forward(x, wg, experts, K)
+        np.testing.assert_array_equal(o.numpy(), want)
+
+
+def _gloo_worker_split(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wg, experts = _layer(5)
+        rng = np.random.default_rng(200 + rank)
+        x = _tokens(rng, 25 + 9 * rank)
+        # expert 0 hot: split over both ranks (each serves its own tokens)
+        pl = ExpertPlacement.balanced([400, 5, 30, 30, 10, 20], world)
+        assert len(pl.holders(0)) == 2
+        m = ExpertParallelMoE(OracleBackend(wg, experts, pl.local_experts(rank), K), pl)
+        out = m(torch.from_numpy(x)).numpy()
+        want, _, _ = M.moe_forward(x, wg, experts, K)
+        np.save(os.path.join(outdir, f"r{rank}.npy"), np.stack([out, want]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_gloo_world2_split_expert():
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_worker_split, args=(2, _free_port(), d), nprocs=2, join=True)
+        for r in range(2):
+            got, want = np.load(os.path.join(d, f"r{r}.npy"))
+            np.testing.assert_array_equal(got, want)

@@ -155,3 +155,103 @@ def test_ep_peer_symmetric_memory_single_rank(tmp_path):
     """)
     r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300)
     assert "EQUAL" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+def _offsets_from_counts(C):
+    """Per sender s: route_permute offsets over its W*E keys from C[s, r, e]."""
+    W, _, E = C.shape
+    return np.stack([np.concatenate([[0], np.cumsum(C[s].reshape(-1))]) for s in range(W)]).astype(np.int32)
+
+
+@pytest.mark.parametrize("W,E,seed", [(1, 8, 0), (3, 6, 1), (8, 8, 2), (4, 16, 3)])
+def test_ep_peer_plan_matches_host_layout(cuda, W, E, seed):
+    """The device exchange plan (moe_ep_peer_plan) equals the host layout
+    functions for every rank, with split (multi-holder) placements; an
+    overflowing capacity is refused on the device (valid 0, nothing received)."""
+    from paper_2508_07329_b200.ep import peer_recv_layout, peer_send_layout
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(50, 400, E)
+    pl = ExpertPlacement.balanced(counts, W, replicated=(1,) if E > 2 else ())
+    C = np.zeros((W, W, E), dtype=np.int64)
+    for s in range(W):
+        dest = pl.dest_table(s)
+        for e in range(E):
+            C[s, dest[e], e] = rng.integers(0, 40)
+    offs = torch.from_numpy(_offsets_from_counts(C)).cuda()
+    cap = int(C.sum(axis=(0, 2)).max()) + 3
+    cap_home = int(C.sum(axis=(1, 2)).max())
+    for me in range(W):
+        local = pl.local_experts(me)
+        G = len(local)
+        plan = ops.ep_peer_plan(offs, me, torch.tensor(local, dtype=torch.int32, device=cuda), cap, cap_home)
+        v = {k: t.cpu().numpy() for k, t in ops.plan_views(plan, W, E, G).items()}
+        assert v["valid"][0] == 1
+        _, base = peer_send_layout(C, me, pl)
+        live = C[me].reshape(-1) > 0
+        np.testing.assert_array_equal(v["send_base"][live], base[live])
+        starts, ranks, homes, gc = peer_recv_layout(C, me, local)
+        np.testing.assert_array_equal(v["starts"], starts)
+        np.testing.assert_array_equal(v["ranks"], ranks)
+        np.testing.assert_array_equal(v["homes"], homes)
+        np.testing.assert_array_equal(v["goff"], np.concatenate([[0], np.cumsum(gc)]))
+        np.testing.assert_array_equal(v["group"], np.repeat(np.arange(G), W))
+        assert v["R"][0] == starts[-1]
+        bad = ops.ep_peer_plan(offs, me, torch.tensor(local, dtype=torch.int32, device=cuda), cap - 4, cap_home)
+        assert bad[0].item() == 0 and bad[1].item() == 0
+
+
+@pytest.mark.parametrize("W,T", [(2, (600, 333)), (4, (256, 1, 700, 90)), (8, (64,) * 8)])
+def test_ep_peer_loopback_balanced_split(layer, W, T):
+    """Split experts (ExpertPlacement.balanced: one hot expert served by
+    several ranks, each for a fixed set of sources) over the fused peer
+    transport and over the NCCL-style transport: bit-identical to the
+    single-GPU forward."""
+    from paper_2508_07329_b200.ep import PeerBuffers, PeerExpertParallelMoE, run_loopback_peer
+    rng = np.random.default_rng(W)
+    xs = [_x(rng, t, layer.d) for t in T]
+    counts = np.bincount(layer.route(torch.cat(xs))[1].cpu().numpy().ravel(), minlength=layer.E)
+    pl = ExpertPlacement.balanced(counts * 10, W)
+    if W >= 4:
+        assert any(len(pl.holders(e)) > 1 for e in range(layer.E))
+    cap_home = max(T) * layer.k
+    bufs = PeerBuffers.loopback(W, layer.d, W * cap_home, cap_home)
+    ranks = [PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, bufs[r],
+                                   rank=r, exchange=_Local(W, r)) for r in range(W)]
+    for x, out in zip(xs, run_loopback_peer(ranks, xs)):
+        assert torch.equal(out, layer.forward(x))
+    ranks = [ExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, rank=r,
+                               exchange=_Local(W, r)) for r in range(W)]
+    for x, out in zip(xs, run_loopback(ranks, xs)):
+        assert torch.equal(out, layer.forward(x))
+
+
+def test_ep_peer_overflow_refused(layer):
+    """Receive buffers too small for the routed rows: no rank writes peer
+    memory and the refusal is raised (not a silent overflow)."""
+    from paper_2508_07329_b200.ep import PeerBuffers, PeerExpertParallelMoE, run_loopback_peer
+    rng = np.random.default_rng(5)
+    W, T = 2, (500, 500)
+    xs = [_x(rng, t, layer.d) for t in T]
+    pl = ExpertPlacement.sharded(layer.E, W)
+    bufs = PeerBuffers.loopback(W, layer.d, 64, max(T) * layer.k)
+    ranks = [PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, bufs[r],
+                                   rank=r, exchange=_Local(W, r)) for r in range(W)]
+    sentinel = [b.codes.clone() for b in bufs]
+    with pytest.raises(RuntimeError, match="exchange refused"):
+        run_loopback_peer(ranks, xs)
+    for b, s in zip(bufs, sentinel):
+        assert torch.equal(b.codes, s)
+
+
+def test_ep_forward_host_stream(layer):
+    """EP serving loop from pinned host batches equals the device forward."""
+    from paper_2508_07329_b200.ep import PeerBuffers, PeerExpertParallelMoE
+    rng = np.random.default_rng(6)
+    pl = ExpertPlacement.sharded(layer.E, 1)
+    bufs = PeerBuffers.loopback(1, layer.d, 2 * 700 * layer.k, 700 * layer.k)[0]
+    ep = PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(0)), pl, bufs)
+    xs = [_x(rng, t, layer.d) for t in (700, 300, 512)]
+    batches = [(x.cpu().pin_memory(), None) for x in xs]
+    outs = ep.forward_host_stream(batches)
+    for x, o in zip(xs, outs):
+        assert torch.equal(o, layer.forward(x).cpu())
