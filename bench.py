@@ -35,6 +35,8 @@ sys.path.insert(0, str(ROOT))
 E, D, F, TOPK = 8, 4096, 14336, 2
 OPS_PER_TOKEN = TOPK * 6 * D * F + 2 * D * E          # 704.6 M int8 ops / token
 WORKLOAD = "C4: Mixtral-8x7B-shape single MoE layer (8 experts, top-2, d=4096, ffn=14336), W8A8"
+WORKLOAD_C5 = ("C5: Mixtral-8x7B-shape {L}-layer W8A8 MoE token path (pre-norm residual blocks, RMSNorm fused with "
+               "the residual add, attention omitted), expert-parallel with statistics-driven placement at N > 1")
 
 
 def parse():
@@ -53,6 +55,9 @@ def parse():
                     help="EP: peer-memory fused dispatch/combine (symmetric memory) or NCCL all-to-all")
     ap.add_argument("--ep-stage1", type=int, default=1, help="EP (N>1): plan_two_stage path residents per layer")
     ap.add_argument("--ep-stage2", type=int, default=1, help="EP (N>1): frequency supplement per layer")
+    ap.add_argument("--layers", type=int, default=1,
+                    help="MoE layers: 1 = config C4 (one layer, the default); 32 = config C5 (the 32-layer "
+                         "Mixtral-shape token path, pre-norm residual blocks, attention omitted)")
     return ap.parse_args()
 
 
@@ -142,11 +147,11 @@ def measured_peaks() -> dict:
 
 # ── CPU reference path (oracle, test infrastructure; timed, never shipped) ──
 def cpu_moe_baseline(experts_host: list, gate_w: np.ndarray, gate_b, x: np.ndarray, tokens: int,
-                     warmup: int, runs: int, budget_s: float | None = None) -> dict:
+                     warmup: int, runs: int, budget_s: float | None = None, layers: int = 1) -> dict:
     """The oracle's reference-style float64 fake-quant MoE layer on ``tokens``
     tokens: ``warmup`` untimed runs, then ``runs`` timed runs (stopping early
     once ``budget_s`` of timed CPU work is spent, if given); value = tokens /
-    mean run time."""
+    mean run time (/ ``layers`` for the stack: every layer costs the same)."""
     from oracle import moe_ref as M
     from oracle import quant_ref as Q
 
@@ -168,11 +173,25 @@ def cpu_moe_baseline(experts_host: list, gate_w: np.ndarray, gate_b, x: np.ndarr
         if budget_s is not None and time.perf_counter() - t_all > budget_s:
             break
     mean = sum(times) / len(times)
-    return {"value": tokens / mean, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+    per = f"; one layer timed, tokens/s divided by {layers} layers" if layers > 1 else ""
+    return {"value": tokens / mean / layers, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{tokens} tokens per run, {warmup} warm-up + {len(times)} timed runs (mean), "
                       f"Mixtral-shape layer, all 8 experts, float64 fake-quant (oracle/moe_ref."
-                      f"moe_forward_fakequant), weights pre-dequantized, numpy/OpenBLAS on all host threads",
-            "seconds_per_run": mean, "runs": len(times), "warmup_runs": warmup}
+                      f"moe_forward_fakequant), weights pre-dequantized, numpy/OpenBLAS on all host threads{per}",
+            "seconds_per_run": mean * layers, "runs": len(times), "warmup_runs": warmup}
+
+
+def stack_roofline(T: int, layers: int, ms: float, peaks: dict) -> dict:
+    """C5: the whole L-layer step against the int8 tensor peak (the grouped
+    GEMMs dominate every layer, SURVEY.md §8d work per token x L)."""
+    ops = T * layers * OPS_PER_TOKEN
+    tops = ops / (ms / 1000.0) / 1e12
+    peak = 2.0 * float(peaks["bf16_tflops"])
+    return {"bound": "tensor", "kernel": f"whole {layers}-layer step (router .. combine, all kernels)",
+            "achieved": tops, "peak": peak, "unit": "TOPS (int8)", "frac": tops / peak, "traffic": None,
+            "traffic_note": "no per-kernel capture for the stack (see the single-layer line)",
+            "peak_note": f"int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops (source={peaks.get('source')})",
+            "algorithmic_ops_per_step": ops, "frac_of_spec_4500": tops / 4500.0}
 
 
 def gemm_roofline(T: int, stages: dict, peaks: dict) -> dict:
@@ -245,13 +264,16 @@ def run_reference(args) -> None:
     x = synth_tokens(args.cpu_tokens, D, 0)
     # every step = one bounded sample (cpu_tokens tokens) of the workload: W
     # untimed warm-up steps, then exactly K timed steps
-    cb = cpu_moe_baseline(experts, gw, None, x, args.cpu_tokens, args.warmup, args.steps)
+    cb = cpu_moe_baseline(experts, gw, None, x, args.cpu_tokens, args.warmup, args.steps, layers=args.layers)
     v = cb["value"]
-    line = {"impl": "reference", "metric": "W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)", "value": v,
+    metric = ("W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)" if args.layers == 1 else
+              f"W8A8 MoE-stack tokens/s (Mixtral-8x7B shape, {args.layers} MoE layers, attention omitted)")
+    line = {"impl": "reference", "metric": metric, "value": v,
             "unit": "tokens/s", "n_gpus": args.gpus, "steps": cb["runs"], "warmup": cb["warmup_runs"],
             "ms_per_step": 1000.0 * cb["seconds_per_run"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64 (fake-quant int8)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "tokens_per_step": args.cpu_tokens, "experts": E, "top_k": TOPK,
+            "config": {"workload": WORKLOAD if args.layers == 1 else WORKLOAD_C5.format(L=args.layers),
+                       "layers": args.layers, "tokens_per_step": args.cpu_tokens, "experts": E, "top_k": TOPK,
                        "d": D, "ffn": F},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
@@ -302,33 +324,60 @@ def main() -> None:
 
     lib = _lib.load()
     T = args.tokens
-    layer = MoELayer.random(E, D, F, top_k=TOPK, seed=1)
+    L_ = args.layers
+    if L_ > 1:
+        from paper_2508_07329_b200.moe import MoEStack
+        stack = MoEStack.random(L_, E, D, F, top_k=TOPK, seed=1)
+        layer = stack.layers[0]
+    else:
+        stack = None
+        layer = MoELayer.random(E, D, F, top_k=TOPK, seed=1)
     x_np = synth_tokens(T, D, seed=100 + rank)
     x_host = torch.from_numpy(x_np).to(torch.bfloat16).pin_memory()
     x_dev = x_host.cuda()
     torch.cuda.synchronize()
     ep_info = None
-    model = layer
+    model = stack if stack is not None else layer
     if world > 1 or args.ep:
         try:
             # expert parallelism: plan_two_stage over the GPU-measured routing of
-            # all ranks -> replicated residents, the rest bin-packed (ep.py)
-            from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertParallelMoE, PeerBuffers,
-                                                  PeerExpertParallelMoE, plan_placement)
-            placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
-            backend = CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank))
+            # all ranks -> replicated residents, the rest load-split (ep.py)
+            from paper_2508_07329_b200.ep import (CudaExpertBackend, ExpertParallelMoE, ExpertParallelStack,
+                                                  PeerBuffers, PeerExpertParallelMoE, plan_placement,
+                                                  plan_stack_placements)
+            from paper_2508_07329_b200.trace import RoutingStats
+            # receive capacity: every rank could route all its tokens to one owner
+            bufs = None
             if args.ep_transport == "peer":
-                # receive capacity: every rank could route all its tokens to one owner
                 bufs = (PeerBuffers.symmetric(D, world * T * TOPK, T * TOPK) if world > 1
                         else PeerBuffers.loopback(1, D, T * TOPK, T * TOPK)[0])
-                model = PeerExpertParallelMoE(backend, placement, bufs)
+            if stack is not None:
+                stats = RoutingStats(L_, E, TOPK)
+                stack(x_dev, stats=stats)
+                placements = plan_stack_placements(stats, world, args.ep_stage1, args.ep_stage2)
+                model = ExpertParallelStack.from_stack(stack, placements, rank, bufs, transport=args.ep_transport)
+                counts = stats.counts.cpu().numpy()
+                ep_info = {"transport": args.ep_transport,
+                           "local_fraction_est": float(np.mean([pl.local_fraction(c)
+                                                                for pl, c in zip(placements, counts)])),
+                           "max_over_mean_load_est": float(np.mean([pl.rank_loads(c).max() / pl.rank_loads(c).mean()
+                                                                    for pl, c in zip(placements, counts)])),
+                           "experts_held_per_layer": float(np.mean([len(pl.local_experts(rank))
+                                                                    for pl in placements]))}
+                for lay in stack.layers:          # this rank keeps only its local experts' weights
+                    del lay.w13, lay.w2
             else:
-                model = ExpertParallelMoE(backend, placement)
-            counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
-            ep_info = {"transport": args.ep_transport, "replicated": list(placement.replicated),
-                       "owner": list(placement.owner),
-                       "local_fraction_est": placement.local_fraction(counts)}
-            del layer.w13, layer.w2            # this rank keeps only its local experts' weights
+                placement = plan_placement(layer.route(x_dev)[1], E, TOPK, world, args.ep_stage1, args.ep_stage2)
+                backend = CudaExpertBackend.from_layer_spec(layer, placement.local_experts(rank))
+                model = (PeerExpertParallelMoE(backend, placement, bufs) if bufs is not None
+                         else ExpertParallelMoE(backend, placement))
+                counts = np.bincount(layer.route(x_dev)[1].cpu().numpy().ravel(), minlength=E)
+                ep_info = {"transport": args.ep_transport, "replicated": list(placement.replicated),
+                           "holders": [list(placement.holders(e)) for e in range(E)],
+                           "local_fraction_est": placement.local_fraction(counts),
+                           "max_over_mean_load_est": float(placement.rank_loads(counts).max()
+                                                           / placement.rank_loads(counts).mean())}
+                del layer.w13, layer.w2            # this rank keeps only its local experts' weights
             torch.cuda.empty_cache()
             ep_error = None
         except Exception as exc:
@@ -341,7 +390,10 @@ def main() -> None:
             model.forward(x_dev)                            # one EP forward before the timing
             torch.cuda.synchronize()
         else:                                               # labelled fallback: independent replicas
-            model = layer if hasattr(layer, "w13") else MoELayer.random(E, D, F, top_k=TOPK, seed=1)
+            if stack is not None:
+                model = stack if hasattr(stack.layers[-1], "w13") else MoEStack.random(L_, E, D, F, top_k=TOPK, seed=1)
+            else:
+                model = layer if hasattr(layer, "w13") else MoELayer.random(E, D, F, top_k=TOPK, seed=1)
             ep_info = {"fallback": "replicas (no exchange)", "error": ep_error or "failed on another rank"}
             torch.cuda.synchronize()
 
@@ -432,26 +484,28 @@ def main() -> None:
                "h2d_gbs_raw": nbytes / c0.elapsed_time(c1) / 1e6, "d2h_gbs_raw": nbytes / c1.elapsed_time(c2) / 1e6}
 
     # ---- roofline of the dominant kernel (grouped W8A8 GEMMs) --------------
-    roofline = gemm_roofline(T, stages, measured_peaks())
+    roofline = gemm_roofline(T, stages, measured_peaks()) if L_ == 1 else stack_roofline(T, L_, ms, measured_peaks())
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         experts_host = [layer.expert_host(e) for e in range(E)]
         cpu = cpu_moe_baseline(experts_host, layer.gate_w.cpu().numpy(),
                                None if layer.gate_b is None else layer.gate_b.cpu().numpy(),
-                               x_host.float().numpy(), args.cpu_tokens, 1, 50, args.cpu_seconds)
+                               x_host.float().numpy(), args.cpu_tokens, 1, 50, args.cpu_seconds, layers=L_)
 
     if rank == 0:
         value = T * world / (ms / 1000.0)
+        metric = ("W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)" if L_ == 1 else
+                  f"W8A8 MoE-stack tokens/s (Mixtral-8x7B shape, {L_} MoE layers, attention omitted)")
         line = {
-            "metric": "W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)", "value": value, "unit": "tokens/s",
+            "metric": metric, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
+            "config": {"workload": WORKLOAD if L_ == 1 else WORKLOAD_C5.format(L=L_), "layers": L_, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
                        "top_k": TOPK, "d": D, "ffn": F, "parallelism": (f"replicas{world}" if ep_info and "fallback" in ep_info else
                                        f"ep{world}" if ep_info is not None else "1gpu"),
                        "l2": "inputs larger than L2 (x 134 MB, expert weights 1.41 GB per layer)"},
-            "int8_tops_layer": value / world * OPS_PER_TOKEN / 1e12,
+            "int8_tops_layer": value / world * OPS_PER_TOKEN * L_ / 1e12,
             "stages_ms": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches,
         }

@@ -69,6 +69,10 @@ enum { MOE_ORDER_MAX_ABS = 1, MOE_ORDER_SUM_SQUARES = 2 };
 
 /* ---- library ------------------------------------------------------------ */
 const char* moe_last_error(void);
+/* Numeric detail of the last MOE_ENOTPD on this thread: the failing pivot
+ * (0-based column, -1 if none) and its value (numkit.cholesky's
+ * NotPositiveDefiniteError(pivot, value), numkit.py:89-90). */
+moe_status moe_last_error_detail(int64_t* pivot, double* value);
 int moe_abi_version(void);
 /* Number of kernels this library has launched in the process (all entry
  * points count every launch they make) — the bench's gpu_launches. */

@@ -37,6 +37,7 @@ _P, _I64, _I, _D = C.c_void_p, C.c_int64, C.c_int, C.c_double
 # name -> (restype, argtypes)
 _SIGS = {
     "moe_last_error": (C.c_char_p, []),
+    "moe_last_error_detail": (_I, [_P, _P]),
     "moe_abi_version": (_I, []),
     "moe_launch_count": (C.c_uint64, []),
     "moe_device_check": (_I, [_I]),
@@ -142,7 +143,10 @@ def check(status: int, what: str = "") -> None:
     if status == EINVAL:
         raise ValueError(msg)
     if status == ENOTPD:
-        raise NotPositiveDefiniteError(-1, float("nan"))
+        piv, val = C.c_int64(-1), C.c_double(float("nan"))
+        if _lib is not None:
+            _lib.moe_last_error_detail(C.byref(piv), C.byref(val))
+        raise NotPositiveDefiniteError(int(piv.value), float(val.value))
     if status == EDEGENERATE:
         raise DegenerateHessianError(msg)
     if status == EQUANTFAIL:

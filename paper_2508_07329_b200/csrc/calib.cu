@@ -2,6 +2,8 @@
 // quant.py:327-343), K8 the compensated column loop of hessian_quantize
 // (quant.py:415-434) in strict reference order, and the Frobenius-loss
 // reduction used by quant_loss / search_smoothing (quant.py:267-311).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -311,6 +313,15 @@ extern "C" moe_status moe_hessian_finalize(double* H, int64_t n, double damping_
   return MOE_OK;
 }
 
+// first column i whose factor diagonal U[i, i] is not a positive finite
+// number (a U that did not come from a successful Cholesky)
+__global__ void factor_diag_check_kernel(const double* U, int64_t n, unsigned long long* first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = U[i * n + i];
+    if (!(d > 0.0) || isinf(d)) atomicMin(first, (unsigned long long)i);
+  }
+}
+
 extern "C" int64_t moe_gptq_workspace(int64_t R, int64_t n) { return R * n * (int64_t)sizeof(double); }
 
 extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, int64_t ldw, const int32_t* order,
@@ -321,6 +332,29 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
   MOE_REQUIRE(R >= 1 && n >= 1 && ldw >= n && ldc >= n, "gptq_columns: bad shape");
   MOE_REQUIRE(bits >= 2 && bits <= 8, "bits must be in [2, 8]");
   MOE_REQUIRE(err_ws_bytes >= moe_gptq_workspace(R, n), "gptq_columns: workspace too small");
+  {
+    // the column loop divides by U[i, i] (quant.py:428): a factor with a
+    // non-positive diagonal is reported as numkit.cholesky would report it
+    // (NotPositiveDefiniteError(pivot, value), numkit.py:89-90)
+    cudaStream_t s0 = as_stream(stream);
+    unsigned long long* first = nullptr;
+    MOE_CUDA_TRY(cudaMallocAsync(&first, sizeof(unsigned long long), s0));
+    MOE_CUDA_TRY(cudaMemsetAsync(first, 0xFF, sizeof(unsigned long long), s0));
+    factor_diag_check_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 256), 256, 0, s0>>>(U, n, first);
+    ::moe::count_launch();
+    unsigned long long bad = 0;
+    MOE_CUDA_TRY(cudaMemcpyAsync(&bad, first, sizeof(bad), cudaMemcpyDeviceToHost, s0));
+    MOE_CUDA_TRY(cudaFreeAsync(first, s0));
+    MOE_CUDA_TRY(cudaStreamSynchronize(s0));
+    if (bad != ~0ull) {
+      double v = 0.0;
+      MOE_CUDA_TRY(cudaMemcpy(&v, U + (int64_t)bad * n + (int64_t)bad, sizeof(double), cudaMemcpyDeviceToHost));
+      set_error_detail((int64_t)bad, v);
+      set_error("gptq_columns: factor diagonal U[" + std::to_string(bad) + ", " + std::to_string(bad) +
+                "] is not positive");
+      return MOE_ENOTPD;
+    }
+  }
   // few rows (e.g. W2 of an expert, 4096): a whole warp per row so the SMs
   // have enough independent rows; many rows: 8 lanes per row, 4 columns each
   static const int env_p = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;

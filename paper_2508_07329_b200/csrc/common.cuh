@@ -18,6 +18,8 @@
 namespace moe {
 
 void set_error(const std::string& msg);
+// (pivot, value) of the last MOE_ENOTPD (moe_last_error_detail)
+void set_error_detail(int64_t pivot, double value);
 void count_launch();  // every kernel launch of the library is counted (moe_launch_count)
 int64_t k1_small_rows();         // MOE_TUNE_K1_SMALL_ROWS
 int64_t tune_value(int key);     // any MOE_TUNE_* knob

@@ -5,6 +5,12 @@
 
 namespace moe {
 static thread_local std::string g_last_error;
+static thread_local int64_t g_err_pivot = -1;
+static thread_local double g_err_value = 0.0;
+void set_error_detail(int64_t pivot, double value) {
+  g_err_pivot = pivot;
+  g_err_value = value;
+}
 static std::atomic<unsigned long long> g_launches{0};
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -42,6 +48,12 @@ extern "C" moe_status moe_tune(int key, int64_t value, int64_t* old) {
 }
 
 extern "C" const char* moe_last_error(void) { return moe::g_last_error.c_str(); }
+
+extern "C" moe_status moe_last_error_detail(int64_t* pivot, double* value) {
+  if (pivot) *pivot = moe::g_err_pivot;
+  if (value) *value = moe::g_err_value;
+  return MOE_OK;
+}
 
 extern "C" uint64_t moe_launch_count(void) { return moe::g_launches.load(); }
 

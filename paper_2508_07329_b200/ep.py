@@ -404,6 +404,9 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         self._rank_of = backend.to_index_tensor(np.repeat(np.arange(W, dtype=np.int32), E))
         self._local_t = backend.to_index_tensor(np.asarray(self.local, dtype=np.int32))
         self._flags = []             # (event, pinned valid flag) of forwards not checked yet
+        self._flag_ring, self._flag_next = None, 0
+
+    _RING = 64
 
     def migrate(self, placement: ExpertPlacement) -> None:
         super().migrate(placement)
@@ -420,11 +423,17 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
     def peer_plan(self, offsets_all: torch.Tensor) -> torch.Tensor:
         plan = ops.ep_peer_plan(offsets_all, self.rank, self._local_t, self.bufs.codes.shape[0],
                                 self.bufs.yhome.shape[0])
-        flag = torch.empty(1, dtype=torch.int32, pin_memory=True)
-        flag.copy_(plan[:1], non_blocking=True)
+        # the valid flag goes to a pinned ring slot (no allocation per forward)
+        if self._flag_ring is None:
+            self._flag_ring = torch.empty(self._RING, dtype=torch.int32, pin_memory=True)
+        slot = self._flag_ring[self._flag_next % self._RING: self._flag_next % self._RING + 1]
+        self._flag_next += 1
+        if len(self._flags) >= self._RING:        # ring full: retire the oldest entry first
+            self.check(wait=True)
+        slot.copy_(plan[:1], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        self._flags.append((ev, flag))
+        self._flags.append((ev, slot))
         return plan
 
     def check(self, wait: bool = False) -> None:
@@ -815,3 +824,75 @@ def plan_stack_placements(stats, world: int, top_k_per_layer: int = 1, supplemen
 
 def _np(a):
     return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+
+
+# ── the 32-layer token path over expert parallelism ────────
+class ExpertParallelStack:
+    """``moe.MoEStack``'s block structure, x_{l+1} = x_l + MoE_l(RMSNorm(x_l))
+    (bf16, attention omitted), with every MoE layer expert-parallel on this
+    rank. All layers of the peer transport share ONE set of PeerBuffers: a
+    layer's peers write this rank's receive / home buffers only after the
+    cross-rank barriers of that layer, which this rank reaches only after
+    its stream has consumed the previous layer's contents."""
+
+    def __init__(self, layers: list):
+        if not layers:
+            raise ValueError("empty stack")
+        self.layers = layers
+        self.d = layers[0].be.d
+        self.out_dtype = torch.bfloat16
+
+    @classmethod
+    def from_stack(cls, stack, placements: list, rank: int, buffers: PeerBuffers | None = None, exchange=None,
+                   transport: str = "peer") -> "ExpertParallelStack":
+        """Per-layer EP modules of ``rank`` from a full ``MoEStack`` (its host
+        expert lists) and one placement per layer (``plan_stack_placements``)."""
+        if len(placements) != len(stack.layers):
+            raise ValueError(f"{len(placements)} placements for {len(stack.layers)} layers")
+        mods = []
+        for layer, pl in zip(stack.layers, placements):
+            be = CudaExpertBackend.from_layer_spec(layer, pl.local_experts(rank))
+            if transport == "peer":
+                mods.append(PeerExpertParallelMoE(be, pl, buffers, exchange, rank))
+            else:
+                mods.append(ExpertParallelMoE(be, pl, exchange, rank))
+        return cls(mods)
+
+    def forward(self, x: torch.Tensor, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        n = ops.rmsnorm_residual(x, None)[1]
+        last = len(self.layers) - 1
+        for l, m in enumerate(self.layers):
+            y = m.forward(n)
+            if l < last:
+                x, n = ops.rmsnorm_residual(x, y)
+            else:
+                x = ops.rmsnorm_residual(x, y, want_norm=False)[0]
+        if timer is not None:
+            timer.mark("stack")
+        if out is not None:
+            out.copy_(x)
+            return out
+        return x
+
+    __call__ = forward
+
+    def check(self, wait: bool = False) -> None:
+        for m in self.layers:
+            if hasattr(m, "check"):
+                m.check(wait)
+
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        x = x_host.to(self.layers[0].be.device, non_blocking=True)
+        y = self.forward(x)
+        if out_host is None:
+            out_host = torch.empty(tuple(y.shape), dtype=y.dtype, pin_memory=True)
+        out_host.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.check(wait=True)
+        return out_host
+
+    def forward_host_stream(self, batches: list, depth: int = 2) -> list:
+        from .hostio import stream_batches
+        outs = stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth)
+        self.check(wait=True)
+        return outs

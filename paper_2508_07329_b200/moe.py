@@ -405,7 +405,7 @@ class MoEStack:
         """bf16(x + y), the block's residual add (same kernel)."""
         return ops.rmsnorm_residual(x, y, want_norm=False)[0]
 
-    def forward(self, x: torch.Tensor, stats=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, stats=None, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
         # one fused pass per block boundary: residual add + next block's norm
         n = self.norm(x)
         for l, layer in enumerate(self.layers):
@@ -414,9 +414,28 @@ class MoEStack:
                 x, n = ops.rmsnorm_residual(x, y)
             else:
                 x = self.residual(x, y)
+        if timer is not None:
+            timer.mark("stack")
+        if out is not None:
+            out.copy_(x)
+            return out
         return x
 
     __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        """Pinned host tokens in, host tokens out (one synchronous call)."""
+        y = self.forward(x_host.to("cuda", non_blocking=True))
+        if out_host is None:
+            out_host = torch.empty(tuple(y.shape), dtype=y.dtype, pin_memory=True)
+        out_host.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out_host
+
+    def forward_host_stream(self, batches: list, depth: int = 2) -> list:
+        """Serving loop over host batches (hostio.stream_batches)."""
+        from .hostio import stream_batches
+        return stream_batches(self, self.forward, self.d, torch.bfloat16, batches, depth)
 
 
 class _LayerStats:

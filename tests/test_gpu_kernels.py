@@ -530,3 +530,20 @@ def test_gptq_columns_bitexact_many_rows(cuda):
     got = ops.gptq_columns(torch.from_numpy(w).to(cuda), U, torch.from_numpy(sc).to(cuda),
                            torch.from_numpy(zp).to(cuda), 8)
     np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_gptq_columns_bad_factor_reports_pivot(cuda):
+    """A factor whose diagonal is not positive: MOE_ENOTPD through the C ABI,
+    raised as NotPositiveDefiniteError with the pivot and value
+    (numkit.py:89-90) from moe_last_error_detail."""
+    from paper_2508_07329_b200.errors import NotPositiveDefiniteError
+    rng = np.random.default_rng(3)
+    n = 40
+    U = torch.eye(n, dtype=torch.float64, device=cuda)
+    U[17, 17] = -0.25
+    w = torch.from_numpy(rng.normal(size=(5, n))).to(cuda)
+    sc = torch.full((5,), 0.01, dtype=torch.float64, device=cuda)
+    zp = torch.full((5,), 128, dtype=torch.int32, device=cuda)
+    with pytest.raises(NotPositiveDefiniteError) as exc:
+        ops.gptq_columns(w, U, sc, zp, 8)
+    assert exc.value.pivot == 17 and exc.value.value == -0.25
