@@ -353,7 +353,10 @@ moe_status moe_ep_unpack_params(const int32_t* params, const int32_t* index, int
  *   [valid, R, send_base[W*E], starts[G*W+1], ranks[G*W], homes[G*W],
  *   group[G*W], goff[G+1]]; valid = 0 (and R = 0) when some rank would
  *   receive more than cap rows, route more than cap_home rows, or this rank
- *   receives rows for an expert it does not hold. */
+ *   receives rows for an expert it does not hold. host_flag (optional,
+ *   pinned host memory) receives valid too, stored by the kernel through
+ *   the host mapping (no copy-engine transfer that could queue behind bulk
+ *   D2H copies of other streams). */
 moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
                                   const int32_t* gather_rows, const int32_t* token_pos, int k,
                                   const double* smooth, const double* smooth_recip,
@@ -362,7 +365,7 @@ moe_status moe_act_quant_dispatch(const void* x, int x_dtype, int64_t rows, int6
                                   const int32_t* dst_row, const float* row_weight, int64_t ldc, moe_stream_t stream);
 int64_t moe_ep_peer_plan_size(int W, int E, int G);
 moe_status moe_ep_peer_plan(const int32_t* offsets_all, int W, int E, int me, const int32_t* local, int G,
-                            int64_t cap, int64_t cap_home, int32_t* plan, moe_stream_t stream);
+                            int64_t cap, int64_t cap_home, int32_t* plan, int32_t* host_flag, moe_stream_t stream);
 moe_status moe_block_map(int64_t n, const int32_t* n_dev, int nblocks, const int32_t* block_start,
                          const int32_t* val0, const int32_t* val1, const int32_t* val2, const int32_t* valid,
                          int32_t* out0, int32_t* out1, int32_t* out2, moe_stream_t stream);

@@ -90,7 +90,7 @@ __global__ void block_map_kernel(int64_t n, const int32_t* n_dev, int nb, const 
 //   goff[G+1]          grouped-GEMM offsets of the local experts
 // Single CTA; W*E <= 4096 keys.
 __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, const int32_t* local, int G,
-                                    int64_t cap, int64_t cap_home, int32_t* plan) {
+                                    int64_t cap, int64_t cap_home, int32_t* plan, volatile int32_t* host_flag) {
   __shared__ int bad;
   const int KE = W * E, ld = KE + 1;
   auto C = [&](int s, int r, int e) { return offs[s * ld + r * E + e + 1] - offs[s * ld + r * E + e]; };
@@ -147,6 +147,7 @@ __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, c
     if (bad) for (int g = 0; g < G; ++g) goff[g] = 0;
     plan[0] = bad ? 0 : 1;
     plan[1] = (int32_t)pos;
+    if (host_flag) *host_flag = bad ? 0 : 1;   // mapped pinned memory: no copy-engine transfer
   }
 }
 
@@ -221,11 +222,19 @@ extern "C" int64_t moe_ep_peer_plan_size(int W, int E, int G) {
 }
 
 extern "C" moe_status moe_ep_peer_plan(const int32_t* offsets_all, int W, int E, int me, const int32_t* local,
-                                       int G, int64_t cap, int64_t cap_home, int32_t* plan, moe_stream_t stream) {
+                                       int G, int64_t cap, int64_t cap_home, int32_t* plan, int32_t* host_flag,
+                                       moe_stream_t stream) {
   MOE_REQUIRE(offsets_all && plan && (local || G == 0), "ep_peer_plan: null pointer");
   MOE_REQUIRE(W >= 1 && E >= 1 && W * E <= 4096 && me >= 0 && me < W && G >= 0 && G <= E,
               "ep_peer_plan: bad sizes");
-  ep_peer_plan_kernel<<<1, 256, 0, as_stream(stream)>>>(offsets_all, W, E, me, local, G, cap, cap_home, plan);
+  int32_t* hflag = nullptr;
+  if (host_flag) {
+    void* dp = nullptr;
+    MOE_REQUIRE(cudaHostGetDevicePointer(&dp, host_flag, 0) == cudaSuccess,
+                "ep_peer_plan: host_flag must be pinned (mapped) host memory");
+    hflag = static_cast<int32_t*>(dp);
+  }
+  ep_peer_plan_kernel<<<1, 256, 0, as_stream(stream)>>>(offsets_all, W, E, me, local, G, cap, cap_home, plan, hflag);
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;

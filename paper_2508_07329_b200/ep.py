@@ -421,16 +421,17 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         return DispatchState(x.shape[0], perm, [x], None)
 
     def peer_plan(self, offsets_all: torch.Tensor) -> torch.Tensor:
-        plan = ops.ep_peer_plan(offsets_all, self.rank, self._local_t, self.bufs.codes.shape[0],
-                                self.bufs.yhome.shape[0])
-        # the valid flag goes to a pinned ring slot (no allocation per forward)
+        # the plan kernel also stores its valid flag into a pinned ring slot
+        # through the host mapping (no allocation, no copy-engine transfer
+        # queued behind other streams' bulk D2H copies)
         if self._flag_ring is None:
             self._flag_ring = torch.empty(self._RING, dtype=torch.int32, pin_memory=True)
         slot = self._flag_ring[self._flag_next % self._RING: self._flag_next % self._RING + 1]
         self._flag_next += 1
         if len(self._flags) >= self._RING:        # ring full: retire the oldest entry first
             self.check(wait=True)
-        slot.copy_(plan[:1], non_blocking=True)
+        plan = ops.ep_peer_plan(offsets_all, self.rank, self._local_t, self.bufs.codes.shape[0],
+                                self.bufs.yhome.shape[0], host_flag=slot)
         ev = torch.cuda.Event()
         ev.record()
         self._flags.append((ev, slot))

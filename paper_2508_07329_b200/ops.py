@@ -480,18 +480,19 @@ def block_map(n: int, block_start: torch.Tensor, val0: torch.Tensor, val1: torch
 
 
 def ep_peer_plan(offsets_all: torch.Tensor, me: int, local: torch.Tensor, cap: int, cap_home: int,
-                 out: torch.Tensor | None = None) -> torch.Tensor:
+                 out: torch.Tensor | None = None, host_flag: torch.Tensor | None = None) -> torch.Tensor:
     """Device-side exchange plan of a peer-memory EP forward (moe_ep_peer_plan):
     offsets_all [W, W*E+1] int32 (every rank's route_permute offsets over
     its W*E keys) -> int32 plan [valid, R, send_base[W*E], starts[G*W+1],
-    ranks[G*W], homes[G*W], group[G*W], goff[G+1]]."""
+    ranks[G*W], homes[G*W], group[G*W], goff[G+1]]; ``host_flag`` (pinned
+    int32, optional) receives valid from the kernel."""
     W = offsets_all.shape[0]
     E = (offsets_all.shape[1] - 1) // W
     G = local.numel()
     size = L.load().moe_ep_peer_plan_size(W, E, G)
     plan = out if out is not None else torch.empty(size, dtype=torch.int32, device=offsets_all.device)
     L.call("moe_ep_peer_plan", L.ptr(offsets_all.contiguous()), W, E, me, L.ptr(local), G, cap, cap_home,
-           L.ptr(plan), _s())
+           L.ptr(plan), host_flag.data_ptr() if host_flag is not None else None, _s())
     return plan
 
 

@@ -15,7 +15,7 @@ slice and scaled (labelled): search_smoothing and the column loop on a row
 slice (linear in R: rows are independent), build_hessian on a token slice
 (linear in T), the inverse factor at a smaller n (cubic in n).
 
-    python tools/calib_bench.py [T] [out.json]
+    python tools/calib_bench.py [T] [out.json]   (on gpurun: write the json under gpurun_out/)
 """
 import json
 import os
