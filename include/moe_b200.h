@@ -93,10 +93,11 @@ moe_status moe_device_check(int dev);
  *   for its second GEMM, 0 (default) the separate K1 + GEMM.
  *   MOE_TUNE_FUSED_COMBINE: 1 (default) lets the top-2 MoE forward use
  *   moe_w8a8_gemm_combine, 0 the separate GEMM + combine.
- *   MOE_TUNE_K1_TOKENS: 1 (default) lets the MoE forward quantize x with
- *   moe_act_quant_tokens (x read once per token), 0 the gathered
- *   moe_act_quant. (These three are read by the host layer; same results
- *   either way.)
+ *   MOE_TUNE_K1_TOKENS: x of the MoE forward quantized token-major
+ *   (moe_act_quant_tokens, x read from HBM once per token): 2 (default) the
+ *   row kernel walking tokens in order (a token's k rows on adjacent warps,
+ *   32 warps per SM), 1 the register-resident one-warp-per-token kernel,
+ *   0 the gathered moe_act_quant. (Same results every way.)
  *   MOE_TUNE_GPTQ_LANES: lanes per weight row of the moe_gptq_columns loop
  *   (0 = automatic: 8 above 8192 rows, else 32; 8 or 32 forced).
  *   MOE_TUNE_BAND_MB: grouped-GEMM raster band — MB of activation rows kept
@@ -157,12 +158,14 @@ moe_status moe_act_quant(const void* x, int x_dtype, int64_t rows, int64_t cols,
  * output row r = token_pos[t * k + j] (t < T, j < k) holds token t of x
  * divided by smoothing row row_group[r]; every output row gets codes, scale,
  * scale_f32, zp and rowsum exactly as moe_act_quant(gather_rows = the
- * inverse of token_pos) would give. x is read once per token (all k rows
- * are encoded from registers). Requires bf16 x, cols % 8 == 0, cols <= 4096,
+ * inverse of token_pos) would give. x is read from HBM once per token (a
+ * token's k rows are encoded by adjacent warps at the same time, or from one
+ * warp's registers: MOE_TUNE_K1_TOKENS). Requires bf16 x, cols % 8 == 0,
  * 16-byte aligned rows and the three smoothing tables; MOE_EINVAL otherwise.
- * PDL-launched: x must not be written by the immediately preceding kernel
- * of the stream when that kernel triggers its dependents early (none of
- * this library's kernels that do write activations). */
+ * The register variant is PDL-launched: x must not be written by the
+ * immediately preceding kernel of the stream when that kernel triggers its
+ * dependents early (none of this library's kernels that do write
+ * activations). */
 /* K1 with producer records (row_ext, as moe_act_quant(row_ext=...)) whose
  * row count lives on the device: rows r < *rows_dev of the capacity
  * rows_cap are quantized (the expert-parallel receiver, whose row count

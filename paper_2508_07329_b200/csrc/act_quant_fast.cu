@@ -38,8 +38,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
   int64_t r_lo, r_hi;
   cta_row_range(a, rows_per_cta, r_lo, r_hi);
-  for (int64_t r = r_lo + warp; r < r_hi; r += WARPS)
-    k1_row_warp<GIVEN>(a, r, rs32_tab, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, lane);
+  for (int64_t i = r_lo + warp; i < r_hi; i += WARPS) {
+    if (a.order)   // token-major walk: item i = (token i / k, its (i % k)-th row)
+      k1_row_warp<GIVEN>(a, a.order[i], rs32_tab, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, lane,
+                         NoPoll(), i);
+    else
+      k1_row_warp<GIVEN>(a, i, rs32_tab, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, lane);
+  }
   if (a.ep.codes_tab) __threadfence_system();   // peer writes visible before the rank barrier
 }
 
@@ -756,7 +761,20 @@ bool launch_act_quant_fast(const RowArgs& a, const float* rs32, int bits, int sy
 bool launch_act_quant_tokens(const RowArgs& a, const int32_t* token_pos, int k, int64_t T, const float* rs32,
                              int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                              int32_t* zp, int32_t* rowsum, cudaStream_t s, cudaError_t* err) {
-  if (!eligible(a, rs32, codes, ldc) || a.gather || k < 1 || a.cols > 256 * 16) return false;
+  if (!eligible(a, rs32, codes, ldc) || a.gather || k < 1) return false;
+  if (tune_value(MOE_TUNE_K1_TOKENS) != 1 || a.cols > 256 * 16) {
+    // token-major walk of the row kernel: the k rows of a token go to
+    // adjacent warps of one CTA at the same time (x read from HBM once, the
+    // second read an L1/L2 hit), 32 warps per SM of 64 registers
+    RowArgs b = a;
+    b.order = token_pos;
+    b.order_k = k;
+    b.rows = T * k;
+    launch_cfg<false, 16, 2>(b, rs32, nullptr, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, s);
+    count_launch();
+    *err = cudaGetLastError();
+    return true;
+  }
   const int nvec32 = (int)((a.cols / 8 + 31) / 32);
   // one warp per token; one CTA per SM (grid-stride over the tokens)
   auto go = [&](auto kern, int warps) {

@@ -35,6 +35,11 @@ struct RowArgs {
   SmoothArgs sm;
   EpOut ep;               // optional (zero: local output arrays)
   const int32_t* rows_dev = nullptr;  // optional: the row count lives on the device (<= rows, the capacity)
+  // optional token-major walk (MoE dispatch): item i is output row order[i]
+  // of source row i / order_k, so the k rows of a token go to adjacent warps
+  // of one CTA at the same time and x is read from HBM once
+  const int32_t* order = nullptr;
+  int order_k = 1;
 };
 
 // Rows [lo, hi) of this CTA: `rows_per_cta` from the host, or, with a device
@@ -64,8 +69,8 @@ struct RowView {
   int64_t gbase;  // element offset of the smoothing table row
 };
 
-__device__ __forceinline__ RowView row_view(const RowArgs& a, int64_t r) {
-  const int64_t src = a.gather ? (int64_t)a.gather[r] : r;
+__device__ __forceinline__ RowView row_view(const RowArgs& a, int64_t r, int64_t src_item = -1) {
+  const int64_t src = src_item >= 0 ? src_item / a.order_k : a.gather ? (int64_t)a.gather[r] : r;
   const int64_t g = a.group ? (int64_t)a.group[r] : 0;
   return RowView{src * a.ldx, g * a.sm.cols};
 }

@@ -629,11 +629,12 @@ template <bool GIVEN, int NB = kBatch, typename Poll = NoPoll>
 __device__ __forceinline__ void k1_row_warp(const RowArgs& a, int64_t r, const float* __restrict__ rs32_tab,
                                             const unsigned long long* __restrict__ ext, int bits, int sym,
                                             uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
-                                            int32_t* zp, int32_t* rowsum, int lane, Poll poll = Poll()) {
+                                            int32_t* zp, int32_t* rowsum, int lane, Poll poll = Poll(),
+                                            int64_t item = -1) {
   if (ep_row_dropped(a, r)) return;
   const int nvec = (int)(a.cols / 8);
   const bool smooth = a.sm.mode == MOE_SMOOTH_DIVIDE;
-  const RowView rv = row_view(a, r);
+  const RowView rv = row_view(a, r, item);
   const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(a.x) + rv.off;
   const uint4* src = reinterpret_cast<const uint4*>(row);
   const float* tab = smooth ? rs32_tab + rv.gbase : nullptr;

@@ -25,7 +25,7 @@ static std::atomic<int64_t> g_tune[MOE_TUNE_COUNT] = {
     {64},   // router cluster tiles: tools/router_bench.py crossover
     {0},    // fused K1 in GEMM2 (off)
     {1},    // fused top-2 combine (on)
-    {1},    // token-major K1 on x (on)
+    {2},    // K1 on x: 2 token-major walk of the row kernel (146 us), 1 token kernel (182 us), 0 gathered rows
     {0},    // GPTQ lanes per row (0: automatic)
     {[] {
       const char* env = getenv("MOE_B200_BAND_MB");

@@ -228,7 +228,7 @@ extern "C" moe_status moe_act_quant_tokens(const void* x, int x_dtype, int64_t T
   cudaError_t err = cudaSuccess;
   MOE_REQUIRE(launch_act_quant_tokens(a, token_pos, k, T, smooth_recip_f32, bits, symmetric, codes, ldc, scale,
                                       scale_f32, zp, rowsum, as_stream(stream), &err),
-              "act_quant_tokens: needs bf16 x with cols % 8 == 0, cols <= 4096, 16-byte aligned rows");
+              "act_quant_tokens: needs bf16 x with cols % 8 == 0 and 16-byte aligned rows");
   MOE_CUDA_TRY(err);
   MOE_LAUNCH_CHECK();
   return MOE_OK;

@@ -106,9 +106,9 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
 
 
 def act_quant_tokens_ok(x: torch.Tensor) -> bool:
-    """Whether moe_act_quant_tokens takes x (bf16, d % 8 == 0, d <= 4096, aligned rows)."""
+    """Whether moe_act_quant_tokens takes x (bf16, d % 8 == 0, aligned rows)."""
     return (x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1 and x.shape[1] % 8 == 0
-            and x.shape[1] <= 4096 and x.stride(0) % 8 == 0 and x.data_ptr() % 16 == 0)
+            and x.stride(0) % 8 == 0 and x.data_ptr() % 16 == 0)
 
 
 def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.Tensor, *, smooth: torch.Tensor,

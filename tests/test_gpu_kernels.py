@@ -141,13 +141,16 @@ def test_act_quant_edge_values(cuda, k1_kernel):
                 np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("T,d,k,G", [(1, 8, 1, 1), (300, 512, 2, 8), (257, 1024, 4, 16), (1000, 4096, 2, 8),
-                                      (70, 2056, 3, 5), (5, 4096, 8, 8)])
-def test_act_quant_tokens_bitexact(cuda, T, d, k, G):
-    """Token-major K1 (x read once per token, all k expert rows encoded from
-    registers) == the oracle on the gathered rows, bit for bit, with
-    per-row smoothing groups, ragged d (not a multiple of 256), tie rows,
-    constant / zero / one-sided / tiny / huge rows."""
+                                      (70, 2056, 3, 5), (5, 4096, 8, 8), (40, 6144, 2, 4)])
+def test_act_quant_tokens_bitexact(cuda, T, d, k, G, mode):
+    """Token-major K1 (x read from HBM once per token; mode 1: all k expert
+    rows encoded from one warp's registers, mode 2: the row kernel walking
+    tokens in order, a token's rows on adjacent warps; d > 4096 always takes
+    mode 2) == the oracle on the gathered rows, bit for bit, with per-row
+    smoothing groups, ragged d (not a multiple of 256), tie rows, constant /
+    zero / one-sided / tiny / huge rows."""
     rng = np.random.default_rng(T * 7 + d + k)
     x = _acts(rng, T, d)
     special = [np.zeros(d), np.full(d, 5.0), np.abs(x[0]) + 1.0, -np.abs(x[0]),
@@ -164,9 +167,9 @@ def test_act_quant_tokens_bitexact(cuda, T, d, k, G):
     sd = torch.from_numpy(s).to(cuda)
     rec, rec32 = ops.reciprocal(sd, with_f32=True)
     xd = torch.from_numpy(x).to(cuda).bfloat16()
-    assert ops.act_quant_tokens_ok(xd)
-    r = ops.act_quant_tokens(xd, torch.from_numpy(pos).to(cuda), torch.from_numpy(grp).to(cuda), smooth=sd,
-                             smooth_recip=rec, smooth_recip_f32=rec32)
+    with L.tuned(L.TUNE_K1_TOKENS, mode):
+        r = ops.act_quant_tokens(xd, torch.from_numpy(pos).to(cuda), torch.from_numpy(grp).to(cuda), smooth=sd,
+                                 smooth_recip=rec, smooth_recip_f32=rec32)
     src = np.empty(T * k, np.int64)
     src[pos.ravel()] = np.repeat(np.arange(T), k)
     codes, sc, zp, rs = M.quantize_rows_grouped(x.astype(np.float64)[src], grp, s)

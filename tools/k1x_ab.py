@@ -51,6 +51,12 @@ def timed(fn):
     return {"median_us": ts[len(ts) // 2], "min_us": ts[0]}
 
 
-ref = qx()
-print(json.dumps({"lib": os.environ.get("MOE_B200_LIB", "default"), "quant_x": timed(qx), "quant_h": timed(qh),
-                  "codes_sum": int(ref["codes"].sum(dtype=torch.int64))}), flush=True)
+out = {"lib": os.environ.get("MOE_B200_LIB", "default"), "quant_h": timed(qh)}
+for rnd in range(2):
+    for mode in (1, 2):      # MOE_TUNE_K1_TOKENS: 1 token kernel, 2 token-major walk of the row kernel
+        with L.tuned(L.TUNE_K1_TOKENS, mode):
+            ref = qx()
+            out.setdefault(f"quant_x_mode{mode}", []).append(timed(qx)["median_us"])
+            out[f"codes_sum_mode{mode}"] = int(ref["codes"].sum(dtype=torch.int64))
+            out[f"codes_eq_mode{mode}"] = bool(torch.equal(ref["codes"], a1["codes"]) and torch.equal(ref["scale"], a1["scale"]))
+print(json.dumps(out), flush=True)
