@@ -67,6 +67,8 @@ FULL_METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active %"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor mem active %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe active %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
@@ -93,6 +95,20 @@ def full(path: str, tag: str):
             else:
                 cells.append("-")
         out.append(f"| `{short(r[h.index('Kernel Name')])}` | " + " | ".join(cells) + " |")
+    # top stall reasons (PC sampling) per kernel
+    st_cols = [(i, c.replace("smsp__pcsamp_warps_issue_stalled_", "")) for i, c in enumerate(h)
+               if c.startswith("smsp__pcsamp_warps_issue_stalled_") and not c.endswith("not_issued")]
+    out += ["", "Top warp stall reasons (PC sampling, share of samples):", ""]
+    for r in data:
+        vals = []
+        for i, n in st_cols:
+            try:
+                vals.append((n, float(r[i].replace(",", ""))))
+            except ValueError:
+                pass
+        tot = sum(v for _, v in vals) or 1.0
+        top = ", ".join(f"{n} {v / tot * 100:.0f}%" for n, v in sorted(vals, key=lambda x: -x[1])[:5])
+        out.append(f"- `{short(r[h.index('Kernel Name')])}`: {top}")
     (PROF / f"ncu_full_{tag}.md").write_text("\n".join(out) + "\n")
     print("\n".join(out))
 
