@@ -35,8 +35,9 @@ sys.path.insert(0, str(ROOT))
 E, D, F, TOPK = 8, 4096, 14336, 2
 OPS_PER_TOKEN = TOPK * 6 * D * F + 2 * D * E          # 704.6 M int8 ops / token
 WORKLOAD = "C4: Mixtral-8x7B-shape single MoE layer (8 experts, top-2, d=4096, ffn=14336), W8A8"
-WORKLOAD_C5 = ("C5: Mixtral-8x7B-shape {L}-layer W8A8 MoE token path (pre-norm residual blocks, RMSNorm fused with "
-               "the residual add, attention omitted), expert-parallel with statistics-driven placement at N > 1")
+WORKLOAD_C5 = ("C5: Mixtral-8x7B-shape {L}-layer W8A8 token path ({blocks}, pre-norm residual blocks, RMSNorm fused "
+               "with the residual add), expert-parallel with statistics-driven placement at N > 1")
+ATTN_INT8_OPS = 2 * D * (32 + 2 * 8) * 128 + 2 * 32 * 128 * D   # fused QKV + output projection per token
 
 
 def parse():
@@ -56,8 +57,11 @@ def parse():
     ap.add_argument("--ep-stage1", type=int, default=1, help="EP (N>1): plan_two_stage path residents per layer")
     ap.add_argument("--ep-stage2", type=int, default=1, help="EP (N>1): frequency supplement per layer")
     ap.add_argument("--layers", type=int, default=1,
-                    help="MoE layers: 1 = config C4 (one layer, the default); 32 = config C5 (the 32-layer "
-                         "Mixtral-shape token path, pre-norm residual blocks, attention omitted)")
+                    help="layers: 1 = config C4 (one MoE layer, the default); 32 = config C5 (the 32-layer "
+                         "Mixtral-shape token path, pre-norm residual blocks)")
+    ap.add_argument("--no-attention", action="store_true",
+                    help="C5 without the attention half of each block (MoE-only blocks)")
+    ap.add_argument("--seq-len", type=int, default=4096, help="C5: tokens per packed causal sequence")
     return ap.parse_args()
 
 
@@ -181,10 +185,12 @@ def cpu_moe_baseline(experts_host: list, gate_w: np.ndarray, gate_b, x: np.ndarr
             "seconds_per_run": mean * layers, "runs": len(times), "warmup_runs": warmup}
 
 
-def stack_roofline(T: int, layers: int, ms: float, peaks: dict) -> dict:
+def stack_roofline(T: int, layers: int, ms: float, peaks: dict, attention: bool = False) -> dict:
     """C5: the whole L-layer step against the int8 tensor peak (the grouped
-    GEMMs dominate every layer, SURVEY.md §8d work per token x L)."""
-    ops = T * layers * OPS_PER_TOKEN
+    GEMMs dominate every layer, SURVEY.md §8d work per token x L; with
+    attention also its W8A8 projections — the bf16 attention core is not
+    counted)."""
+    ops = T * layers * (OPS_PER_TOKEN + (ATTN_INT8_OPS if attention else 0))
     tops = ops / (ms / 1000.0) / 1e12
     peak = 2.0 * float(peaks["bf16_tflops"])
     return {"bound": "tensor", "kernel": f"whole {layers}-layer step (router .. combine, all kernels)",
@@ -267,12 +273,13 @@ def run_reference(args) -> None:
     cb = cpu_moe_baseline(experts, gw, None, x, args.cpu_tokens, args.warmup, args.steps, layers=args.layers)
     v = cb["value"]
     metric = ("W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)" if args.layers == 1 else
-              f"W8A8 MoE-stack tokens/s (Mixtral-8x7B shape, {args.layers} MoE layers, attention omitted)")
+              f"W8A8 {args.layers}-layer Mixtral token path tokens/s (MoE-only blocks)")
     line = {"impl": "reference", "metric": metric, "value": v,
             "unit": "tokens/s", "n_gpus": args.gpus, "steps": cb["runs"], "warmup": cb["warmup_runs"],
             "ms_per_step": 1000.0 * cb["seconds_per_run"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64 (fake-quant int8)", "data": "synthetic",
-            "config": {"workload": WORKLOAD if args.layers == 1 else WORKLOAD_C5.format(L=args.layers),
+            "config": {"workload": WORKLOAD if args.layers == 1 else WORKLOAD_C5.format(L=args.layers,
+                                                                                         blocks="MoE-only blocks"),
                        "layers": args.layers, "tokens_per_step": args.cpu_tokens, "experts": E, "top_k": TOPK,
                        "d": D, "ffn": F},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -327,7 +334,8 @@ def main() -> None:
     L_ = args.layers
     if L_ > 1:
         from paper_2508_07329_b200.moe import MoEStack
-        stack = MoEStack.random(L_, E, D, F, top_k=TOPK, seed=1)
+        stack = MoEStack.random(L_, E, D, F, top_k=TOPK, seed=1, attention=not args.no_attention,
+                                seq_len=args.seq_len)
         layer = stack.layers[0]
     else:
         stack = None
@@ -391,7 +399,8 @@ def main() -> None:
             torch.cuda.synchronize()
         else:                                               # labelled fallback: independent replicas
             if stack is not None:
-                model = stack if hasattr(stack.layers[-1], "w13") else MoEStack.random(L_, E, D, F, top_k=TOPK, seed=1)
+                model = stack if hasattr(stack.layers[-1], "w13") else MoEStack.random(
+                    L_, E, D, F, top_k=TOPK, seed=1, attention=not args.no_attention, seq_len=args.seq_len)
             else:
                 model = layer if hasattr(layer, "w13") else MoELayer.random(E, D, F, top_k=TOPK, seed=1)
             ep_info = {"fallback": "replicas (no exchange)", "error": ep_error or "failed on another rank"}
@@ -484,7 +493,8 @@ def main() -> None:
                "h2d_gbs_raw": nbytes / c0.elapsed_time(c1) / 1e6, "d2h_gbs_raw": nbytes / c1.elapsed_time(c2) / 1e6}
 
     # ---- roofline of the dominant kernel (grouped W8A8 GEMMs) --------------
-    roofline = gemm_roofline(T, stages, measured_peaks()) if L_ == 1 else stack_roofline(T, L_, ms, measured_peaks())
+    roofline = gemm_roofline(T, stages, measured_peaks()) if L_ == 1 else stack_roofline(T, L_, ms, measured_peaks(),
+                                                                                    not args.no_attention)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         experts_host = [layer.expert_host(e) for e in range(E)]
@@ -495,17 +505,22 @@ def main() -> None:
     if rank == 0:
         value = T * world / (ms / 1000.0)
         metric = ("W8A8 MoE-layer tokens/s (Mixtral-8x7B shape)" if L_ == 1 else
-                  f"W8A8 MoE-stack tokens/s (Mixtral-8x7B shape, {L_} MoE layers, attention omitted)")
+                  f"W8A8 {L_}-layer Mixtral token path tokens/s"
+                  + (" (MoE-only blocks)" if args.no_attention else ""))
         line = {
             "metric": metric, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD if L_ == 1 else WORKLOAD_C5.format(L=L_), "layers": L_, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
+            "config": {"workload": WORKLOAD if L_ == 1 else WORKLOAD_C5.format(
+                           L=L_, blocks="MoE-only blocks" if args.no_attention else
+                           f"attention (W8A8 QKV/O, GQA 32/8, causal SDPA, seq {args.seq_len}) + MoE"),
+                       "layers": L_, "tokens_per_gpu": T, "global_tokens": T * world, "experts": E,
                        "top_k": TOPK, "d": D, "ffn": F, "parallelism": (f"replicas{world}" if ep_info and "fallback" in ep_info else
                                        f"ep{world}" if ep_info is not None else "1gpu"),
                        "l2": "inputs larger than L2 (x 134 MB, expert weights 1.41 GB per layer)"},
-            "int8_tops_layer": value / world * OPS_PER_TOKEN * L_ / 1e12,
+            "int8_tops_layer": value / world * (OPS_PER_TOKEN + (ATTN_INT8_OPS if L_ > 1 and not args.no_attention
+                                                                else 0)) * L_ / 1e12,
             "stages_ms": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches,
         }

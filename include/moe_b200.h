@@ -423,6 +423,14 @@ moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t
  * d <= 8192, contiguous. */
 moe_status moe_rmsnorm_residual(const void* x, const void* y, void* x_out, void* norm_out, int64_t T, int64_t d,
                                 float eps, moe_stream_t stream);
+/* Attention block glue (C5 token path): rotary position embedding in place
+ * on `heads` heads of head_dim bf16 values at the start of each row of x
+ * [T, ld] (rotate-half pairs (i, i + head_dim/2)); position of row t =
+ * positions[t] (NULL: t); cos_tab / sin_tab float32 [max_pos, head_dim/2]
+ * (cos / sin of position * theta^(-2i/head_dim), built in float64 by the
+ * caller). head_dim % 16 == 0, 16-byte aligned rows. */
+moe_status moe_rope_bf16(void* x, int64_t T, int heads, int head_dim, int64_t ld, const int32_t* positions,
+                         const float* cos_tab, const float* sin_tab, moe_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ _SIGS = {
                                    _I, _P, _P, _P, _I, _I64, _P]),
     "moe_block_map": (_I, [_I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moe_ep_peer_plan_size": (_I64, [_I, _I, _I]),
+    "moe_rope_bf16": (_I, [_P, _I64, _I, _I, _I64, _P, _P, _P, _P]),
     "moe_ep_peer_plan": (_I, [_P, _I, _I, _I, _P, _I, _I64, _I64, _P, _P, _P]),
     "moe_gather_rows": (_I, [_P, _I64, _P, _I64, _I64, _P, _I64, _P]),
     "moe_ep_pack_params": (_I, [_P, _P, _P, _P, _I64, _P, _P]),

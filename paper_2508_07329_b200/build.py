@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libmoe_b200.so"
-SOURCES = ["lib.cu", "quant_kernels.cu", "act_quant_fast.cu", "gemm_i8.cu", "moe_route.cu", "calib.cu", "ep_kernels.cu", "router_tc.cu"]
+SOURCES = ["lib.cu", "quant_kernels.cu", "act_quant_fast.cu", "gemm_i8.cu", "moe_route.cu", "calib.cu", "ep_kernels.cu", "router_tc.cu", "attn_kernels.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-DNDEBUG"]

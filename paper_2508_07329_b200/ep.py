@@ -836,10 +836,11 @@ class ExpertParallelStack:
     cross-rank barriers of that layer, which this rank reaches only after
     its stream has consumed the previous layer's contents."""
 
-    def __init__(self, layers: list):
+    def __init__(self, layers: list, attn: list | None = None, seq_len: int | None = None):
         if not layers:
             raise ValueError("empty stack")
         self.layers = layers
+        self.attn, self.seq_len = attn, seq_len      # replicated attention blocks (tokens stay home)
         self.d = layers[0].be.d
         self.out_dtype = torch.bfloat16
 
@@ -857,12 +858,16 @@ class ExpertParallelStack:
                 mods.append(PeerExpertParallelMoE(be, pl, buffers, exchange, rank))
             else:
                 mods.append(ExpertParallelMoE(be, pl, exchange, rank))
-        return cls(mods)
+        return cls(mods, stack.attn, stack.seq_len)
 
     def forward(self, x: torch.Tensor, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        if timer is not None:
+            timer.mark("start")
         n = ops.rmsnorm_residual(x, None)[1]
         last = len(self.layers) - 1
         for l, m in enumerate(self.layers):
+            if self.attn is not None:
+                x, n = ops.rmsnorm_residual(x, self.attn[l](n, self.seq_len))
             y = m.forward(n)
             if l < last:
                 x, n = ops.rmsnorm_residual(x, y)

@@ -376,23 +376,37 @@ def _np(a):
 
 
 class MoEStack:
-    """A stack of W8A8 MoE layers with pre-norm residual connections,
-    x_{l+1} = x_l + MoE_l(RMSNorm(x_l)) (bf16, Mixtral's block structure),
-    the token path of SURVEY.md C5 minus attention. ``forward(x, stats=RoutingStats(L, E, k))`` records every
-    layer's routing, so ``stats.to_trace()`` is a reference trace whose
-    events are the tokens' full activation paths (trace.py:40-44) — the
-    input of placement.plan_path / plan_two_stage."""
+    """A stack of W8A8 Mixtral blocks with pre-norm residual connections,
+    x = x + Attn_l(RMSNorm(x)); x = x + MoE_l(RMSNorm(x)) (bf16) — the token
+    path of SURVEY.md C5; with ``attn=None`` the blocks are MoE-only. Every
+    residual add is fused with the next RMSNorm (``moe_rmsnorm_residual``).
+    ``forward(x, stats=RoutingStats(L, E, k))`` records every layer's
+    routing, so ``stats.to_trace()`` is a reference trace whose events are
+    the tokens' full activation paths (trace.py:40-44) — the input of
+    placement.plan_path / plan_two_stage. Attention runs on packed
+    sequences of ``seq_len`` tokens (causal)."""
 
-    def __init__(self, layers: list):
+    def __init__(self, layers: list, attn: list | None = None, seq_len: int | None = None):
         if not layers:
             raise ValueError("empty stack")
+        if attn is not None and (len(attn) != len(layers) or not seq_len):
+            raise ValueError("one attention block per layer and a seq_len are needed")
         self.layers = layers
+        self.attn = attn
+        self.seq_len = seq_len
         self.E, self.k, self.d = layers[0].E, layers[0].k, layers[0].d
 
     @classmethod
-    def random(cls, L: int, E: int, d: int, F: int, top_k: int = 2, seed: int = 1, **kw) -> "MoEStack":
-        return cls([MoELayer.random(E, d, F, top_k=top_k, seed=seed + 17 * l, router_seed=2 + 17 * l, **kw)
-                    for l in range(L)])
+    def random(cls, L: int, E: int, d: int, F: int, top_k: int = 2, seed: int = 1, attention: bool = False,
+               seq_len: int = 4096, heads: int = 32, kv_heads: int = 8, **kw) -> "MoEStack":
+        layers = [MoELayer.random(E, d, F, top_k=top_k, seed=seed + 17 * l, router_seed=2 + 17 * l, **kw)
+                  for l in range(L)]
+        attn = None
+        if attention:
+            from .attention import W8A8Attention
+            attn = [W8A8Attention.random(d, heads, kv_heads, d // heads, seed=seed + 17 * l + 5,
+                                         max_pos=max(seq_len, 1)) for l in range(L)]
+        return cls(layers, attn, seq_len if attention else None)
 
     @staticmethod
     def norm(x: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
@@ -407,8 +421,12 @@ class MoEStack:
 
     def forward(self, x: torch.Tensor, stats=None, timer=None, out: torch.Tensor | None = None) -> torch.Tensor:
         # one fused pass per block boundary: residual add + next block's norm
+        if timer is not None:
+            timer.mark("start")
         n = self.norm(x)
         for l, layer in enumerate(self.layers):
+            if self.attn is not None:
+                x, n = ops.rmsnorm_residual(x, self.attn[l](n, self.seq_len))
             y = layer.forward(n, stats=_LayerStats(stats, l) if stats is not None else None)
             if l + 1 < len(self.layers):
                 x, n = ops.rmsnorm_residual(x, y)

@@ -557,3 +557,24 @@ def w8a8_gemm_scatter(a: dict, w: dict, *, out_tab: torch.Tensor, out_rank: torc
            L.ptr(a["rowsum"]), L.ptr(wc), N, wc.stride(0), L.ptr(w["scale_f32"]), L.ptr(w["zp"]), L.ptr(w_rs), None,
            L.ptr(row_weight), L.ptr(group_offsets), num_groups, L.EPI_DEQUANT | flags, L.ptr(out_tab),
            L.ptr(out_rank), L.ptr(out_row), L.DT_BF16 if out_dtype == torch.bfloat16 else L.DT_F32, ldo, _s())
+
+
+# ── attention block glue (C5 token path) ───────────────────────────────────
+def rope_tables(max_pos: int, head_dim: int, theta: float = 1e6, device="cuda"):
+    """float32 cos / sin tables [max_pos, head_dim/2] of position *
+    theta^(-2i/head_dim), computed in float64."""
+    i = torch.arange(head_dim // 2, dtype=torch.float64, device=device)
+    inv = theta ** (-2.0 * i / head_dim)
+    ang = torch.arange(max_pos, dtype=torch.float64, device=device)[:, None] * inv[None, :]
+    return torch.cos(ang).float().contiguous(), torch.sin(ang).float().contiguous()
+
+
+def rope_(x: torch.Tensor, heads: int, head_dim: int, cos_tab: torch.Tensor, sin_tab: torch.Tensor,
+          positions: torch.Tensor | None = None) -> torch.Tensor:
+    """In place: rotary embedding of the first heads * head_dim columns of the
+    bf16 rows of x (moe_rope_bf16)."""
+    if x.dtype != torch.bfloat16 or x.stride(1) != 1:
+        raise ValueError("rope_: bf16 rows with unit column stride")
+    L.call("moe_rope_bf16", L.ptr(x), x.shape[0], heads, head_dim, x.stride(0), L.ptr(positions), L.ptr(cos_tab),
+           L.ptr(sin_tab), _s())
+    return x

@@ -248,3 +248,42 @@ def test_layer_save_load_reference_formats(cuda, small_layer, tmp_path):
     back = MoELayer.load(tmp_path)
     x = torch.from_numpy(_x(np.random.default_rng(31), 600, 512)).to(cuda).bfloat16()
     assert torch.equal(back.forward(x), small_layer.forward(x))
+
+
+def test_attention_block_stagewise(cuda):
+    """The C5 attention half (attention.W8A8Attention) against the float64
+    oracle (oracle/attn_ref.py), stage by stage on the GPU's own inputs:
+    fused W8A8 QKV projection, RoPE on q and k, causal grouped-query
+    attention of packed sequences, W8A8 output projection."""
+    from oracle import attn_ref as A
+    from paper_2508_07329_b200.attention import W8A8Attention
+
+    rng = np.random.default_rng(21)
+    d, H, Hk, hd, S, B = 256, 4, 2, 32, 64, 3
+    att = W8A8Attention.random(d, H, Hk, hd, seed=5, max_pos=128)
+    x = torch.from_numpy((rng.normal(size=(B * S, d)) * 2).astype(np.float32)).cuda().bfloat16()
+    xf = x.double().cpu().numpy()
+    wq = att.qkv.w
+    sm = att.qkv.smooth.cpu().numpy().ravel()
+    qkv_raw = att.qkv(x, out_dtype=torch.float32).double().cpu().numpy()
+    want = A.w8a8_linear(xf, wq["codes"].cpu().numpy().astype(np.int32), wq["scale"].cpu().numpy(),
+                         wq["zp"].cpu().numpy(), sm)
+    np.testing.assert_allclose(qkv_raw, want, rtol=1e-5, atol=1e-5 * np.abs(want).max())
+    qkv = att.project_qkv(x, S)
+    pos = np.arange(B * S) % S
+    base = att.qkv(x, out_dtype=torch.bfloat16).double().cpu().numpy()
+    rq = A.rope(base, H, hd, pos)
+    rk = A.rope(base[:, H * hd:], Hk, hd, pos)
+    got = qkv.double().cpu().numpy()
+    ulp = 2.0 ** -7
+    np.testing.assert_allclose(got[:, :H * hd], rq[:, :H * hd], rtol=ulp, atol=1e-3)
+    np.testing.assert_allclose(got[:, H * hd:(H + Hk) * hd], rk[:, :Hk * hd], rtol=ulp, atol=1e-3)
+    np.testing.assert_array_equal(got[:, (H + Hk) * hd:], base[:, (H + Hk) * hd:])     # v untouched
+    a = att.attend(qkv, S).double().cpu().numpy()
+    wa = A.causal_gqa(got[:, :H * hd], got[:, H * hd:(H + Hk) * hd], got[:, (H + Hk) * hd:], H, Hk, hd, S)
+    np.testing.assert_allclose(a, wa, rtol=2e-2, atol=2e-2 * np.abs(wa).max())
+    y = att(x, S).double().cpu().numpy()
+    wo = att.o.w
+    wy = A.w8a8_linear(att.attend(qkv, S).double().cpu().numpy(), wo["codes"].cpu().numpy().astype(np.int32),
+                       wo["scale"].cpu().numpy(), wo["zp"].cpu().numpy(), att.o.smooth.cpu().numpy().ravel())
+    np.testing.assert_allclose(y, wy, rtol=1e-2, atol=1e-2 * np.abs(wy).max())

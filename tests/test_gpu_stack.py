@@ -103,3 +103,25 @@ def test_stack_expert_parallel_with_migration(stack):
             m.migrate(ExpertPlacement.sharded(E, W))
     for got, w in zip(ep_stack(xs), want):
         assert torch.equal(got, w)
+
+
+def test_stack_with_attention_expert_parallel(cuda):
+    """Full Mixtral blocks (W8A8 attention + MoE, pre-norm residual): the
+    expert-parallel stack (ExpertParallelStack, one rank, peer transport
+    with the device-side plan, replicated attention) equals the
+    single-GPU stack bit for bit, and the host serving loop equals both."""
+    from paper_2508_07329_b200.ep import ExpertParallelStack
+    st = MoEStack.random(2, E, D, F, top_k=K, seed=31, attention=True, seq_len=128, heads=8, kv_heads=2)
+    assert st.attn is not None and st.attn[0].head_dim == D // 8
+    x = _x(512, 40)
+    want = st(x)
+    assert torch.isfinite(want.float()).all()
+    pls = [ExpertPlacement.sharded(E, 1) for _ in range(2)]
+    bufs = PeerBuffers.loopback(1, D, 512 * K, 512 * K)[0]
+    ep = ExpertParallelStack.from_stack(st, pls, 0, bufs)
+    assert torch.equal(ep(x), want)
+    outs = ep.forward_host_stream([(x.cpu().pin_memory(), None), (x.cpu().pin_memory(), None)])
+    for o in outs:
+        assert torch.equal(o, want.cpu())
+    with pytest.raises(ValueError):
+        st.attn[0](x[:100], 128)            # not whole sequences
