@@ -352,7 +352,7 @@ class ExpertParallelMoE:
         transport's split sizes come back to the host every forward, so this
         pipelines only the copies, not the host round trips."""
         from .hostio import stream_batches
-        return stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth)
+        return stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth, split_ends=4)
 
     def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
         """Pinned host tokens in, host tokens out (the end-to-end call)."""
@@ -506,7 +506,7 @@ class PeerExpertParallelMoE(ExpertParallelMoE):
         """Serving loop over host batches (hostio.stream_batches): the H2D of
         batch b+1 and the D2H of batch b-1 overlap batch b's EP forward."""
         from .hostio import stream_batches
-        outs = stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth)
+        outs = stream_batches(self, self.forward, self.be.d, self.be.out_dtype, batches, depth, split_ends=4)
         self.check(wait=True)
         return outs
 
@@ -899,6 +899,7 @@ class ExpertParallelStack:
 
     def forward_host_stream(self, batches: list, depth: int = 2) -> list:
         from .hostio import stream_batches
-        outs = stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth)
+        outs = stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth, split_ends=4,
+                              quantum=self.seq_len or 1)
         self.check(wait=True)
         return outs

@@ -9,13 +9,37 @@ from __future__ import annotations
 import torch
 
 
-def stream_batches(owner, forward, d: int, out_dtype, batches: list, depth: int = 2) -> list:
+def _split_ends(batches: list, d: int, out_dtype, split_ends: int, quantum: int):
+    """Allocate missing outputs; cut the first and the last batch into
+    ``split_ends`` chunks (multiples of ``quantum`` rows) so the pipeline's
+    fill (first H2D) and drain (last D2H) expose one chunk's copy, not a
+    whole batch's. Returns (work items, the callers' output tensors)."""
+    outs, items = [], []
+    last = len(batches) - 1
+    for i, (xh, oh) in enumerate(batches):
+        n = xh.shape[0]
+        if oh is None:
+            oh = torch.empty((n, d), dtype=out_dtype, pin_memory=True)
+        outs.append(oh)
+        per = (n // split_ends) // quantum * quantum
+        if split_ends > 1 and (i == 0 or i == last) and per > 0:
+            cuts = [k * per for k in range(split_ends)] + [n]
+            items += [(xh[a:b], oh[a:b]) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+        else:
+            items.append((xh, oh))
+    return items, outs
+
+
+def stream_batches(owner, forward, d: int, out_dtype, batches: list, depth: int = 2, split_ends: int = 1,
+                   quantum: int = 1) -> list:
     """batches = [(x_host, out_host | None), ...] -> the out_host tensors
     after the last D2H. ``forward(x_dev, out=o)`` must write its [n, d]
-    result into ``o`` on the current stream. The staging ring and copy
-    streams are cached on ``owner`` (``_stream_io``)."""
+    result into ``o`` on the current stream (and be row-parallel in chunks
+    of ``quantum`` rows when ``split_ends`` > 1 cuts the end batches). The
+    staging ring and copy streams are cached on ``owner`` (``_stream_io``)."""
     if not batches:
         return []
+    batches, final = _split_ends(batches, d, out_dtype, split_ends, quantum)
     T = max(x.shape[0] for x, _ in batches)
     cur = torch.cuda.current_stream()
     io = getattr(owner, "_stream_io", None)
@@ -53,4 +77,4 @@ def stream_batches(owner, forward, d: int, out_dtype, batches: list, depth: int 
             copied[i].record(d2h)
         outs.append(oh)
     d2h.synchronize()
-    return outs
+    return final

@@ -300,7 +300,9 @@ class MoELayer:
         keeps the allocator out of the loop (no cross-stream frees).
         Returns the out_host tensors after the last D2H."""
         from .hostio import stream_batches
-        return stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth)
+        # the layer is token-parallel: the first and last batches go in 4
+        # chunks, so the pipeline fill / drain expose a quarter of a copy
+        return stream_batches(self, self.forward, self.d, self.out_dtype, batches, depth, split_ends=4)
 
     # ------------------------------------------------------------------
     def save(self, out_dir) -> None:
@@ -453,7 +455,8 @@ class MoEStack:
     def forward_host_stream(self, batches: list, depth: int = 2) -> list:
         """Serving loop over host batches (hostio.stream_batches)."""
         from .hostio import stream_batches
-        return stream_batches(self, self.forward, self.d, torch.bfloat16, batches, depth)
+        return stream_batches(self, self.forward, self.d, torch.bfloat16, batches, depth, split_ends=4,
+                              quantum=self.seq_len or 1)
 
 
 class _LayerStats:
