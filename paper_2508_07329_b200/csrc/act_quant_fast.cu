@@ -50,20 +50,34 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
 // ── bulk-async (TMA) streaming variant ─────────────────────────────────────
 // Same per-row algorithm as act_quant_warp_kernel, but rows are streamed
-// through a per-warp ring of kRing x 2 KB shared-memory stages filled by
-// cp.async.bulk (one elected lane issues, an mbarrier per stage completes
-// on the byte count): 6 KB in flight per warp regardless of register
-// pressure, ~100 KB per 16-warp CTA. Rows that fit the ring (d <= 3072) are
-// held for the second pass; longer rows without records are streamed twice.
-constexpr int kChunkBytes = 2048;
-constexpr int kChunkVec = kChunkBytes / 16;   // 128 x 16 B: 4 vectors per lane
-// 3 stages (6 KB per warp, 98 KB per CTA): the rest of the SM's 256 KB stays
-// L1 and holds the expert's float32 reciprocal table (57 KB at ffn = 14336);
-// 6 stages left ~30 KB of L1 and the table loads went to L2 (368 vs 346 us)
-constexpr int kRing = 3;
+// through a per-warp ring of kRing x kChunkBytes shared-memory stages filled
+// by cp.async.bulk (one elected lane issues, an mbarrier per stage completes
+// on the byte count): 8 KB in flight per warp regardless of register
+// pressure, 128 KB per 16-warp CTA. Rows that fit the ring are held for the
+// second pass; longer rows without records are streamed twice.
+//
+// Ring shape (K1 on h at the Mixtral shape, tools/k1x_ab.py, interleaved
+// A/B): 2 x 4 KB 316 us, 3 x 2 KB 335 us, 3 x 4 KB 337 us (L1 left for the
+// expert's 57 KB float32 reciprocal table shrinks), 6 x 2 KB 368 us. Larger
+// chunks halve the per-chunk bookkeeping (ring wait, bulk issue), which
+// ncu put at ~15 % of the kernel's instructions with 2 KB chunks.
+// Deferring the rare slow vectors to one warp-wide pass per row measured
+// slower (+1-2 %) and was dropped.
+#ifndef MOE_K1_CHUNK
+#define MOE_K1_CHUNK 4096
+#endif
+#ifndef MOE_K1_RING
+#define MOE_K1_RING 2
+#endif
+constexpr int kChunkBytes = MOE_K1_CHUNK;
+constexpr int kChunkVec = kChunkBytes / 16;   // 16-byte vectors per chunk
+constexpr int kLaneVec = kChunkVec / 32;      // per lane (8 at 4 KB)
+static_assert(kChunkBytes % 512 == 0, "chunk = whole 16-byte vectors for every lane");
+constexpr int kRing = MOE_K1_RING;
 constexpr int kBulkWarps = 16;       // (24 / 32 warps with smaller rings: register spills, 476 / 550 us)
 constexpr int kVecStep = 4;     // vectors per lane processed together (119 registers, no spills; 2: 334 us, 4: 328 us)
 constexpr int kBulkSmem = kBulkWarps * kRing * (kChunkBytes + 8) + 128;
+static_assert(kLaneVec % kVecStep == 0, "a chunk's per-lane vectors come in kVecStep groups");
 
 template <bool GIVEN>
 __global__ void __launch_bounds__(kBulkWarps * 32, 1)
@@ -100,7 +114,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   auto produce = [&]() {
     if (prow >= r_hi) return;
     if (lane == 0) {
-      const int chunk = pitem % nchunks;
+      const int chunk = pitem >= nchunks ? pitem - nchunks : pitem;   // items_per_row <= 2 * nchunks
       const int64_t b0 = (int64_t)chunk * kChunkBytes;
       const uint32_t bytes = (uint32_t)min((int64_t)kChunkBytes, row_bytes - b0);
       const int st = (int)(pcount % kRing);
@@ -146,10 +160,10 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         const uint4* v = item_vec(it);
         const int64_t cb = (int64_t)k * kChunkVec + lane;
         const bool full = (int64_t)(k + 1) * kChunkVec <= nvec;
-        uint4 u[4];
-        float4 ta[4], tb[4];
+        uint4 u[kLaneVec];
+        float4 ta[kLaneVec], tb[kLaneVec];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < kLaneVec; ++b) {
           const bool ok = full || cb + 32 * b < nvec;
           u[b] = ok ? v[lane + 32 * b] : make_uint4(0u, 0u, 0u, 0u);
           const int64_t ct = ok ? cb + 32 * b : 0;
@@ -157,7 +171,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
           tb[b] = __ldg(reinterpret_cast<const float4*>(tab) + 2 * ct + 1);
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < kLaneVec; ++b) {
           if (!(full || cb + 32 * b < nvec)) continue;
           float xs[8];
           smooth8_pre(u[b], ta[b], tb[b], xs);
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
           // per-vector branches; the rare slow vectors are redone afterwards
           // from the staged copy (same lane, same addresses)
 #pragma unroll
-          for (int hf = 0; hf < 4; hf += kVecStep) {
+          for (int hf = 0; hf < kLaneVec; hf += kVecStep) {
             uint4 u[kVecStep];
             float4 ta[kVecStep], tb[kVecStep];
 #pragma unroll
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
             }
 #pragma unroll
             for (int b = 0; b < kVecStep; ++b) {
-              sum += bytesum(out[b]);
+              sum += (slowm >> b & 1u) ? 0 : bytesum(out[b]);
               __stcs(dst + cb + 32 * (hf + b), out[b]);
             }
             if (slowm) {
@@ -251,14 +265,14 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
                 const uint4 sv = slow_vec8(v[lane + 32 * (hf + b)], tab, c, srow, rrow, f);
                 cnt += sv.z;
                 const uint2 o2 = make_uint2(sv.x, sv.y);
-                sum += bytesum(o2) - bytesum(out[b]);
+                sum += bytesum(o2);
                 __stcs(dst + c, o2);
               }
             }
           }
         } else {
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < kLaneVec; ++b) {
             const int64_t c = cb + 32 * b;
             if (c < nvec) {
               const uint2 out = fast_vec8<G>(v[lane + 32 * b], c, tab, srow, rrow, f, cnt);
