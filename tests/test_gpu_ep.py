@@ -255,3 +255,29 @@ def test_ep_forward_host_stream(layer):
     outs = ep.forward_host_stream(batches)
     for x, o in zip(xs, outs):
         assert torch.equal(o, layer.forward(x).cpu())
+
+
+def test_ep_fetch_decisions_then_migrate(layer):
+    """The Eq. 7-8 predictor re-targeted to NVLink (fetch.plan_fetches) on
+    measured per-source routing: the returned placement (fetched experts
+    served on their sources) is realised by migrate on every rank and the
+    forward stays bit-identical to the single-GPU layer."""
+    from paper_2508_07329_b200 import fetch as F
+    from paper_2508_07329_b200.ep import PeerBuffers, PeerExpertParallelMoE, run_loopback_peer
+    rng = np.random.default_rng(12)
+    W, T = 4, 600
+    xs = [_x(rng, T, layer.d) for _ in range(W)]
+    per_source = np.stack([np.bincount(layer.route(x)[1].cpu().numpy().ravel(), minlength=layer.E) for x in xs])
+    pl = ExpertPlacement.sharded(layer.E, W)
+    caches = [F.FetchCache(2) for _ in range(W)]
+    # a tiny "expert" makes fetching cheap, so the rule fires for the larger row groups
+    new, dec = F.plan_fetches(pl, per_source, 0, caches, row_ms=1.4e-4, d=layer.d, expert_bytes=2e5)
+    assert any(d.kind == F.KIND_FETCH for _, _, d in dec)
+    cap_home = T * layer.k
+    bufs = PeerBuffers.loopback(W, layer.d, W * cap_home, cap_home)
+    ranks = [PeerExpertParallelMoE(CudaExpertBackend.from_layer_spec(layer, pl.local_experts(r)), pl, bufs[r],
+                                   rank=r, exchange=_Local(W, r)) for r in range(W)]
+    for m in ranks:
+        m.migrate(new)
+    for x, out in zip(xs, run_loopback_peer(ranks, xs)):
+        assert torch.equal(out, layer.forward(x))
