@@ -1,35 +1,33 @@
-"""Expert-parallel MoE forward: one process per GPU, NCCL all-to-all
-(SURVEY.md §8e).
+"""Expert-parallel MoE forward: one process per GPU.
 
 Tokens are data-parallel (each rank routes its own tokens); experts are
 placed per layer. The reference only *plans* residency (placement.py:125-176,
 evaluate_plan :179-208) for a single device; here the plan's residents become
 experts REPLICATED on every rank (always served locally, no traffic) and the
-remaining experts are SHARDED by greedy bin-packing on routing counts, so
-``evaluate_plan``'s hit rate is exactly the fraction of activations that
+remaining experts are placed by load (``ExpertPlacement.balanced``: a hot
+expert may be split over several ranks, each serving a fixed set of source
+ranks), so ``evaluate_plan``'s hit rate is the fraction of activations that
 never leave their home GPU.
 
-One forward on rank r:
+Two transports share the routing front end (K3 router, route keys =
+destination * E + expert, one counting sort over W*E keys) and the per-row
+arithmetic of the single-GPU layer, so every EP forward is bit-identical to
+``MoELayer.forward`` on the same tokens (tests/test_gpu_ep.py):
 
-  1. K3 router on the local tokens -> (idx, w) over all E experts
-  2. route_keys: key = dest_rank[e] * E + e, and route_permute over W*E keys:
-     rows for each destination are contiguous, expert-sorted within it
-  3. K1 on the sender (per-expert smoothing of the destination expert) ->
-     u8 codes [n, d] + an int32 [n, 4] sidecar (scale_f32, zp, rowsum, w):
-     dispatch moves d + 16 bytes per row instead of 2d
-  4. counts [W, E] all-to-all, then the codes / sidecar all_to_all_v
-  5. receiver: gather rows into expert-contiguous order, grouped GEMM13 +
-     SwiGLU (+ extreme records), K1 on h, grouped GEMM2 (x routing weight),
-     gather back into receive order
-  6. bf16 rows all_to_all_v back to their home rank, K6 combine
-
-The per-row arithmetic is the single-GPU path's (same K1 rows, exact int32
-accumulators, same epilogues), so an EP forward is bit-identical to
-``MoELayer.forward`` on the same tokens (tests/test_gpu_ep.py).
+* ``PeerExpertParallelMoE`` (default) — fused dispatch / combine over peer
+  memory with a device-side exchange plan: the routing offsets of all ranks
+  are all-gathered on the device, ``moe_ep_peer_plan`` lays out every send
+  base, receive block and grouped-GEMM offset, K1 writes each row straight
+  into its owner's receive buffer, the owner's GEMM2 epilogue writes each
+  output row straight into the home rank's buffer, the home rank combines.
+  No host round trip inside a forward.
+* ``ExpertParallelMoE`` — the NCCL baseline: counts all-to-all, codes /
+  sidecar all_to_all_v, receiver regroup, grouped GEMMs, bf16 rows back.
 
 The compute is behind a small backend interface (``CudaExpertBackend`` is the
 product; tests plug a float64 CPU backend into the same runtime to check the
-host logic and the gloo exchange at world size 2).
+host logic and the gloo exchange at world size 2). ``ExpertParallelStack``
+runs the 32-layer token path on top of either transport.
 """
 
 from __future__ import annotations

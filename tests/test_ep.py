@@ -272,3 +272,38 @@ def test_ep_gloo_world2_split_expert():
         for r in range(2):
             got, want = np.load(os.path.join(d, f"r{r}.npy"))
             np.testing.assert_array_equal(got, want)
+
+
+def test_balanced_placement_properties():
+    """Randomised invariants of ExpertPlacement.balanced (hypothesis):
+    every (source, expert) goes to a holder of the expert, holders serve
+    their own tokens, replicated experts stay local, the busiest rank is
+    never worse than one-holder packing and is within one source unit of
+    the mean whenever the split placement is the one chosen."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=120, deadline=None)
+    @given(W=st.integers(1, 12), E=st.integers(1, 24), seed=st.integers(0, 10 ** 6), nrep=st.integers(0, 3))
+    def check(W, E, seed, nrep):
+        rng = np.random.default_rng(seed)
+        counts = rng.zipf(1.5, E).astype(np.int64) * rng.integers(1, 50)
+        rep = tuple(sorted(set(rng.choice(E, min(nrep, E), replace=False).tolist())))
+        pl = ExpertPlacement.balanced(counts, W, rep)
+        whole = ExpertPlacement.from_counts(counts, W, rep)
+        for s in range(W):
+            d = pl.dest_table(s)
+            for e in range(E):
+                assert d[e] in pl.holders(e)
+                if e in rep or s in pl.holders(e):
+                    assert d[e] == s
+        lb, lw = pl.rank_loads(counts), whole.rank_loads(counts)
+        assert lb.max() <= lw.max() + 1e-9
+        assert lb.sum() == pytest.approx(counts.sum())
+        if pl != whole:
+            nonrep = [e for e in range(E) if e not in rep]
+            unit = max(counts[e] for e in nonrep) / W
+            rep_load = sum(counts[e] for e in rep) / W
+            assert lb.max() <= (counts[nonrep].sum() / W + rep_load) + unit + 1e-9
+
+    check()
