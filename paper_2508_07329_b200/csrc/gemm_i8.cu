@@ -146,6 +146,22 @@ __device__ __forceinline__ TileInfo map_tile(int t, int G, const int* tile_start
   return TileInfo{g, off[g] + m_tile * TM, off[g + 1], n_tile * BN};
 }
 
+// Debug variant (-DMOE_GEMM_PROFILE=1, tools/gemm_waits.py): the MMA
+// issuer and the producer accumulate the cycles they spend waiting on each
+// barrier into a __device__ table (per CTA: [mma_tempty, mma_full,
+// prod_empty, total]); off by default.
+#ifndef MOE_GEMM_PROFILE
+#define MOE_GEMM_PROFILE 0
+#endif
+#if MOE_GEMM_PROFILE
+__device__ unsigned long long g_gemm_waits[1024][6];
+#define MOE_PROF_T0() const long long _t0 = clock64()
+#define MOE_PROF_ADD(slot) atomicAdd(&g_gemm_waits[blockIdx.x][slot], (unsigned long long)(clock64() - _t0))
+#else
+#define MOE_PROF_T0()
+#define MOE_PROF_ADD(slot)
+#endif
+
 __device__ __forceinline__ uint64_t l2_policy(int which) {
   uint64_t pol;
   if (which == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -771,7 +787,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
+        {
+          MOE_PROF_T0();
+          mbar_wait(&empty[s], ph ^ 1);
+          MOE_PROF_ADD(2);
+        }
         uint8_t* sa = smem + s * L::kStage;
         uint8_t* sb = sa + L::kA;
         if (CG == 2) {
@@ -791,15 +811,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr uint32_t idesc = idesc_i8(TM, BN);
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0, tile_it = 0;
+#if MOE_GEMM_PROFILE
+    const long long _tall = clock64();
+#endif
     for (int t = unit; t < total_tiles; t += n_units, ++tile_it) {
       const uint32_t as = tile_it & 1, aph = (tile_it >> 1) & 1;
-      mbar_wait(&tempty[as], aph ^ 1);
+      {
+        MOE_PROF_T0();
+        mbar_wait(&tempty[as], aph ^ 1);
+        MOE_PROF_ADD(0);
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + as * BN;
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+        {
+          MOE_PROF_T0();
+          mbar_wait(&full[s], ph);
+          MOE_PROF_ADD(kb < STAGES ? 4 : 1);   // tile start vs steady state
+        }
         tc_fence_after();
         const uint32_t a_addr = smem_u32(smem + s * L::kStage);
         const uint32_t b_addr = a_addr + L::kA;
@@ -818,6 +849,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (CG == 2) umma_commit_pair(&tfull[as]);
       else umma_commit(&tfull[as]);
     }
+#if MOE_GEMM_PROFILE
+    atomicAdd(&g_gemm_waits[blockIdx.x][3], (unsigned long long)(clock64() - _tall));
+#endif
   } else if (warp >= 4) {
     // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
     const int q = warp & 3;            // TMEM lane quarter this warp may access
@@ -1292,3 +1326,15 @@ extern "C" moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t
                     group_offsets, num_groups, epilogue & ~MOE_EPI_FLAG_WS_ZEROED, y, MOE_DT_BF16, ldy, nullptr, 0,
                     nullptr, 0, nullptr, nullptr, nullptr, nullptr, stream, nullptr, &cb);
 }
+
+#if MOE_GEMM_PROFILE
+extern "C" int moe_debug_gemm_waits(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_gemm_waits, sizeof(g_gemm_waits));
+  if (reset) {
+    static unsigned long long zeros[1024][6] = {};
+    cudaMemcpyToSymbol(g_gemm_waits, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
