@@ -100,16 +100,28 @@ __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, c
   int32_t* homes = ranks + G * W;
   int32_t* group = homes + G * W;
   int32_t* goff = group + G * W;
+  __shared__ int32_t tot[4096];   // rows of all senders for key (r, e)
+  __shared__ int32_t pre[4096];   // rows of senders before `me` for key (r, e)
   if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  // sender side: one thread per (r, e)
   for (int key = threadIdx.x; key < KE; key += blockDim.x) {
     const int r = key / E, e = key % E;
-    int64_t base = 0;
-    for (int e2 = 0; e2 < e; ++e2)
-      for (int s = 0; s < W; ++s) base += C(s, r, e2);
-    for (int s = 0; s < me; ++s) base += C(s, r, e);
-    send_base[key] = (int32_t)base;
+    int32_t t = 0, b = 0;
+    for (int s = 0; s < W; ++s) {
+      const int32_t c = C(s, r, e);
+      t += c;
+      if (s < me) b += c;
+    }
+    tot[key] = t;
+    pre[key] = b;
+  }
+  __syncthreads();
+  // sender side: receiver r's buffer is expert-major, sender-minor
+  for (int r = threadIdx.x; r < W; r += blockDim.x) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      send_base[r * E + e] = run + pre[r * E + e];
+      run += tot[r * E + e];
+    }
   }
   // capacity checks (every rank evaluates the same global counts)
   for (int r = threadIdx.x; r < W; r += blockDim.x) {
