@@ -116,9 +116,16 @@ class Clocks:
         use = inside or [r for _, r in good]
         sm = [float(r[2]) for r in use]
         mx = [float(r[3]) for r in use]
+        pw = []
+        for r in use:
+            try:
+                pw.append(float(r[4]))
+            except ValueError:
+                pass
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({n for r in use for n, v in zip(names, r[6:10]) if v.strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w": statistics.median(pw) if pw else None,
                 "reasons": reasons, "samples_in_timed_region": len(inside), "samples_total": len(good)}
 
 
