@@ -162,3 +162,20 @@ def test_abi_argument_errors_without_gpu():
     assert lib.moe_tune(99, 1, P) == _lib.EINVAL and b"unknown key" in lib.moe_last_error()
     # rmsnorm: d must be a multiple of 8
     assert lib.moe_rmsnorm_residual(16, P, P, 16, 4, 12, 1e-5, P) == _lib.EINVAL
+
+
+def test_hostio_split_ends():
+    """The serving loop cuts only the first and last batch into chunks
+    (multiples of the quantum rows) and returns the callers' outputs."""
+    import torch
+    from paper_2508_07329_b200.hostio import _split_ends
+    xs = [torch.zeros((n, 4)) for n in (16384, 100, 8192)]
+    outs = [torch.empty((n, 4)) for n in (16384, 100, 8192)]
+    items, final = _split_ends(list(zip(xs, outs)), 4, torch.float32, 4, 1)
+    assert [it[0].shape[0] for it in items] == [4096] * 4 + [100] + [2048] * 4
+    assert all(a is b for a, b in zip(final, outs))
+    assert items[1][1].data_ptr() == outs[0][4096:].data_ptr()          # views into the caller's buffer
+    items, _ = _split_ends(list(zip(xs, outs)), 4, torch.float32, 4, 4096)
+    assert [it[0].shape[0] for it in items] == [4096] * 4 + [100] + [8192]   # 8192 / 4 < quantum: whole
+    items, _ = _split_ends(list(zip(xs, outs)), 4, torch.float32, 1, 1)
+    assert len(items) == 3
