@@ -74,6 +74,122 @@ __global__ void __launch_bounds__(256) hessian_accum_kernel(const void* x, int d
   if (nonzero && nz) atomicAdd(nonzero, nz);
 }
 
+// ── K7 on the FP64 tensor cores (DMMA m8n8k4) ───────────────────────────────
+// 128 x 128 upper-triangle tiles of H, 8 warps as 4 (rows) x 2 (columns),
+// each warp 32 x 64 = 4 x 8 DMMA tiles (64 float64 accumulators per
+// thread). Tokens stream through double-buffered shared-memory stages of 16
+// (x / s applied on the load, exactly as the SIMT kernel does); rows of a
+// stage are padded to 136 doubles so the fragment loads of a warp (4 token
+// rows x 8 channels) take the minimum two wavefronts.
+constexpr int kHD = 128;           // output tile
+constexpr int kHDK = 16;           // tokens per stage
+constexpr int kHDLd = kHD + 8;     // padded row (doubles)
+constexpr int kHDSmem = 2 * 2 * kHDK * kHDLd * (int)sizeof(double);   // 2 stages x (a, b)
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) hessian_dmma_kernel(const void* x, int dt, int64_t T, int64_t n, int64_t ldx,
+                                                           const double* s, const double* rs, double* H,
+                                                           unsigned long long* nonzero) {
+  extern __shared__ __align__(16) double hsm[];
+  const int nt = (int)((n + kHD - 1) / kHD);
+  int b = blockIdx.x, bi = 0;
+  while (b >= nt - bi) {
+    b -= nt - bi;
+    ++bi;
+  }
+  const int bj = bi + b;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;             // 4 x 2 warps: rows 32 wm.., cols 64 wn..
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  unsigned long long nz = 0;
+  auto stage_a = [&](int st) { return hsm + (size_t)st * 2 * kHDK * kHDLd; };
+  auto stage_b = [&](int st) { return hsm + (size_t)st * 2 * kHDK * kHDLd + kHDK * kHDLd; };
+  // a stage's elements go through registers: the global loads of stage
+  // ks + 1 are issued before the DMMAs of stage ks and only consumed
+  // (smoothing division, shared-memory store) after them
+  constexpr int kPer = kHDK * kHD / 256;               // elements per thread per operand
+  double ra[kPer], rb[kPer];
+  auto fetch = [&](int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = threadIdx.x + q * 256;
+      const int tt = i / kHD, c = i % kHD;
+      const int64_t t = t0 + tt;
+      const int64_t ca = (int64_t)bi * kHD + c, cb = (int64_t)bj * kHD + c;
+      ra[q] = (t < T && ca < n) ? load_as_f64(x, t * ldx + ca, dt) : 0.0;
+      rb[q] = (bi != bj && t < T && cb < n) ? load_as_f64(x, t * ldx + cb, dt) : 0.0;
+    }
+  };
+  auto commit = [&](int st) {
+    double* xa = stage_a(st);
+    double* xb = stage_b(st);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = threadIdx.x + q * 256;
+      const int tt = i / kHD, c = i % kHD;
+      const int64_t ca = (int64_t)bi * kHD + c, cb = (int64_t)bj * kHD + c;
+      double va = ra[q], vb = rb[q];
+      if (s && ca < n) va = rs ? div_rcp(va, s[ca], rs[ca]) : __ddiv_rn(va, s[ca]);
+      if (bi == bj) {
+        nz += (va != 0.0);
+        vb = va;
+      } else if (s && cb < n) {
+        vb = rs ? div_rcp(vb, s[cb], rs[cb]) : __ddiv_rn(vb, s[cb]);
+      }
+      xa[tt * kHDLd + c] = va;
+      xb[tt * kHDLd + c] = vb;
+    }
+  };
+  const int nst = (int)((T + kHDK - 1) / kHDK);
+  fetch(0);
+  commit(0);
+  __syncthreads();
+  for (int ks = 0; ks < nst; ++ks) {
+    const int cur = ks & 1;
+    if (ks + 1 < nst) fetch((int64_t)(ks + 1) * kHDK);
+    const double* xa = stage_a(cur);
+    const double* xb = stage_b(cur);
+#pragma unroll
+    for (int k0 = 0; k0 < kHDK; k0 += 4) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = xa[(k0 + tig) * kHDLd + wm * 32 + i * 8 + gid];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bf[j] = xb[(k0 + tig) * kHDLd + wn * 64 + j * 8 + gid];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (ks + 1 < nst) commit(cur ^ 1);
+    __syncthreads();
+  }
+  // D fragment: element (gid, 2 tig + e) of each 8 x 8 tile
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = (int64_t)bi * kHD + wm * 32 + i * 8 + gid;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = (int64_t)bj * kHD + wn * 64 + j * 8 + 2 * tig + e;
+        if (r < n && c < n && (bi != bj || c >= r)) H[r * n + c] += 2.0 * acc[i][j][e];
+      }
+    }
+  }
+  if (nonzero && nz) atomicAdd(nonzero, nz);
+}
+
 // mirror the upper triangle, add damping * mean(diag) (deterministic mean)
 __global__ void hessian_diag_mean_kernel(const double* H, int64_t n, double* mean_out) {
   __shared__ double sh[256];
@@ -279,6 +395,18 @@ extern "C" moe_status moe_hessian_accum(const void* x, int x_dtype, int64_t T, i
                                         const double* smooth, const double* smooth_recip, double* H,
                                         unsigned long long* nonzero_count, moe_stream_t stream) {
   MOE_REQUIRE(x && H && T >= 1 && n >= 1 && ldx >= n, "hessian_accum: bad arguments");
+  static const bool simt = getenv("MOE_B200_K7_SIMT") != nullptr;   // A/B against the SIMT kernel
+  if (!simt && n >= 256) {
+    const int64_t nt = (n + kHD - 1) / kHD;
+    const int64_t blocks = nt * (nt + 1) / 2;
+    MOE_REQUIRE(blocks < (1LL << 31), "hessian_accum: n too large");
+    MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(hessian_dmma_kernel), kHDSmem));
+    hessian_dmma_kernel<<<(unsigned)blocks, 256, kHDSmem, as_stream(stream)>>>(x, x_dtype, T, n, ldx, smooth,
+                                                                                smooth_recip, H, nonzero_count);
+    ::moe::count_launch();
+    MOE_LAUNCH_CHECK();
+    return MOE_OK;
+  }
   const int64_t nt = (n + kHT - 1) / kHT;
   const int64_t blocks = nt * (nt + 1) / 2;
   MOE_REQUIRE(blocks < (1LL << 31), "hessian_accum: n too large");

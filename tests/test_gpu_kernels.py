@@ -550,3 +550,22 @@ def test_gptq_columns_bad_factor_reports_pivot(cuda):
     with pytest.raises(NotPositiveDefiniteError) as exc:
         ops.gptq_columns(w, U, sc, zp, 8)
     assert exc.value.pivot == 17 and exc.value.value == -0.25
+
+
+@pytest.mark.parametrize("n,T,dt", [(256, 100, "f64"), (300, 333, "f64"), (1000, 77, "bf16"), (640, 1, "f32")])
+def test_hessian_dmma_matches_oracle(cuda, n, T, dt):
+    """K7 on the FP64 tensor cores (DMMA, n >= 256): ragged tiles, a single
+    token, bf16 / f32 / f64 inputs, fused smoothing division; rtol 1e-12
+    against build_hessian (quant.py:327-343) and exactly symmetric."""
+    rng = np.random.default_rng(n + T)
+    x = rng.normal(size=(n, T))
+    x[5] *= 30
+    s = np.exp(rng.normal(size=n) * 0.5)
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    xt = torch.from_numpy(x.T.copy()).to(cuda).to(tdt)
+    xr = xt.double().cpu().numpy().T
+    Hs = ops.hessian(xt, smooth=torch.from_numpy(s).to(cuda)).cpu().numpy()
+    np.testing.assert_allclose(Hs, Q.build_hessian(xr / s[:, None]), rtol=1e-12, atol=1e-9)
+    assert np.array_equal(Hs, Hs.T)
+    with pytest.raises(Exception):
+        ops.hessian(torch.zeros((T, n), dtype=tdt, device=cuda))
