@@ -484,12 +484,15 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
     }
   }
   // few rows (e.g. W2 of an expert, 4096): a whole warp per row so the SMs
-  // have enough independent rows; many rows: 8 lanes per row, 4 columns each
+  // have enough independent rows; many rows: 16 lanes per row, 2 columns each
   static const int env_p = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
   const int64_t knob = tune_value(MOE_TUNE_GPTQ_LANES);
   const int forced = knob ? (int)knob : env_p;
-  MOE_REQUIRE(forced == 0 || forced == 8 || forced == 32, "gptq_columns: lanes per row must be 8 or 32");
-  const int P = forced ? forced : (R <= 8192 ? 32 : 8);
+  MOE_REQUIRE(forced == 0 || forced == 8 || forced == 16 || forced == 32,
+              "gptq_columns: lanes per row must be 8, 16 or 32");
+  // (tools/k8_ab.py: stacked W1||W3 [28672, 4096]: 16 lanes 99 ms, 8: 137, 32: 154;
+  //  W2 [4096, 14336]: 32 lanes 350 ms, 8: 313, 16: 695 — kept at 32 for few rows)
+  const int P = forced ? forced : (R <= 8192 ? 32 : 16);
   const unsigned blocks = (unsigned)((R + kGThreads / P - 1) / (kGThreads / P));
   auto launch = [&](auto kern, int rows_cta) -> cudaError_t {
     const int smem = (int)sizeof(double) * (2 * kGStage * kGT + 2 * kGStage * rows_cta + kGT * (kGT + 1));
@@ -499,8 +502,9 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
                                                          ldc, static_cast<double*>(err_ws));
     return cudaGetLastError();
   };
-  MOE_CUDA_TRY(P == 32 ? launch(gptq_columns_kernel<32, kGStage>, kGThreads / 32)
-                       : launch(gptq_columns_kernel<8, kGStage>, kGThreads / 8));
+  MOE_CUDA_TRY(P == 32   ? launch(gptq_columns_kernel<32, kGStage>, kGThreads / 32)
+               : P == 16 ? launch(gptq_columns_kernel<16, kGStage>, kGThreads / 16)
+                         : launch(gptq_columns_kernel<8, kGStage>, kGThreads / 8));
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;

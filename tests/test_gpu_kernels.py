@@ -510,12 +510,13 @@ def _gptq_case(rng, R, n, bits, cuda):
 
 
 @pytest.mark.parametrize("n", [4096, 14336])
-@pytest.mark.parametrize("lanes", [8, 32])
+@pytest.mark.parametrize("lanes", [8, 16, 32])
 def test_gptq_columns_bitexact_mixtral_shapes(cuda, n, lanes):
     """K8 at the Mixtral expert shapes (W1||W3: n = d = 4096; W2: n = ffn =
     14336) on a 64-row slice (rows are independent, quant.py:423-430), with
-    both lane splits forced: 8 lanes per row (4 contiguous tile columns each,
-    the double2 path used for R > 8192, i.e. the stacked W1||W3) and 32."""
+    every lane split forced: 8 lanes per row (4 contiguous tile columns
+    each), 16 (2 each: the automatic choice above 8192 rows, i.e. the
+    stacked W1||W3) and 32 (one each)."""
     rng = np.random.default_rng(n + lanes)
     w, U, sc, zp = _gptq_case(rng, 64, n, 8, cuda)
     want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
@@ -526,7 +527,7 @@ def test_gptq_columns_bitexact_mixtral_shapes(cuda, n, lanes):
 
 
 def test_gptq_columns_bitexact_many_rows(cuda):
-    """More than 8192 rows: the automatic choice is 8 lanes per row."""
+    """More than 8192 rows: the automatic choice is 16 lanes per row."""
     rng = np.random.default_rng(9)
     w, U, sc, zp = _gptq_case(rng, 8200, 96, 8, cuda)
     want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
