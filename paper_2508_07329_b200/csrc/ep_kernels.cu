@@ -57,20 +57,30 @@ __global__ void unpack_params_kernel(const int4* params, const int32_t* index, i
 // i < n (or i < *n_dev when given; binary search over nb blocks). With
 // `valid` given and *valid == 0 every out0 is -1 (a refused exchange plan:
 // consumers skip such rows instead of writing anywhere).
+constexpr int kMapSmemBlocks = 4096;   // block tables up to this size are staged in shared memory
+
 __global__ void block_map_kernel(int64_t n, const int32_t* n_dev, int nb, const int32_t* start, const int32_t* val0,
                                  const int32_t* val1, const int32_t* val2, const int32_t* valid, int32_t* out0,
                                  int32_t* out1, int32_t* out2) {
+  __shared__ int32_t s_start[kMapSmemBlocks];
   if (n_dev) n = min(n, (int64_t)*n_dev);
   const bool ok = !valid || *valid != 0;
+  // the binary search runs over a shared-memory copy of the block starts
+  // (a chain of dependent global loads per row otherwise)
+  const bool staged = nb <= kMapSmemBlocks;
+  if (staged)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_start[b] = start[b];
+  __syncthreads();
+  const int32_t* st = staged ? s_start : start;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = nb;   // last b with start[b] <= i
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (start[mid] <= i) lo = mid;
+      if (st[mid] <= i) lo = mid;
       else hi = mid;
     }
     out0[i] = ok ? val0[lo] : -1;
-    out1[i] = val1[lo] + (int32_t)(i - start[lo]);
+    out1[i] = val1[lo] + (int32_t)(i - st[lo]);
     if (out2) out2[i] = val2[lo];
   }
 }
@@ -92,8 +102,14 @@ __global__ void block_map_kernel(int64_t n, const int32_t* n_dev, int nb, const 
 __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, const int32_t* local, int G,
                                     int64_t cap, int64_t cap_home, int32_t* plan, volatile int32_t* host_flag) {
   __shared__ int bad;
+  __shared__ int32_t s_offs[3072];   // every rank's offsets, when they fit (W * (W*E + 1) ints)
   const int KE = W * E, ld = KE + 1;
-  auto C = [&](int s, int r, int e) { return offs[s * ld + r * E + e + 1] - offs[s * ld + r * E + e]; };
+  const bool staged = W * ld <= 3072;
+  if (staged)
+    for (int i = threadIdx.x; i < W * ld; i += blockDim.x) s_offs[i] = offs[i];
+  __syncthreads();
+  const int32_t* o = staged ? s_offs : offs;
+  auto C = [&](int s, int r, int e) { return o[s * ld + r * E + e + 1] - o[s * ld + r * E + e]; };
   int32_t* send_base = plan + 2;
   int32_t* starts = send_base + KE;
   int32_t* ranks = starts + G * W + 1;
@@ -128,7 +144,7 @@ __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, c
     int64_t recv = 0, home = 0;
     for (int s = 0; s < W; ++s)
       for (int e = 0; e < E; ++e) recv += C(s, r, e);
-    home = offs[r * ld + KE] - offs[r * ld];
+    home = o[r * ld + KE] - o[r * ld];
     if (recv > cap || home > cap_home) atomicOr(&bad, 1);
   }
   __syncthreads();
@@ -148,7 +164,7 @@ __global__ void ep_peer_plan_kernel(const int32_t* offs, int W, int E, int me, c
         const int b = g * W + s;
         starts[b] = (int32_t)pos;
         ranks[b] = s;
-        homes[b] = offs[s * ld + me * E + e];
+        homes[b] = o[s * ld + me * E + e];
         group[b] = g;
         pos += C(s, me, e);
       }
