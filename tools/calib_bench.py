@@ -6,6 +6,8 @@ calibration tokens.
 Per stage, GPU (CUDA events, after a warm-up) and CPU (the oracle's
 restatement of the reference function, oracle/quant_ref.py, numpy/OpenBLAS
 on all host threads, best of `reps`):
+  rtn_quantize      per-token RTN of the activations       (quant.py:214-231)
+  quant_loss        one smoothing grid point               (quant.py:267-283)
   search_smoothing  21 quant_loss evaluations            (quant.py:286-311)
   build_hessian     K7, 2 n^2 T flops (full product)      (quant.py:327-343)
   inverse factor    damped inverse + Cholesky              (quant.py:366-385)
@@ -118,7 +120,19 @@ def main():
         t = cpu_time(lambda: Q.gptq_columns(wsh, Uh, sc, zp, 255), reps=1)
         r["cpu_column_loop_s"] = t * R / rr
         r["cpu_column_loop_note"] = f"{rr}-row slice x {R / rr:.0f} (rows independent)"
-        for k in ("search_smoothing", "build_hessian", "inverse_factor", "column_loop"):
+        # a6 rtn_quantize of the calibration activations (per token, X channels x tokens) and
+        # a11 quant_loss at exponent 0.5 (one grid point of the search)
+        xtok = torch.from_numpy(x.T.copy()).cuda()
+        r["gpu_rtn_quantize_s"] = gpu_time(lambda: quant.rtn_quantize(xd, cfg))
+        t = cpu_time(lambda: Q.rtn(x, c))
+        r["cpu_rtn_quantize_s"] = t
+        f05 = np.maximum(np.abs(x).max(axis=1), 1e-8) ** 0.5
+        r["gpu_quant_loss_s"] = gpu_time(lambda: quant.quant_loss(wd, xd, f05, cfg))
+        t = cpu_time(lambda: Q.quant_loss(w[:rs], x, f05, c), reps=1)
+        r["cpu_quant_loss_s"] = t * R / rs
+        r["cpu_quant_loss_note"] = f"{rs}-row slice x {R / rs:.0f} (linear in R)"
+        del xtok
+        for k in ("search_smoothing", "build_hessian", "inverse_factor", "column_loop", "rtn_quantize", "quant_loss"):
             r[f"speedup_{k}"] = r[f"cpu_{k}_s"] / r[f"gpu_{k}_s"]
         res["shapes"][name] = r
         print(name, json.dumps(r), flush=True)
