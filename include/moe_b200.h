@@ -99,7 +99,7 @@ moe_status moe_device_check(int dev);
  *   32 warps per SM), 1 the register-resident one-warp-per-token kernel,
  *   0 the gathered moe_act_quant. (Same results every way.)
  *   MOE_TUNE_GPTQ_LANES: lanes per weight row of the moe_gptq_columns loop
- *   (0 = automatic: 16 above 8192 rows, else 32; 8, 16 or 32 forced).
+ *   (0 = automatic: 16; 8, 16 or 32 forced).
  *   MOE_TUNE_BAND_MB: grouped-GEMM raster band — MB of activation rows kept
  *   L2-resident while the weight blocks stream past them (default 24; env
  *   MOE_B200_BAND_MB sets the initial value). */

@@ -3,6 +3,7 @@
 // (quant.py:415-434) in strict reference order, and the Frobenius-loss
 // reduction used by quant_loss / search_smoothing (quant.py:267-311).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -232,7 +233,6 @@ constexpr int kGStage = MOE_GPTQ_STAGE;   // U rows per shared-memory stage (dou
 // lanes. Every element still receives its updates one at a time, separate
 // multiply and subtract, in ascending column order (quant.py:425-430), so
 // the codes equal the reference's bit for bit.
-constexpr int kGThreads = 128;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
@@ -244,12 +244,14 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int kGP, int kGS>   // lanes per row (8 or 32; lane p owns tile columns [p * kGQ, (p + 1) * kGQ)), staged U rows
-__global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
+// lanes per row kGP (lane p owns tile columns [p * kGQ, (p + 1) * kGQ)), staged
+// U rows kGS, threads per CTA NT (rows per CTA = NT / kGP share every staged U chunk)
+template <int kGP, int kGS, int NT>
+__global__ void __launch_bounds__(NT) gptq_columns_kernel(const double* W, int64_t R, int64_t n, int64_t ldw,
                                                                   const int32_t* order, const double* U,
                                                                   const double* scale, const int32_t* zp, int qmax,
                                                                   uint8_t* codes, int64_t ldc, double* err) {
-  constexpr int kGRowsCta = kGThreads / kGP;             // rows per CTA
+  constexpr int kGRowsCta = NT / kGP;                    // rows per CTA
   constexpr int kGQ = kGT / kGP;                         // tile columns per lane
   constexpr int kGU = kGS;
   extern __shared__ __align__(16) double gsm[];
@@ -279,12 +281,12 @@ __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W
     // and errors streams in (cp.async) while this one is applied
     auto stage = [&](int64_t i0, int buf) {
       const int ni = (int)((J - i0) < kGU ? (J - i0) : kGU);
-      for (int t = threadIdx.x; t < kGU * kGT; t += kGThreads) {
+      for (int t = threadIdx.x; t < kGU * kGT; t += NT) {
         const int ii = t / kGT, jj = t % kGT;
         const bool ok = ii < ni && jj < tw;
         cp_async8(&us[buf][ii][jj], ok ? U + (i0 + ii) * n + J + jj : U, ok);
       }
-      for (int t = threadIdx.x; t < kGU * kGRowsCta; t += kGThreads) {
+      for (int t = threadIdx.x; t < kGU * kGRowsCta; t += NT) {
         const int ii = t / kGRowsCta, rr = t % kGRowsCta;
         const bool ok = ii < ni && r0 + rr < R;
         cp_async8(&es[buf][ii][rr], ok ? err + (i0 + ii) * R + r0 + rr : err, ok);
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(kGThreads) gptq_columns_kernel(const double* W
       __syncthreads();   // this buffer is restaged two chunks later
     }
     // in-tile sequential part
-    for (int t = threadIdx.x; t < kGT * kGT; t += kGThreads) {
+    for (int t = threadIdx.x; t < kGT * kGT; t += NT) {
       const int ii = t / kGT, jj = t % kGT;
       ut[ii][jj] = (ii < tw && jj < tw) ? U[(J + ii) * n + J + jj] : 0.0;
     }
@@ -483,28 +485,37 @@ extern "C" moe_status moe_gptq_columns(const double* W, int64_t R, int64_t n, in
       return MOE_ENOTPD;
     }
   }
-  // few rows (e.g. W2 of an expert, 4096): a whole warp per row so the SMs
-  // have enough independent rows; many rows: 16 lanes per row, 2 columns each
   static const int env_p = getenv("MOE_B200_GPTQ_P") ? atoi(getenv("MOE_B200_GPTQ_P")) : 0;
   const int64_t knob = tune_value(MOE_TUNE_GPTQ_LANES);
   const int forced = knob ? (int)knob : env_p;
   MOE_REQUIRE(forced == 0 || forced == 8 || forced == 16 || forced == 32,
               "gptq_columns: lanes per row must be 8, 16 or 32");
-  // (tools/k8_ab.py: stacked W1||W3 [28672, 4096]: 16 lanes 99 ms, 8: 137, 32: 154;
-  //  W2 [4096, 14336]: 32 lanes 350 ms, 8: 313, 16: 695 — kept at 32 for few rows)
-  const int P = forced ? forced : (R <= 8192 ? 32 : 16);
-  const unsigned blocks = (unsigned)((R + kGThreads / P - 1) / (kGThreads / P));
-  auto launch = [&](auto kern, int rows_cta) -> cudaError_t {
+  // 16 lanes per row (2 columns each) and 256-thread CTAs (16 rows share every
+  // staged U chunk). tools/k8_ab.py, seeded, best of 3: stacked W1||W3
+  // [28672, 4096] 94-99 ms (8 lanes 137-160, 32 lanes 120-135); W2
+  // [4096, 14336] 184-186 ms (32 lanes 221-257, 8 lanes 293-527); 128- and
+  // 512-thread CTAs within 10 %.
+  const int P = forced ? forced : 16;
+  static const int env_nt = getenv("MOE_B200_GPTQ_NT") ? atoi(getenv("MOE_B200_GPTQ_NT")) : 0;
+  const int NT = env_nt == 128 || env_nt == 256 || env_nt == 512 ? env_nt : 256;
+  auto launch = [&](auto kern, int threads, int rows_cta) -> cudaError_t {
+    const unsigned blocks = (unsigned)((R + rows_cta - 1) / rows_cta);
     const int smem = (int)sizeof(double) * (2 * kGStage * kGT + 2 * kGStage * rows_cta + kGT * (kGT + 1));
     const cudaError_t e = set_max_smem_once(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    kern<<<blocks, kGThreads, smem, as_stream(stream)>>>(W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes,
-                                                         ldc, static_cast<double*>(err_ws));
+    kern<<<blocks, threads, smem, as_stream(stream)>>>(W, R, n, ldw, order, U, scale, zp, (1 << bits) - 1, codes, ldc,
+                                                       static_cast<double*>(err_ws));
     return cudaGetLastError();
   };
-  MOE_CUDA_TRY(P == 32   ? launch(gptq_columns_kernel<32, kGStage>, kGThreads / 32)
-               : P == 16 ? launch(gptq_columns_kernel<16, kGStage>, kGThreads / 16)
-                         : launch(gptq_columns_kernel<8, kGStage>, kGThreads / 8));
+  auto go = [&](auto nt) -> cudaError_t {
+    constexpr int T_ = decltype(nt)::value;
+    return P == 32   ? launch(gptq_columns_kernel<32, kGStage, T_>, T_, T_ / 32)
+           : P == 16 ? launch(gptq_columns_kernel<16, kGStage, T_>, T_, T_ / 16)
+                     : launch(gptq_columns_kernel<8, kGStage, T_>, T_, T_ / 8);
+  };
+  MOE_CUDA_TRY(NT == 512 ? go(std::integral_constant<int, 512>{})
+               : NT == 256 ? go(std::integral_constant<int, 256>{})
+                           : go(std::integral_constant<int, 128>{}));
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;

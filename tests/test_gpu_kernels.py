@@ -515,8 +515,7 @@ def test_gptq_columns_bitexact_mixtral_shapes(cuda, n, lanes):
     """K8 at the Mixtral expert shapes (W1||W3: n = d = 4096; W2: n = ffn =
     14336) on a 64-row slice (rows are independent, quant.py:423-430), with
     every lane split forced: 8 lanes per row (4 contiguous tile columns
-    each), 16 (2 each: the automatic choice above 8192 rows, i.e. the
-    stacked W1||W3) and 32 (one each)."""
+    each), 16 (2 each: the automatic choice) and 32 (one each)."""
     rng = np.random.default_rng(n + lanes)
     w, U, sc, zp = _gptq_case(rng, 64, n, 8, cuda)
     want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
@@ -527,7 +526,7 @@ def test_gptq_columns_bitexact_mixtral_shapes(cuda, n, lanes):
 
 
 def test_gptq_columns_bitexact_many_rows(cuda):
-    """More than 8192 rows: the automatic choice is 16 lanes per row."""
+    """More than 8192 rows with the automatic lane split (16 lanes per row)."""
     rng = np.random.default_rng(9)
     w, U, sc, zp = _gptq_case(rng, 8200, 96, 8, cuda)
     want = Q.gptq_columns(w, U.cpu().numpy(), sc, zp, 255)
