@@ -776,7 +776,8 @@ bool launch_act_quant_tokens(const RowArgs& a, const int32_t* token_pos, int k, 
                              int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                              int32_t* zp, int32_t* rowsum, cudaStream_t s, cudaError_t* err) {
   if (!eligible(a, rs32, codes, ldc) || a.gather || k < 1) return false;
-  if (tune_value(MOE_TUNE_K1_TOKENS) != 1 || a.cols > 256 * 16) {
+  const int mode = tune_value(MOE_TUNE_K1_TOKENS);
+  if (mode != 1 || a.cols > 256 * 16) {
     // token-major walk of the row kernel: the k rows of a token go to
     // adjacent warps of one CTA at the same time (x read from HBM once, the
     // second read an L1/L2 hit), 32 warps per SM of 64 registers

@@ -468,8 +468,9 @@ static __device__ __noinline__ int fallback_row(const uint4* src, int64_t nvec, 
 
 template <bool GEN>
 __device__ __forceinline__ bool fast_ok(const float (&xs)[8], const float (&t)[8], float dm, const FastRow& f) {
-  bool ok = max8(t) <= f.thi && min8(t) >= f.tlo && dm < kFastThr;
-  if (GEN) ok = ok && max8(xs) <= f.xhi && min8(xs) >= f.xlo;
+  // bitwise (not short-circuit): one predicate chain, no branches
+  bool ok = (max8(t) <= f.thi) & (min8(t) >= f.tlo) & (dm < kFastThr);
+  if (GEN) ok = ok & (max8(xs) <= f.xhi) & (min8(xs) >= f.xlo);
   return ok;
 }
 
@@ -623,6 +624,21 @@ __device__ __forceinline__ int encode_row_fast(const uint4* __restrict__ src, co
   return sum;
 }
 
+// Row parameters (or the EP sidecar) of output row r.
+__device__ __forceinline__ void store_row_params(const RowArgs& a, int64_t r, const AffineParams& p, int sum,
+                                                 double* scale, float* scale_f32, int32_t* zp, int32_t* rowsum) {
+  if (a.ep.codes_tab) {
+    const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
+    a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
+        make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
+  } else {
+    if (rowsum) rowsum[r] = sum;
+    scale[r] = p.scale;
+    if (scale_f32) scale_f32[r] = (float)p.scale;
+    zp[r] = p.zp;
+  }
+}
+
 // One row of K1 by one warp (the per-row body of act_quant_warp_kernel;
 // also run by the grouped GEMM's epilogue warps when K1 is fused into it).
 template <bool GIVEN, int NB = kBatch, typename Poll = NoPoll>
@@ -677,18 +693,7 @@ __device__ __forceinline__ void k1_row_warp(const RowArgs& a, int64_t r, const f
     }
   }
   if (!done) sum = fallback_row(src, nvec, lane, tab, srow, rrow, lb_max, ub_min, exact_all, bits, sym, dst, &p);
-  if (lane == 0) {
-    if (a.ep.codes_tab) {
-      const float wgt = a.ep.weight ? a.ep.weight[r] : 1.0f;
-      a.ep.params_tab[a.ep.dst_rank[r]][a.ep.dst_row[r]] =
-          make_int4(__float_as_int((float)p.scale), p.zp, sum, __float_as_int(wgt));
-    } else {
-      if (rowsum) rowsum[r] = sum;
-      scale[r] = p.scale;
-      if (scale_f32) scale_f32[r] = (float)p.scale;
-      zp[r] = p.zp;
-    }
-  }
+  if (lane == 0) store_row_params(a, r, p, sum, scale, scale_f32, zp, rowsum);
 }
 
 }  // namespace moe
