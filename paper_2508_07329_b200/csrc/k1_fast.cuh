@@ -325,15 +325,18 @@ __device__ __forceinline__ float min8(const float (&v)[8]) {
 // t = RN(xs * rsc + (1.5*2^23 + zp)) holds round(p) + zp in its low mantissa
 // bits (p = xs * rsc exact inside the FMA); d = RN(p - round(p)). A vector
 // of 8 takes the fast path when every code is in [2, 253] and every |d| is
-// below 0.5 - 2^-13: those codes equal the float64 reference's (|p| <= 254
-// there and p = y (1 + e), |e| <= 3 2^-24 + 2^-50, so |p - y| < 2^-14; d
-// itself carries one rounding of at most 2^-26). Everything else —
-// clipping, rounding-boundary cases, non-finite values and the elements
-// that could be row extremes (codes <= 1 / >= 254) — goes out of line.
+// below 0.5 - 2^-14 - 2^-24: those codes equal the float64 reference's
+// (|p| <= 255 there and p = y (1 + e), |e| <= 3 2^-24 + 2^-50, so
+// |p - y| <= 4.6e-5 < 2^-14; d itself carries one rounding of at most
+// 2^-26, so y stays more than 1.5e-5 away from the rounding boundary).
+// Everything else — clipping, rounding-boundary cases, non-finite values and
+// the elements that could be row extremes (codes <= 1 / >= 254) — goes out
+// of line. (The window was 0.5 - 2^-13 in round 1: twice as many boundary
+// vectors on the slow path for the same proof.)
 constexpr float kMagicF = 12582912.0f;
 constexpr float kFastTlo = 12582914.0f;          // code 2
 constexpr float kFastThi = 12583165.0f;          // code 253
-constexpr float kFastThr = 0.4998779296875f;     // 0.5 - 2^-13
+constexpr float kFastThr = 0.49993890523910522f;  // 0.5 - 2^-14 - 2^-24
 
 // Per-row constants of the fast encode. Two variants:
 //  * two-sided rows (asymmetric, the extremes land on codes <= 0 / >= 255):

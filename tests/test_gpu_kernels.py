@@ -226,6 +226,39 @@ def test_act_quant_row_ext_speculation(cuda, k1_kernel):
             np.testing.assert_array_equal(got.cpu().numpy(), exp)
 
 
+def test_act_quant_near_rounding_boundaries(cuda, k1_kernel):
+    """Rows whose quotients x / s / scale sit within +-2^-11 of half-integers
+    (a quarter of them inside the float32 filter's margin band 2^-14 .. 2^-13
+    around the boundary, and exact ties): every code, scale, zero point and
+    row sum equals the float64 oracle's, with and without producer records.
+    Each row's extremes are -127.5 and +127.5 (scale ~1, zero point 128), so
+    the target quotient of column j is exactly what the smoothing encodes."""
+    rng = np.random.default_rng(31)
+    R, d = 64, 2048
+    n = rng.integers(-120, 120, size=(R, d)).astype(np.float64)
+    delta = rng.uniform(-2.0 ** -11, 2.0 ** -11, size=(R, d))
+    band = rng.random(size=(R, d)) < 0.25
+    delta[band] = np.sign(delta[band]) * rng.uniform(2.0 ** -14, 2.0 ** -13, size=int(band.sum()))
+    delta[:, 2:40] = 0.0                                          # exact ties
+    target = n + 0.5 + delta
+    target[:, 0], target[:, 1] = 127.5, -127.5
+    x = np.where(target < 0, -1.0, 1.0).astype(np.float32)        # bf16-exact
+    s = 1.0 / np.abs(target)                                      # one smoothing group per row
+    group = np.arange(R, dtype=np.int32)
+    want = M.quantize_rows_grouped(x.astype(np.float64), group, s)
+    assert ((want[2] >= 16) & (want[2] <= 239)).all()             # two-sided rows: the fast window applies
+    xd = torch.from_numpy(x).to(cuda).bfloat16()
+    sd = torch.from_numpy(s).to(cuda)
+    gd = torch.from_numpy(group).to(cuda)
+    recip32 = (1.0 / s).astype(np.float32)
+    rec = _true_records(x, recip32)
+    for records in (None, rec):
+        r = ops.act_quant(xd, smooth=sd, row_group=gd,
+                          row_ext=None if records is None else torch.from_numpy(records).to(cuda))
+        for got, exp in zip((r["codes"], r["scale"], r["zp"], r["rowsum"]), want):
+            np.testing.assert_array_equal(got.cpu().numpy(), exp)
+
+
 def test_swiglu_row_ext_feeds_k1(cuda, k1_kernel):
     """The grouped SwiGLU epilogue's extreme records of h * RN32(1/s2) match
     the stored bf16 h, and K1 fed those records equals K1 without them."""
