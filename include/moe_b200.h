@@ -272,9 +272,10 @@ moe_status moe_route_permute(const int32_t* topk_idx, const float* topk_w, int64
 
 /* ---- K6: combine ----------------------------------------------------------
  * out[t, :] = sum_j y[token_pos[t*k+j], :] (row weights already applied by
- * the GEMM epilogue), summed in slot order j = 0..k-1 in float32. */
+ * the GEMM epilogue), summed in slot order j = 0..k-1 in float32. y rows are
+ * contiguous [T*k, d]; out rows are ldo (>= d) elements apart. */
 moe_status moe_combine(const void* y, int y_dtype, const int32_t* token_pos, int64_t T, int k, int64_t d,
-                       void* out, int out_dtype, moe_stream_t stream);
+                       void* out, int out_dtype, int64_t ldo, moe_stream_t stream);
 
 /* ---- routing statistics (trace.expert_freq, trace.py:216-225) -----------
  * counts[layer*E + e] += number of (t, j) with topk_idx[t, j] == e. Path

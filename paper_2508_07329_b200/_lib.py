@@ -69,7 +69,7 @@ _SIGS = {
     "moe_router_topk": (_I, [_P, _I64, _I, _I, _P, _P, _P]),
     "moe_route_permute_workspace": (_I64, [_I64, _I, _I]),
     "moe_route_permute": (_I, [_P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _I64, _P]),
-    "moe_combine": (_I, [_P, _I, _P, _I64, _I, _I64, _P, _I, _P]),
+    "moe_combine": (_I, [_P, _I, _P, _I64, _I, _I64, _P, _I, _I64, _P]),
     "moe_expert_histogram": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P]),
     "moe_hessian_accum": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P, _P]),
     "moe_hessian_finalize": (_I, [_P, _I64, _D, _P, _P]),

@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_single_kernel(const int3
 
 // ── combine ────────────────────────────────────────────────────────────────
 template <typename TIn, typename TOut>
-__global__ void combine_kernel(const TIn* y, const int32_t* token_pos, int64_t T, int k, int64_t d, TOut* out) {
+__global__ void combine_kernel(const TIn* y, const int32_t* token_pos, int64_t T, int k, int64_t d, TOut* out,
+                               int64_t ldo) {
   const int64_t t = blockIdx.x;
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
     float s = 0.f;
@@ -446,14 +447,14 @@ __global__ void combine_kernel(const TIn* y, const int32_t* token_pos, int64_t T
       if constexpr (sizeof(TIn) == 2) s += __bfloat162float(y[r * d + c]);
       else s += y[r * d + c];
     }
-    if constexpr (sizeof(TOut) == 2) out[t * d + c] = __float2bfloat16_rn(s);
-    else out[t * d + c] = s;
+    if constexpr (sizeof(TOut) == 2) out[t * ldo + c] = __float2bfloat16_rn(s);
+    else out[t * ldo + c] = s;
   }
 }
 
 // vectorised bf16 -> bf16 / f32 -> f32 paths (8 / 4 elements per thread step)
 __global__ void combine_bf16_vec_kernel(const __nv_bfloat16* y, const int32_t* token_pos, int k, int64_t d,
-                                        __nv_bfloat16* out) {
+                                        __nv_bfloat16* out, int64_t ldo) {
   const int64_t t = blockIdx.x;
   int32_t rows[kMaxK];
   for (int j = 0; j < k; ++j) rows[j] = token_pos[t * k + j];
@@ -469,7 +470,7 @@ __global__ void combine_bf16_vec_kernel(const __nv_bfloat16* y, const int32_t* t
     __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
     for (int e = 0; e < 4; ++e) p[e] = __floats2bfloat162_rn(s[2 * e], s[2 * e + 1]);
-    reinterpret_cast<uint4*>(out + t * d)[c] = o;
+    reinterpret_cast<uint4*>(out + t * ldo)[c] = o;
   }
 }
 
@@ -634,29 +635,31 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
 }
 
 extern "C" moe_status moe_combine(const void* y, int y_dtype, const int32_t* token_pos, int64_t T, int k, int64_t d,
-                                  void* out, int out_dtype, moe_stream_t stream) {
+                                  void* out, int out_dtype, int64_t ldo, moe_stream_t stream) {
   MOE_REQUIRE(y && token_pos && out && T >= 1 && d >= 1 && k >= 1 && k <= kMaxK, "combine: bad arguments");
+  MOE_REQUIRE(ldo >= d, "combine: out row stride below d");
   MOE_REQUIRE((y_dtype == MOE_DT_F32 || y_dtype == MOE_DT_BF16) && (out_dtype == MOE_DT_F32 || out_dtype == MOE_DT_BF16),
               "combine: dtypes f32|bf16");
   cudaStream_t s = as_stream(stream);
   const unsigned threads = 256;
-  if (y_dtype == MOE_DT_BF16 && out_dtype == MOE_DT_BF16 && d % 8 == 0 &&
+  if (y_dtype == MOE_DT_BF16 && out_dtype == MOE_DT_BF16 && d % 8 == 0 && ldo % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     combine_bf16_vec_kernel<<<(unsigned)T, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(y), token_pos, k, d,
-                                                            static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+                                                            static_cast<__nv_bfloat16*>(out), ldo);
   } else if (y_dtype == MOE_DT_F32 && out_dtype == MOE_DT_F32) {
     combine_kernel<float, float><<<(unsigned)T, threads, 0, s>>>(static_cast<const float*>(y), token_pos, T, k, d,
-                                                                 static_cast<float*>(out)); ::moe::count_launch();
+                                                                 static_cast<float*>(out), ldo);
   } else if (y_dtype == MOE_DT_F32) {
     combine_kernel<float, __nv_bfloat16><<<(unsigned)T, threads, 0, s>>>(
-        static_cast<const float*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+        static_cast<const float*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out), ldo);
   } else if (out_dtype == MOE_DT_F32) {
     combine_kernel<__nv_bfloat16, float><<<(unsigned)T, threads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<float*>(out)); ::moe::count_launch();
+        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<float*>(out), ldo);
   } else {
     combine_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)T, threads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out)); ::moe::count_launch();
+        static_cast<const __nv_bfloat16*>(y), token_pos, T, k, d, static_cast<__nv_bfloat16*>(out), ldo);
   }
+  ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
 }

@@ -113,7 +113,7 @@ def act_quant_tokens_ok(x: torch.Tensor) -> bool:
 
 def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.Tensor, *, smooth: torch.Tensor,
                      smooth_recip: torch.Tensor, smooth_recip_f32: torch.Tensor, bits: int = 8,
-                     symmetric: bool = False) -> dict:
+                     symmetric: bool = False, out_codes: torch.Tensor | None = None) -> dict:
     """Token-major K1 for the MoE dispatch: row token_pos[t, j] = x[t] /
     smooth[row_group[row]], per-token RTN; x is read once per token. Same
     result as act_quant(x, gather=src_token, row_group=row_group, ...)."""
@@ -121,7 +121,7 @@ def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.
     k = token_pos.numel() // max(T, 1)
     rows = T * k
     dev = x.device
-    codes = torch.empty((rows, cols), dtype=torch.uint8, device=dev)
+    codes = out_codes if out_codes is not None else torch.empty((rows, cols), dtype=torch.uint8, device=dev)
     scale = torch.empty(rows, dtype=torch.float64, device=dev)
     scale_f32 = torch.empty(rows, dtype=torch.float32, device=dev)
     zp = torch.empty(rows, dtype=torch.int32, device=dev)
@@ -373,7 +373,9 @@ def combine(y: torch.Tensor, token_pos: torch.Tensor, T: int, k: int, out_dtype=
     y = _rowmajor(y, "y")
     d = y.shape[1]
     o = out if out is not None else torch.empty((T, d), dtype=out_dtype, device=y.device)
-    L.call("moe_combine", L.ptr(y), _dt(y), L.ptr(token_pos), T, k, d, L.ptr(o), _dt(o), _s())
+    if o.shape != (T, d) or o.stride(1) != 1:
+        raise ValueError(f"combine: out must be [{T}, {d}] with unit column stride")
+    L.call("moe_combine", L.ptr(y), _dt(y), L.ptr(token_pos), T, k, d, L.ptr(o), _dt(o), o.stride(0), _s())
     return o
 
 
