@@ -121,3 +121,62 @@ def test_moe_forward_writes_in_bounds(cuda, T):
     torch.cuda.synchronize()
     _assert_margins(buf, T, 512, 0x3D)
     assert torch.equal(view, want)
+
+
+# ── reads: input rows live inside wider buffers whose margins are poisoned;
+# a kernel that read past a row end (or past the last row) would change its
+# result ────────────────────────────────────────────────────────────────────
+def _poisoned_view(src: torch.Tensor, pad_c: int, fill_byte: int) -> torch.Tensor:
+    rows, cols = src.shape
+    buf = torch.empty((rows + PAD_R, cols + pad_c), dtype=src.dtype, device=src.device)
+    buf.view(torch.uint8).fill_(fill_byte)
+    view = buf[:rows, :cols]
+    view.copy_(src)
+    return view
+
+
+@pytest.mark.parametrize("T,d", [(257, 2056), (33, 14336), (1000, 4096)])
+def test_k1_reads_in_bounds(cuda, T, d, k1_kernel):
+    rng = np.random.default_rng(T * 3 + d)
+    x = torch.from_numpy(_acts(rng, T, d)).to(cuda).bfloat16()
+    xp = _poisoned_view(x, PAD_C, 0xFF)                           # bf16 0xFFFF = NaN
+    s = torch.from_numpy(_smooth(rng, 1, d)).to(cuda)
+    rec = torch.from_numpy(_true_records(x.float().cpu().numpy(),
+                                         np.broadcast_to((1.0 / s.cpu().numpy()).astype(np.float32), (T, d)))).to(cuda)
+    for ext in (None, rec):
+        want = ops.act_quant(x, smooth=s, row_ext=ext)
+        got = ops.act_quant(xp, smooth=s, row_ext=ext)
+        for key in ("codes", "scale", "zp", "rowsum"):
+            assert torch.equal(got[key], want[key]), key
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_k1_tokens_reads_in_bounds(cuda, mode):
+    rng = np.random.default_rng(11)
+    T, d, k, G = 600, 4096, 2, 8
+    x = torch.from_numpy(_acts(rng, T, d)).to(cuda).bfloat16()
+    xp = _poisoned_view(x, PAD_C, 0xFF)
+    s = torch.from_numpy(_smooth(rng, G, d)).to(cuda)
+    rec, rec32 = ops.reciprocal(s, with_f32=True)
+    pos = torch.from_numpy(rng.permutation(T * k).astype(np.int32).reshape(T, k)).to(cuda)
+    grp = torch.from_numpy(rng.integers(0, G, size=T * k).astype(np.int32)).to(cuda)
+    with L.tuned(L.TUNE_K1_TOKENS, mode):
+        want = ops.act_quant_tokens(x, pos, grp, smooth=s, smooth_recip=rec, smooth_recip_f32=rec32)
+        got = ops.act_quant_tokens(xp, pos, grp, smooth=s, smooth_recip=rec, smooth_recip_f32=rec32)
+    for key in ("codes", "scale", "zp", "rowsum"):
+        assert torch.equal(got[key], want[key]), key
+
+
+@pytest.mark.parametrize("M_,N,K", [(300, 512, 520), (2500, 768, 4096), (2049, 328, 1040)])
+def test_gemm_reads_in_bounds(cuda, M_, N, K):
+    """A and W codes with row strides past K (margins 0xFF): the TMA boxes of
+    the last k-block must stop at K (zero fill), not read the neighbour bytes."""
+    rng = np.random.default_rng(M_ + N + K)
+    a = _dev_operand(cuda, *_rand_operand(rng, M_, K))
+    w = _dev_operand(cuda, *_rand_operand(rng, N, K))
+    want = ops.w8a8_gemm(a, w, epilogue=L.EPI_ACC_I32)
+    ap = dict(a, codes=_poisoned_view(a["codes"], 48, 0xFF))
+    wp = dict(w, codes=_poisoned_view(w["codes"], 48, 0xFF))
+    assert torch.equal(ops.w8a8_gemm(ap, wp, epilogue=L.EPI_ACC_I32), want)
+    want = ops.w8a8_gemm(a, w, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16)
+    assert torch.equal(ops.w8a8_gemm(ap, wp, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16), want)
