@@ -243,8 +243,9 @@ int64_t moe_quant_sq_error_workspace(int64_t M, int64_t N);
  * trace.py:40-44). logits[t, e] = x[t,:] . gate_w[e,:] (float32 accumulate);
  * top-k on logits, ties to the lower expert id, descending order; weights
  * = softmax over the selected logits. gate_bias [E] (optional) is added to the
- * logits. logits may be NULL (not stored). */
-moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, const float* gate_w,
+ * logits. logits may be NULL (not stored). x rows are ldx (>= d) elements
+ * apart. */
+moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, int64_t ldx, const float* gate_w,
                            const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx,
                            float* topk_w, moe_stream_t stream);
 /* top-k only, from given float32 logits [T, E]. */

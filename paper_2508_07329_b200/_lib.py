@@ -62,7 +62,7 @@ _SIGS = {
     "moe_rmsnorm_residual": (_I, [_P, _P, _P, _P, _I64, _I64, C.c_float, _P]),
     "moe_quant_sq_error": (_I, [_P, _I64, _I64, _P, _I, _P, _P, _P, _P, _I64, _P]),
     "moe_quant_sq_error_workspace": (_I64, [_I64, _I64]),
-    "moe_router_gate": (_I, [_P, _I, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "moe_router_gate": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),
     "moe_router_tc_workspace": (_I64, [_I64]),
     "moe_router_prepare": (_I, [_P, _I, _I64, _P, _P]),
     "moe_router_gate_tc": (_I, [_P, _I64, _I64, _I64, _P, _P, _I, _I, _P, _P, _P, _P]),

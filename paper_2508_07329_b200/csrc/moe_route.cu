@@ -43,7 +43,7 @@ __device__ __forceinline__ void topk_select(const float* l, int E, int k, int32_
 // One warp per token: logits[t, e] = x[t] . gate_w[e] in float32, lane-strided
 // then butterfly-reduced (fixed order -> deterministic), then top-k.
 template <int E_T>
-__global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt, int64_t T, int64_t d,
+__global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt, int64_t T, int64_t d, int64_t ldx,
                                                           const float* __restrict__ gw, const float* gb, int E,
                                                           int k, float* logits, int32_t* idx, float* w) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt,
   float acc[E_T];
 #pragma unroll
   for (int e = 0; e < E_T; ++e) acc[e] = 0.f;
-  const int64_t row = (int64_t)warp * d;
-  const bool vec = dt == MOE_DT_BF16 && d % 256 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t row = (int64_t)warp * ldx;
+  const bool vec = dt == MOE_DT_BF16 && d % 256 == 0 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   if (vec) {
     const uint4* xp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + row);
     for (int64_t c = lane; c < d / 8; c += 32) {
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) router_gate_kernel(const void* x, int dt,
 // per-lane accumulation order as router_gate_kernel.
 template <int E_T>
 __global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat16* __restrict__ x, int64_t T,
-                                                               int64_t d, const float* __restrict__ gw,
+                                                               int64_t d, int64_t ldx, const float* __restrict__ gw,
                                                                const float* gb, int E, int k, float* logits,
                                                                int32_t* idx, float* w) {
   extern __shared__ __align__(16) float sgw[];
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat
     for (int e = 0; e < E_T; ++e) acc[e] = 0.f;
     // 4 elements (8 B of x, one conflict-free float4 of each gate row) per
     // lane and step; 4 steps in flight
-    const uint2* xp = reinterpret_cast<const uint2*>(x + t * d);
+    const uint2* xp = reinterpret_cast<const uint2*>(x + t * ldx);
     const int64_t n4 = d / 4;
 #pragma unroll 4
     for (int64_t c = lane; c < n4; c += 32) {
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(512) router_gate_smem_kernel(const __nv_bfloat
 constexpr int kRouterTB = 4;
 
 __global__ void __launch_bounds__(512, 1)
-    router_gate_reg_kernel(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t d, const float* __restrict__ gw,
+    router_gate_reg_kernel(const __nv_bfloat16* __restrict__ x, int64_t T, int64_t d, int64_t ldx,
+                           const float* __restrict__ gw,
                            const float* gb, int E, int k, float* logits, int32_t* idx, float* w) {
   __shared__ float part[2][16][32];   // [buffer][warp][lane] -> entry lane = token * 8 + expert
   const int lane = threadIdx.x & 31;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(512, 1)
     uint4 u[kRouterTB];
 #pragma unroll
     for (int t = 0; t < kRouterTB; ++t)
-      u[t] = t0 + t < T ? __ldcs(reinterpret_cast<const uint4*>(x + (t0 + t) * d + col0)) : make_uint4(0, 0, 0, 0);
+      u[t] = t0 + t < T ? __ldcs(reinterpret_cast<const uint4*>(x + (t0 + t) * ldx + col0)) : make_uint4(0, 0, 0, 0);
     float v[32];
 #pragma unroll
     for (int t = 0; t < kRouterTB; ++t) {
@@ -552,34 +553,35 @@ __global__ void histogram_kernel(const int32_t* idx, int64_t T, int k, int E, in
 
 using namespace moe;
 
-extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, const float* gate_w,
+extern "C" moe_status moe_router_gate(const void* x, int x_dtype, int64_t T, int64_t d, int64_t ldx, const float* gate_w,
                                       const float* gate_bias, int E, int k, float* logits, int32_t* topk_idx, float* topk_w, moe_stream_t stream) {
   MOE_REQUIRE(x && gate_w && topk_idx && topk_w, "router_gate: null pointer");
   MOE_REQUIRE(T >= 1 && d >= 1, "router_gate: empty input");
+  MOE_REQUIRE(ldx >= d, "router_gate: row stride below d");
   MOE_REQUIRE(E >= 1 && E <= 32 && k >= 1 && k <= kMaxK && k <= E, "router_gate: need 1 <= k <= E <= 32");
   const int64_t threads = T * 32;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   cudaStream_t s = as_stream(stream);
   const int64_t gw_bytes = (int64_t)E * d * 4;
-  if (x_dtype == MOE_DT_BF16 && d % 256 == 0 && d <= 4096 && E <= 8 &&
+  if (x_dtype == MOE_DT_BF16 && d % 256 == 0 && d <= 4096 && E <= 8 && ldx % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
     const int64_t grid = std::min<int64_t>((T + kRouterTB - 1) / kRouterTB, num_sms());
     router_gate_reg_kernel<<<(unsigned)grid, (unsigned)(d / 256 * 32), 0, s>>>(
-        static_cast<const __nv_bfloat16*>(x), T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
+        static_cast<const __nv_bfloat16*>(x), T, d, ldx, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
     ::moe::count_launch();
-  } else if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
+  } else if (x_dtype == MOE_DT_BF16 && d % 8 == 0 && ldx % 4 == 0 && E <= 8 && gw_bytes <= 200 * 1024 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0) {
     MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(router_gate_smem_kernel<8>), 200 * 1024));
     const int64_t grid = std::min<int64_t>((T + 15) / 16, num_sms());
     router_gate_smem_kernel<8><<<(unsigned)grid, 512, (size_t)gw_bytes, s>>>(
-        static_cast<const __nv_bfloat16*>(x), T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
+        static_cast<const __nv_bfloat16*>(x), T, d, ldx, gate_w, gate_bias, E, k, logits, topk_idx, topk_w);
     ::moe::count_launch();
   } else if (E <= 8) {
-    router_gate_kernel<8><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+    router_gate_kernel<8><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, ldx, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
   } else if (E <= 16) {
-    router_gate_kernel<16><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+    router_gate_kernel<16><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, ldx, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
   } else {
-    router_gate_kernel<32><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
+    router_gate_kernel<32><<<blocks, 256, 0, s>>>(x, x_dtype, T, d, ldx, gate_w, gate_bias, E, k, logits, topk_idx, topk_w); ::moe::count_launch();
   }
   MOE_LAUNCH_CHECK();
   return MOE_OK;

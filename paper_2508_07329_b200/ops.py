@@ -143,6 +143,8 @@ def dequantize(codes: torch.Tensor, scale: torch.Tensor, zp: torch.Tensor, granu
 
 def apply_smoothing(w: torch.Tensor | None, x: torch.Tensor | None, f: torch.Tensor):
     f = f.contiguous()
+    w = w.contiguous() if w is not None else None       # the kernel walks dense row-major matrices
+    x = x.contiguous() if x is not None else None
     ws = torch.empty_like(w) if w is not None else None
     xs = torch.empty_like(x) if x is not None else None
     n = f.numel()
@@ -286,6 +288,7 @@ def with_wcorr(w: dict) -> dict:
 
 
 def quant_sq_error(acc: torch.Tensor, a_scale: torch.Tensor, w_scale: torch.Tensor, ref: torch.Tensor) -> torch.Tensor:
+    acc = acc.contiguous()
     M, N = acc.shape
     lib = L.load()
     wsb = lib.moe_quant_sq_error_workspace(M, N)
@@ -333,7 +336,7 @@ def router_gate(x: torch.Tensor, gate_w: torch.Tensor, k: int, want_logits: bool
         L.call("moe_router_gate_tc", L.ptr(x), T, d, x.stride(0), L.ptr(router_pieces(gw)), L.ptr(gb), E, k,
                L.ptr(logits), L.ptr(idx), L.ptr(w), _s())
     else:
-        L.call("moe_router_gate", L.ptr(x), _dt(x), T, d, L.ptr(gw), L.ptr(gb), E, k, L.ptr(logits), L.ptr(idx),
+        L.call("moe_router_gate", L.ptr(x), _dt(x), T, d, x.stride(0), L.ptr(gw), L.ptr(gb), E, k, L.ptr(logits), L.ptr(idx),
                L.ptr(w), _s())
     return logits, idx, w
 

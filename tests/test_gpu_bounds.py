@@ -180,3 +180,62 @@ def test_gemm_reads_in_bounds(cuda, M_, N, K):
     assert torch.equal(ops.w8a8_gemm(ap, wp, epilogue=L.EPI_ACC_I32), want)
     want = ops.w8a8_gemm(a, w, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16)
     assert torch.equal(ops.w8a8_gemm(ap, wp, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16), want)
+
+
+@pytest.mark.parametrize("T", [16, 300, 9000])
+def test_router_reads_in_bounds(cuda, T):
+    """Tensor-core router (cluster kernel for small batches, persistent
+    kernel for large ones) and the SIMT router on token rows with poisoned
+    margins and a ragged last 128-token tile: identical logits, ids, weights."""
+    rng = np.random.default_rng(T)
+    d, E = 1024, 8
+    x = torch.from_numpy(bf16_round(rng.normal(size=(T, d)).astype(np.float32))).to(cuda).bfloat16()
+    xp = _poisoned_view(x, 64, 0xFF)
+    gw = torch.from_numpy(rng.normal(size=(E, d)).astype(np.float32) / np.sqrt(d)).to(cuda)
+    for tc in (True, False):
+        want = ops.router_gate(x, gw, 2, tensor_cores=tc)
+        got = ops.router_gate(xp, gw, 2, tensor_cores=tc)
+        for a, b in zip(got, want):
+            assert torch.equal(a, b)
+
+
+def test_gather_rows_writes_in_bounds(cuda):
+    rng = np.random.default_rng(4)
+    src = torch.from_numpy(rng.integers(0, 256, size=(500, 1000)).astype(np.uint8)).to(cuda)
+    idx = torch.from_numpy(rng.integers(0, 500, size=777).astype(np.int32)).to(cuda)
+    buf, view = _carve(777, 1000, torch.uint8, cuda, 0x11)
+    ops.gather_rows(_poisoned_view(src, 24, 0x22), idx, out=view)
+    torch.cuda.synchronize()
+    _assert_margins(buf, 777, 1000, 0x11)
+    assert torch.equal(view, src[idx.long()])
+
+
+def test_rope_writes_in_bounds(cuda):
+    """RoPE rotates only the first heads * head_dim columns of each row (the
+    q and k heads of the fused QKV rows): v columns and margins untouched."""
+    rng = np.random.default_rng(6)
+    T, heads, hd, extra = 77, 12, 128, 4 * 128
+    cos, sin = ops.rope_tables(4096, hd)
+    x = torch.from_numpy(bf16_round(rng.normal(size=(T, heads * hd + extra)).astype(np.float32))).to(cuda).bfloat16()
+    buf, view = _carve(T, x.shape[1], torch.bfloat16, cuda, 0x44)
+    view.copy_(x)
+    pos = torch.from_numpy(rng.integers(0, 4096, size=T).astype(np.int32)).to(cuda)
+    ops.rope_(view, heads, hd, cos, sin, positions=pos)
+    want = ops.rope_(x.clone(), heads, hd, cos, sin, positions=pos)
+    torch.cuda.synchronize()
+    _assert_margins(buf, T, x.shape[1], 0x44)
+    assert torch.equal(view[:, heads * hd:], x[:, heads * hd:])
+    assert torch.equal(view, want)
+
+
+def test_apply_smoothing_strided_inputs(cuda):
+    """apply_smoothing on transposed / column-sliced views equals the dense call."""
+    rng = np.random.default_rng(8)
+    w = torch.from_numpy(rng.normal(size=(96, 64))).to(cuda)
+    x = torch.from_numpy(rng.normal(size=(64, 40))).to(cuda)
+    f = torch.from_numpy(np.exp(rng.normal(size=64))).to(cuda)
+    want = ops.apply_smoothing(w, x, f)
+    wt = w.t().contiguous().t()                                  # same values, column-major storage
+    xs = torch.cat([x, x], dim=1)[:, :40]                        # row stride 80
+    got = ops.apply_smoothing(wt, xs, f)
+    assert torch.equal(got[0], want[0]) and torch.equal(got[1], want[1])
