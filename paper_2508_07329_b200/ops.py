@@ -27,6 +27,18 @@ def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+def _vec(t: torch.Tensor | None, name: str, dtype) -> torch.Tensor | None:
+    """Index / table / per-row argument: a dense CUDA tensor of ``dtype``
+    (None passes through). The kernels read these as raw arrays, so a wrong
+    dtype would be reinterpreted silently: refuse it instead."""
+    if t is None:
+        return None
+    _cuda(t, name)
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
 def _rowmajor(t: torch.Tensor, name: str) -> torch.Tensor:
     _cuda(t, name)
     if t.dim() != 2:
@@ -69,6 +81,9 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
               out_codes: torch.Tensor | None = None, row_ext: torch.Tensor | None = None) -> dict:
     """K1: codes/scales/zero points of (x[gather] (/ or *) smooth[row_group])."""
     x = _rowmajor(x, "x")
+    gather = _vec(gather, "gather", torch.int32)
+    row_group = _vec(row_group, "row_group", torch.int32)
+    row_ext = _vec(row_ext, "row_ext", torch.int64)
     n_rows = rows if rows is not None else (gather.numel() if gather is not None else x.shape[0])
     cols = x.shape[1]
     gran = L.GRAN[granularity]
@@ -90,11 +105,11 @@ def act_quant(x: torch.Tensor, *, smooth: torch.Tensor | None = None, smooth_rec
         row_group = None
     mode = L.SMOOTH_NONE if smooth is None else smooth_mode
     if smooth is not None:
-        smooth = smooth.contiguous()
-        if smooth.dtype != torch.float64:
-            raise ValueError("smoothing table must be float64")
+        smooth = _vec(smooth, "smoothing table", torch.float64)
         if smooth_recip is None and mode == L.SMOOTH_DIVIDE:
             smooth_recip, smooth_recip_f32 = reciprocal(smooth, with_f32=True)
+        smooth_recip = _vec(smooth_recip, "smooth_recip", torch.float64)
+        smooth_recip_f32 = _vec(smooth_recip_f32, "smooth_recip_f32", torch.float32)
     div = mode == L.SMOOTH_DIVIDE
     L.call("moe_act_quant", L.ptr(x), _dt(x), n_rows, cols, x.stride(0), L.ptr(gather), L.ptr(smooth),
            L.ptr(smooth_recip) if div else None, L.ptr(smooth_recip_f32) if div else None, mode,
@@ -117,6 +132,12 @@ def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.
     """Token-major K1 for the MoE dispatch: row token_pos[t, j] = x[t] /
     smooth[row_group[row]], per-token RTN; x is read once per token. Same
     result as act_quant(x, gather=src_token, row_group=row_group, ...)."""
+    x = _rowmajor(x, "x")
+    token_pos = _vec(token_pos, "token_pos", torch.int32)
+    row_group = _vec(row_group, "row_group", torch.int32)
+    smooth = _vec(smooth, "smooth", torch.float64)
+    smooth_recip = _vec(smooth_recip, "smooth_recip", torch.float64)
+    smooth_recip_f32 = _vec(smooth_recip_f32, "smooth_recip_f32", torch.float32)
     T, cols = x.shape
     k = token_pos.numel() // max(T, 1)
     rows = T * k
@@ -126,7 +147,7 @@ def act_quant_tokens(x: torch.Tensor, token_pos: torch.Tensor, row_group: torch.
     scale_f32 = torch.empty(rows, dtype=torch.float32, device=dev)
     zp = torch.empty(rows, dtype=torch.int32, device=dev)
     rs = torch.empty(rows, dtype=torch.int32, device=dev)
-    L.call("moe_act_quant_tokens", L.ptr(x), _dt(x), T, cols, x.stride(0), k, L.ptr(token_pos.contiguous()),
+    L.call("moe_act_quant_tokens", L.ptr(x), _dt(x), T, cols, x.stride(0), k, L.ptr(token_pos),
            L.ptr(row_group), L.ptr(smooth), L.ptr(smooth_recip), L.ptr(smooth_recip_f32), bits, int(bool(symmetric)),
            L.ptr(codes), codes.stride(0), L.ptr(scale), L.ptr(scale_f32), L.ptr(zp), L.ptr(rs), _s())
     return {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
@@ -171,6 +192,9 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
     ac, wc = a["codes"], w["codes"]
     M, K = ac.shape
     N = n_per_group if n_per_group is not None else wc.shape[0] // num_groups
+    group_offsets = _vec(group_offsets, "group_offsets", torch.int32)
+    row_weight = _vec(row_weight, "row_weight", torch.float32)
+    row_ext = _vec(row_ext, "row_ext", torch.int64)
     if wc.shape[1] != K:
         raise ValueError(f"A has K={K} but W has K={wc.shape[1]}")
     dev = ac.device
@@ -249,6 +273,10 @@ def w8a8_gemm_combine(a: dict, w: dict, *, row_weight: torch.Tensor, group_offse
     M, K = ac.shape
     N = n_per_group
     dev = ac.device
+    src_token = _vec(src_token, "src_token", torch.int32)
+    token_pos = _vec(token_pos, "token_pos", torch.int32)
+    row_weight = _vec(row_weight, "row_weight", torch.float32)
+    group_offsets = _vec(group_offsets, "group_offsets", torch.int32)
     y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     o = out if out is not None else torch.empty((T, N), dtype=torch.bfloat16, device=dev)
     wsb = L.load().moe_w8a8_gemm_combine_workspace(T, N)
@@ -351,7 +379,8 @@ def router_topk(logits: torch.Tensor, k: int):
 
 
 def route_permute(idx: torch.Tensor, w: torch.Tensor | None, E: int) -> dict:
-    idx = idx.contiguous()
+    idx = _vec(idx, "idx", torch.int32)
+    w = _vec(w, "w", torch.float32)
     T, k = idx.shape
     dev = idx.device
     n = T * k
@@ -373,7 +402,8 @@ def route_permute(idx: torch.Tensor, w: torch.Tensor | None, E: int) -> dict:
 
 def combine(y: torch.Tensor, token_pos: torch.Tensor, T: int, k: int, out_dtype=torch.bfloat16,
             out: torch.Tensor | None = None) -> torch.Tensor:
-    y = _rowmajor(y, "y")
+    y = _rowmajor(y, "y").contiguous()                  # y rows are read as dense [T*k, d]
+    token_pos = _vec(token_pos, "token_pos", torch.int32)
     d = y.shape[1]
     o = out if out is not None else torch.empty((T, d), dtype=out_dtype, device=y.device)
     if o.shape != (T, d) or o.stride(1) != 1:
@@ -385,7 +415,10 @@ def combine(y: torch.Tensor, token_pos: torch.Tensor, T: int, k: int, out_dtype=
 def expert_histogram(idx: torch.Tensor, E: int, layer: int, counts: torch.Tensor,
                      path_codes: torch.Tensor | None = None) -> None:
     T, k = idx.shape
-    L.call("moe_expert_histogram", L.ptr(idx.contiguous()), T, k, E, layer, L.ptr(counts), L.ptr(path_codes), _s())
+    idx = _vec(idx, "idx", torch.int32)
+    if counts.dtype != torch.int64 or not counts.is_contiguous():
+        raise ValueError("counts must be a dense int64 tensor")
+    L.call("moe_expert_histogram", L.ptr(idx), T, k, E, layer, L.ptr(counts), L.ptr(path_codes), _s())
 
 
 # ── K7 / K8 ───────────────────────────────────────────────────────────────
@@ -433,11 +466,12 @@ def route_keys(idx: torch.Tensor, dest_rank: torch.Tensor, E: int) -> torch.Tens
 def gather_rows(src: torch.Tensor, index: torch.Tensor | None, out: torch.Tensor | None = None) -> torch.Tensor:
     """out[r] = src[index[r]] for a row-major 2-D tensor (any dtype)."""
     src = _rowmajor(src, "src")
+    index = _vec(index, "index", torch.int32)
     n = index.numel() if index is not None else src.shape[0]
     o = out if out is not None else torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
     row_bytes = src[0].numel() * src.element_size() if src.shape[0] else o[0].numel() * o.element_size()
     L.call("moe_gather_rows", L.ptr(src), src.stride(0) * src.element_size(),
-           L.ptr(index.contiguous() if index is not None else None), n, row_bytes, L.ptr(o),
+           L.ptr(index), n, row_bytes, L.ptr(o),
            o.stride(0) * o.element_size(), _s())
     return o
 

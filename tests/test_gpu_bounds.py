@@ -239,3 +239,21 @@ def test_apply_smoothing_strided_inputs(cuda):
     xs = torch.cat([x, x], dim=1)[:, :40]                        # row stride 80
     got = ops.apply_smoothing(wt, xs, f)
     assert torch.equal(got[0], want[0]) and torch.equal(got[1], want[1])
+
+
+def test_index_dtypes_refused(cuda):
+    """Index and per-row arguments are raw int32 / float32 arrays to the
+    kernels: a tensor of another dtype raises instead of being reinterpreted."""
+    x = torch.zeros((4, 64), dtype=torch.bfloat16, device=cuda)
+    s = torch.ones((2, 64), dtype=torch.float64, device=cuda)
+    with pytest.raises(ValueError, match="row_group"):
+        ops.act_quant(x, smooth=s, row_group=torch.zeros(4, dtype=torch.int64, device=cuda))
+    with pytest.raises(ValueError, match="gather"):
+        ops.act_quant(x, gather=torch.zeros(4, dtype=torch.int64, device=cuda))
+    with pytest.raises(ValueError, match="idx"):
+        ops.route_permute(torch.zeros((4, 2), dtype=torch.int64, device=cuda), None, 8)
+    with pytest.raises(ValueError, match="token_pos"):
+        ops.combine(torch.zeros((8, 64), dtype=torch.bfloat16, device=cuda),
+                    torch.arange(8, dtype=torch.int64, device=cuda), 4, 2)
+    with pytest.raises(ValueError, match="smoothing table"):
+        ops.act_quant(x, smooth=s.float())
