@@ -24,6 +24,10 @@ def _dt(t: torch.Tensor) -> int:
 def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        # kernels launch on the current device's current stream
+        raise ValueError(f"{name} is on {t.device} but the current device is cuda:{torch.cuda.current_device()} "
+                         "(wrap the call in torch.cuda.device(...))")
     return t
 
 

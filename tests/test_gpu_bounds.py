@@ -257,3 +257,13 @@ def test_index_dtypes_refused(cuda):
                     torch.arange(8, dtype=torch.int64, device=cuda), 4, 2)
     with pytest.raises(ValueError, match="smoothing table"):
         ops.act_quant(x, smooth=s.float())
+
+
+@pytest.mark.parametrize("T", [9, 1000, 2600])
+def test_moe_forward_strided_input(cuda, T):
+    """The layer on token rows that are a column slice of wider rows (row
+    stride > d, margins poisoned) equals the layer on the dense rows."""
+    layer = MoELayer.random(8, 512, 1024, top_k=2, seed=5)
+    rng = np.random.default_rng(T + 1)
+    x = torch.from_numpy(bf16_round(rng.normal(size=(T, 512)).astype(np.float32))).to(cuda).bfloat16()
+    assert torch.equal(layer.forward(_poisoned_view(x, 64, 0xFF)), layer.forward(x))
