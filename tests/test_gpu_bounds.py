@@ -267,3 +267,27 @@ def test_moe_forward_strided_input(cuda, T):
     rng = np.random.default_rng(T + 1)
     x = torch.from_numpy(bf16_round(rng.normal(size=(T, 512)).astype(np.float32))).to(cuda).bfloat16()
     assert torch.equal(layer.forward(_poisoned_view(x, 64, 0xFF)), layer.forward(x))
+
+
+@pytest.mark.parametrize("T", [9, 1000])
+def test_moe_forward_nonfinite_tokens_are_contained(cuda, T):
+    """The reference refuses non-finite input (numkit.py:52-53); the device
+    forward does not scan for it (that would need a host sync), so a NaN /
+    Inf token must at least stay contained: no fault, no hang, valid routing
+    ids, and every other token's output bit-identical to the clean batch."""
+    layer = MoELayer.random(8, 512, 1024, top_k=2, seed=5)
+    rng = np.random.default_rng(T + 2)
+    x = torch.from_numpy(bf16_round(rng.normal(size=(T, 512)).astype(np.float32))).to(cuda).bfloat16()
+    clean = layer.forward(x)
+    bad = x.clone()
+    bad[0, 3] = float("nan")
+    bad[T // 2, :] = float("inf")
+    bad[T - 1, 7] = float("-inf")
+    out = layer.forward(bad)                      # default path (fused combine at 1000 tokens)
+    _, aux = layer.forward(bad, return_aux=True)
+    torch.cuda.synchronize()
+    idx = aux["idx"]
+    assert bool(((idx >= 0) & (idx < 8)).all())
+    keep = torch.ones(T, dtype=torch.bool, device=cuda)
+    keep[[0, T // 2, T - 1]] = False
+    assert torch.equal(out[keep], clean[keep])
