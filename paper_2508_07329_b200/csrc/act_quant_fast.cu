@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
               for (int b = 0; b < kVecStep; ++b) {
                 if (!(slowm >> b & 1u)) continue;
                 const int64_t c = cb + 32 * (hf + b);
-                const uint4 sv = slow_vec8(v[lane + 32 * (hf + b)], tab, c, srow, rrow, f);
+                const uint4 sv = slow_vec8_packed(v[lane + 32 * (hf + b)], tab, c, srow, rrow, f);
                 cnt += sv.z;
                 const uint2 o2 = make_uint2(sv.x, sv.y);
                 sum += bytesum(o2);
