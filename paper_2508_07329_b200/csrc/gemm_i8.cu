@@ -64,6 +64,7 @@ struct GemmArgs {
   int tma_out;              // bf16 output stored through smem + TMA (tensor map tmO)
   int band;                 // m-tiles per raster band (map_tile)
   int pf_kb;                // k blocks of the first weight tile to prefetch into L2 before griddep_wait
+  int serp;                 // alternate the k direction tile by tile (exact int32 sums: order-free)
   int l2pol;                // L2 eviction priority of the A (bits 0-1) and W (bits 2-3) tile loads:
                             // 0 evict_last, 1 evict_normal, 2 evict_first
   void* const* out_tab;     // DEQUANT: row m goes to out_tab[out_rank[m]] + out_row[m] * ldo (EP combine)
@@ -779,12 +780,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint64_t pol_b = l2_policy((p.l2pol >> 2) & 3);
     const int kblocks = (p.K + kBK - 1) / kBK;
     uint32_t it = 0;
-    for (int t = unit; t < total_tiles; t += n_units) {
+    uint32_t ptile = 0;
+    for (int t = unit; t < total_tiles; t += n_units, ++ptile) {
       const TileInfo ti = map_tile(t, p.G, tile_start, off, TM, BN, n_tiles, p.band);
       const int arow = ti.m0 + (int)rank * kBM;
       const int wrow = ti.g * p.N + ti.n0 + (int)rank * (BN / CG);
       if constexpr (FQ) fq_wait_rows(p, arow, min(arow + kBM, ti.m_end));
+      const bool down = p.serp && (ptile & 1);
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const int kc = down ? kblocks - 1 - kb : kb;   // k block loaded into this stage
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         {
@@ -796,13 +800,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint8_t* sb = sa + L::kA;
         if (CG == 2) {
           if (leader) mbar_expect_tx(&full[s], 2 * L::kStage);
-          tma_load_2d_pair(sa, &tmA, &full[s], kb * kBK, arow, pol_a);
-          tma_load_2d_pair(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+          tma_load_2d_pair(sa, &tmA, &full[s], kc * kBK, arow, pol_a);
+          tma_load_2d_pair(sb, &tmB, &full[s], kc * kBK, wrow, pol_b);
           if (!leader) mbar_arrive_leader(&full[s]);
         } else {
           mbar_expect_tx(&full[s], L::kStage);
-          tma_load_2d(sa, &tmA, &full[s], kb * kBK, arow, pol_a);
-          tma_load_2d(sb, &tmB, &full[s], kb * kBK, wrow, pol_b);
+          tma_load_2d(sa, &tmA, &full[s], kc * kBK, arow, pol_a);
+          tma_load_2d(sb, &tmB, &full[s], kc * kBK, wrow, pol_b);
         }
       }
     }
@@ -1099,6 +1103,10 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   {
     static const int env_pol = getenv("MOE_B200_GEMM_L2POL") ? atoi(getenv("MOE_B200_GEMM_L2POL")) : -1;
     p.l2pol = env_pol >= 0 ? env_pol : 0;
+  }
+  {
+    static const int env_serp = getenv("MOE_B200_GEMM_SERP") ? atoi(getenv("MOE_B200_GEMM_SERP")) : 1;
+    p.serp = env_serp;
   }
   p.pf_kb = (M <= 1024) ? (int)std::min<int64_t>((K + kBK - 1) / kBK, (640 << 10) / ((BN / CG) * kBK)) : 0;
   const int64_t units_bound = ((M + TM - 1) / TM + num_groups) * n_tiles;
