@@ -602,3 +602,36 @@ def test_hessian_dmma_matches_oracle(cuda, n, T, dt):
     assert np.array_equal(Hs, Hs.T)
     with pytest.raises(Exception):
         ops.hessian(torch.zeros((T, n), dtype=tdt, device=cuda))
+
+
+def test_gemm_serpentine_order_bit_identical(cuda, tmp_path):
+    """The grouped GEMM's serpentine k order (every other tile of a CTA pair
+    walks k downwards, MOE_B200_GEMM_SERP, read once per process) cannot
+    change a bit: int32 accumulation is exact. Same accumulators and dequant
+    outputs with it on (this process) and off (a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2508_07329_b200 import _lib as L, ops
+from tests.test_gpu_kernels import _rand_operand, _dev_operand
+rng = np.random.default_rng(77)
+a = _dev_operand("cuda", *_rand_operand(rng, 4096, 1040))
+w = _dev_operand("cuda", *_rand_operand(rng, 2 * 2048, 1040))   # 17 m x 8 n = 136 tiles > 74 pairs
+offs = torch.tensor([0, 1500, 4096], dtype=torch.int32, device="cuda")
+acc = ops.w8a8_gemm(a, w, epilogue=L.EPI_ACC_I32, group_offsets=offs, num_groups=2, n_per_group=2048)
+y = ops.w8a8_gemm(a, w, epilogue=L.EPI_DEQUANT, out_dtype=torch.bfloat16, group_offsets=offs, num_groups=2,
+                  n_per_group=2048)
+np.save(sys.argv[1], np.concatenate([acc.cpu().numpy().ravel().view(np.uint32),
+                                     y.view(torch.int16).cpu().numpy().ravel().astype(np.uint32)]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for serp in ("1", "0"):
+        f = tmp_path / f"serp{serp}.npy"
+        env = dict(os.environ, MOE_B200_GEMM_SERP=serp)
+        subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, check=True, timeout=300)
+        outs.append(np.load(f))
+    np.testing.assert_array_equal(outs[0], outs[1])
