@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                           int bits, int sym, uint8_t* codes, int64_t ldc, double* scale, float* scale_f32,
                           int32_t* zp, int32_t* rowsum, int64_t rows_per_cta) {
   griddep_launch_dependents();   // the next (PDL-launched) GEMM may start its weight prefetch
+  griddep_wait();                // PDL-launched: the previous kernel's outputs are visible from here
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // each CTA owns a contiguous range of rows (shared expert tables in L1)
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     fence_mbar_init();
   }
   __syncwarp();
+  griddep_wait();   // PDL-launched: the producer's rows and records are visible from here
 
   const int64_t nvec = a.cols / 8;
   const int64_t row_bytes = a.cols * 2;
@@ -699,8 +701,10 @@ static cudaError_t launch_bulk(const RowArgs& a, const float* rs32, const unsign
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((a.rows + kBulkWarps - 1) / kBulkWarps, num_sms()));
   const int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
   const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
-  act_quant_bulk_kernel<GIVEN><<<(unsigned)nblk, kBulkWarps * 32, kBulkSmem, s>>>(
-      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+  const cudaError_t e = launch_pdl(act_quant_bulk_kernel<GIVEN>, dim3((unsigned)nblk), dim3(kBulkWarps * 32),
+                                   (size_t)kBulkSmem, s, a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp,
+                                   rowsum, rows_per_cta);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -724,8 +728,8 @@ static void launch_cfg(const RowArgs& a, const float* rs32, const unsigned long 
   int64_t rows_per_cta = (a.rows + ctas - 1) / ctas;
   if (a.order) rows_per_cta = (rows_per_cta + a.order_k - 1) / a.order_k * a.order_k;   // a token's rows in one CTA
   const int64_t nblk = (a.rows + rows_per_cta - 1) / rows_per_cta;
-  act_quant_warp_kernel<GIVEN, WARPS, MINB><<<(unsigned)nblk, WARPS * 32, 0, s>>>(
-      a, rs32, ext, bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
+  launch_pdl(act_quant_warp_kernel<GIVEN, WARPS, MINB>, dim3((unsigned)nblk), dim3(WARPS * 32), 0, s, a, rs32, ext,
+             bits, sym, codes, ldc, scale, scale_f32, zp, rowsum, rows_per_cta);
 }
 
 // Kernel choice (measured on B200 at the Mixtral shape): rows with producer

@@ -141,6 +141,14 @@ class MoELayer:
             empty = out if out is not None else torch.empty((0, self.d), dtype=out_dtype, device=x.device)
             return (empty, {}) if return_aux else empty
         mark("start")
+        fused_combine = (self.k == 2 and not return_aux and y_dtype == torch.bfloat16
+                         and out_dtype == torch.bfloat16 and self.d % 32 == 0 and self.F % 16 == 0
+                         and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS) and L.tune(L.TUNE_FUSED_COMBINE) > 0
+                         and h_dtype == torch.bfloat16)
+        # the fused combine's counters, zeroed first so no memset sits between
+        # the PDL-chained kernels of the layer
+        cws = (ops.combine_workspace(T, self.d, x.device)
+               if fused_combine and L.tune(L.TUNE_FUSED_QUANT) == 0 else None)
         logits, idx, w = self.route(x, want_logits=return_aux)
         mark("router")
         if stats is not None:
@@ -182,11 +190,8 @@ class MoELayer:
         else:
             # (decode-size batches keep the separate combine: the per-chunk
             # hand-off costs more than the 4 us kernel at a few dozen rows)
-            fused_combine = (self.k == 2 and not return_aux and y_dtype == torch.bfloat16
-                             and out_dtype == torch.bfloat16 and self.d % 32 == 0 and self.F % 16 == 0
-                             and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS) and L.tune(L.TUNE_FUSED_COMBINE) > 0)
-            # (zeroed before K1 of h, so nothing sits between K1 and the PDL-launched GEMM)
-            cws = ops.combine_workspace(T, self.d, x.device) if fused_combine else None
+            if fused_combine and cws is None:
+                cws = ops.combine_workspace(T, self.d, x.device)
             a2 = ops.act_quant(h, smooth=self.s2, smooth_recip=self.s2_recip, smooth_recip_f32=self.s2_recip32,
                                row_group=perm["row_expert"], row_ext=ext)
             mark("quant_h")
