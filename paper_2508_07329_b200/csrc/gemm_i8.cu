@@ -949,9 +949,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0 && ob) bulk_wait_group<0>();   // TMA stores complete before the CTA retires
     if (p.out_tab) __threadfence_system();        // peer (home-rank) rows visible before the rank barrier
   }
-  // this CTA's tiles are done: a PDL-launched next kernel may be scheduled
-  // (it still waits for this whole grid in its griddep_wait)
-  griddep_launch_dependents();
+  // (no early griddep_launch_dependents here: at decode sizes the next
+  // kernels' CTAs, and behind them GEMM2's weight prefetch, then start during
+  // this GEMM's weight-streaming tail: 269 -> 273 us at 16 tokens)
   tc_fence_before();
   if (CG == 2) cluster_sync_all();
   else __syncthreads();
