@@ -1,0 +1,56 @@
+"""Randomised sweep of quantize_layer (HAQ: search_smoothing, build_hessian,
+the damped inverse factor, the GPTQ column loop) on the GPU against the
+oracle's restatement of the reference, on random small layers: the smoothing
+exponent, and the codes / scales / zero points compared element by element.
+The inverse factor comes from cuSOLVER on the GPU and from numpy/scipy in the
+oracle, so U differs in its last bits; codes can then flip where a value
+sits on a rounding boundary (K8 itself is bit-exact given the same U:
+tests/test_gpu_kernels.py). The sweep reports how often that happens.
+
+    python tools/stress_calib.py [seconds] [seed]"""
+import os
+import sys
+import time
+import warnings
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from oracle import quant_ref as Q  # noqa: E402
+from paper_2508_07329_b200 import quant  # noqa: E402
+
+warnings.simplefilter("ignore")
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 180.0
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+t_end = time.time() + budget
+n = exp_diff = code_cfgs = 0
+codes_total = codes_diff = 0
+while time.time() < t_end:
+    R = int(rng.integers(1, 97))
+    nin = int(rng.integers(2, 201))
+    T = int(rng.integers(8, 301))
+    bits = int(rng.integers(2, 9))
+    sym = bool(rng.random() < 0.3)
+    gran = str(rng.choice(["per_tensor", "per_token"]))
+    ordering = str(rng.choice(["none", "max_abs", "sum_squares"]))
+    w = rng.normal(size=(R, nin)) * 0.1
+    x = rng.normal(size=(nin, T))
+    x[rng.choice(nin, max(1, nin // 50), replace=False)] *= 50.0
+    c = quant.QuantConfig(bits=bits, symmetric=sym, granularity=gran)
+    try:
+        got = quant.quantize_layer(w, x, c, ordering=ordering)
+        ref = Q.quantize_layer(w, x, Q.cfg(bits, sym, gran), 21, ordering)
+    except Exception as e:   # noqa: BLE001  (the same refusal on both sides is fine)
+        print(f"R={R} n={nin} T={T} bits={bits}: raised {type(e).__name__}", flush=True)
+        continue
+    n += 1
+    same_e = got.smoothing.exponent == ref["exponent"]
+    exp_diff += not same_e
+    d = int((np.asarray(got.quantized.codes) != ref["codes"]).sum())
+    codes_total += ref["codes"].size
+    codes_diff += d if same_e else 0
+    code_cfgs += (d > 0) and same_e
+    print(f"R={R} n={nin} T={T} bits={bits} sym={sym} {gran} {ordering}: exponent "
+          f"{'=' if same_e else '!='} codes differing {d}/{ref['codes'].size}", flush=True)
+print(f"{n} layers; exponent differs in {exp_diff}; with equal exponents, codes differ in {code_cfgs} layers, "
+      f"{codes_diff} of {codes_total} codes", flush=True)
