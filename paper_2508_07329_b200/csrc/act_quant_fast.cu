@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     FastRow f;
     int mode = 0;
     if (spec) {
-      p = affine_params(mn, mx, bits, sym);
+      p = affine_params_fast(mn, mx, bits, sym);
       mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
     }
     if (mode) {
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(tok_warps<NV>() * 32, 1)
       int sum = 0;
       bool done = false;
       if (spec) {
-        p = affine_params(mn, mx, bits, sym);
+        p = affine_params_fast(mn, mx, bits, sym);
         FastRow f;
         const int mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
         if (mode) {
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     st.exact_all = exact_all;
     st.mode = 0;
     if (spec) {
-      st.p = affine_params(mn, mx, bits, sym);
+      st.p = affine_params_fast(mn, mx, bits, sym);
       st.mode = init_fast_row(st.f, st.p, rec.M, rec.m, mn, mx, bits, sym);
     }
   }
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     }
     mn = block_reduce(mn, shd, OpMin());
     mx = block_reduce(mx, shd, OpMax());
-    p = affine_params(mn, mx, bits, sym);
+    p = affine_params_fast(mn, mx, bits, sym);
     const RowEncoder enc(p, mn, mx, bits, st.exact_all);
     int s = 0;
 #pragma unroll

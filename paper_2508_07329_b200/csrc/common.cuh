@@ -137,6 +137,28 @@ __device__ __forceinline__ AffineParams affine_params(double mn, double mx, int 
   return p;
 }
 
+// affine_params for 8-bit asymmetric codes (the fast K1 rows) with both
+// divisions through div_rcp (Markstein-corrected reciprocal: the correctly
+// rounded quotient absent under/overflow; operands outside [2^-900, 2^1000]
+// take the IEEE division), so the same values as affine_params for ~70
+// fewer instructions per row.
+__device__ __forceinline__ AffineParams affine_params_u8(double mn, double mx) {
+  constexpr double kR255 = 1.0 / 255.0;   // RN(1/255), folded at compile time
+  auto in_range = [](double v) { const double a = fabs(v); return a > 0x1p-900 && a < 0x1p+1000; };
+  AffineParams p;
+  const double diff = __dsub_rn(mx, mn);
+  p.scale = fmax(in_range(diff) ? div_rcp(diff, 255.0, kR255) : __ddiv_rn(diff, 255.0), 1e-12);
+  p.rscale = __drcp_rn(p.scale);
+  const double nm = -mn;
+  double z = rha((in_range(nm) && in_range(p.scale)) ? div_rcp(nm, p.scale, p.rscale) : __ddiv_rn(nm, p.scale));
+  z = z < 0.0 ? 0.0 : (z > 255.0 ? 255.0 : z);
+  p.zp = (int)z;
+  return p;
+}
+__device__ __forceinline__ AffineParams affine_params_fast(double mn, double mx, int bits, int symmetric) {
+  return (bits == 8 && !symmetric) ? affine_params_u8(mn, mx) : affine_params(mn, mx, bits, symmetric);
+}
+
 
 // Launch with programmatic dependent launch allowed: the kernel may start
 // while the previous kernel in the stream is still running and must call

@@ -723,7 +723,7 @@ __device__ __forceinline__ void k1_row_warp(const RowArgs& a, int64_t r, const f
   int sum = 0;
   bool done = false;
   if (spec) {
-    p = affine_params(mn, mx, bits, sym);
+    p = affine_params_fast(mn, mx, bits, sym);
     FastRow f;
     const int mode = init_fast_row(f, p, rec.M, rec.m, mn, mx, bits, sym);
     if (mode) {

@@ -635,3 +635,21 @@ np.save(sys.argv[1], np.concatenate([acc.cpu().numpy().ravel().view(np.uint32),
         subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, check=True, timeout=300)
         outs.append(np.load(f))
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_act_quant_params_many_rows(cuda, k1_kernel):
+    """Scale and zero point of 120k short rows whose extremes span ~60 decades
+    (the fast kernels derive them through a corrected reciprocal instead of two
+    IEEE divisions): bit-identical to the oracle's float64 divisions."""
+    rng = np.random.default_rng(41)
+    R, d = 120_000, 16
+    mag = 10.0 ** rng.uniform(-30, 30, size=(R, 1))
+    x = rng.normal(size=(R, d)) * mag
+    x[::7] = np.abs(x[::7]) + mag[::7]                       # all-positive rows (zp 0)
+    x[1::7] = -np.abs(x[1::7])                                # non-positive rows
+    x = bf16_round(x.astype(np.float32))
+    r = ops.act_quant(torch.from_numpy(x).to(cuda).bfloat16())
+    codes, sc, zp, rs = M.quantize_rows(x.astype(np.float64))
+    np.testing.assert_array_equal(r["scale"].cpu().numpy(), sc)
+    np.testing.assert_array_equal(r["zp"].cpu().numpy(), zp)
+    np.testing.assert_array_equal(r["codes"].cpu().numpy(), codes)
