@@ -282,11 +282,14 @@ __global__ void router_topk_kernel(const float* logits, int64_t T, int E, int k,
 
 // ── stable counting sort ───────────────────────────────────────────────────
 constexpr int kPermThreads = 256;
-constexpr int kPermChunk = 1024;  // (token, slot) pairs per block
-constexpr int kPermScanBlocks = 64;  // above this many blocks: separate scan launch
+constexpr int kPermSingle = 1024;  // up to this many (token, slot) pairs: one single-block launch
+constexpr int kPermChunk = 256;    // pairs per block of the multi-block path (one pass per block)
+constexpr int kPermScanBlocks = 512;  // above this many blocks: separate scan launch
 
 __global__ void permute_count_kernel(const int32_t* idx, int64_t n, int E, int32_t* block_counts) {
   __shared__ int cnt[kMaxE];
+  griddep_wait();                 // PDL: the router's selections are visible from here
+  griddep_launch_dependents();    // the scatter (PDL) may get ready meanwhile
   for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * kPermChunk;
@@ -377,20 +380,29 @@ __global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int
   __shared__ int run[kMaxE];
   __shared__ int tot[kMaxE];
   __shared__ int wcnt[kPermThreads / 32][kMaxE];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    if (bases) {
+  griddep_wait();                 // PDL: the counts (and bases) are visible from here
+  griddep_launch_dependents();    // K1 on x (PDL) may get ready meanwhile
+  if (bases) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
       tot[e] = bases[(int64_t)nblocks * E + e];
       run[e] = bases[(int64_t)blockIdx.x * E + e];
-      continue;
     }
-    int t = 0, before = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      const int c = block_counts[(int64_t)b * E + e];
-      t += c;
-      if (b < (int)blockIdx.x) before += c;
+  } else {   // one warp per expert sums its column of the counts table
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = warp; e < E; e += kPermThreads / 32) {
+      int t = 0, before = 0;
+      for (int b = lane; b < nblocks; b += 32) {
+        const int c = block_counts[(int64_t)b * E + e];
+        t += c;
+        if (b < (int)blockIdx.x) before += c;
+      }
+      t = (int)__reduce_add_sync(0xffffffffu, (unsigned)t);
+      before = (int)__reduce_add_sync(0xffffffffu, (unsigned)before);
+      if (lane == 0) {
+        tot[e] = t;
+        run[e] = before;
+      }
     }
-    tot[e] = t;
-    run[e] = before;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -614,14 +626,15 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
   const int nb = (int)((n + kPermChunk - 1) / kPermChunk);
   int32_t* counts = static_cast<int32_t*>(workspace);
   cudaStream_t s = as_stream(stream);
-  if (nb == 1) {
+  if (n <= kPermSingle) {
     MOE_CUDA_TRY(launch_pdl(permute_single_kernel, dim3(1), dim3(kPermThreads), 0, s, topk_idx, topk_w, n, k, E,
                             expert_offsets, src_token, row_expert, row_weight, token_pos));
     ::moe::count_launch();
     MOE_LAUNCH_CHECK();
     return MOE_OK;
   }
-  permute_count_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, n, E, counts); ::moe::count_launch();
+  MOE_CUDA_TRY(launch_pdl(permute_count_kernel, dim3(nb), dim3(kPermThreads), 0, s, topk_idx, n, E, counts));
+  ::moe::count_launch();
   // beyond kPermScanBlocks blocks the per-block rescan (O(nb^2 E) reads) would
   // dominate: scan once in a separate launch
   int32_t* bases = nullptr;
@@ -629,8 +642,9 @@ extern "C" moe_status moe_route_permute(const int32_t* topk_idx, const float* to
     bases = counts + (int64_t)nb * E;
     permute_scan_kernel<<<E, kPermThreads, 0, s>>>(counts, nb, E, bases); ::moe::count_launch();
   }
-  permute_scatter_kernel<<<nb, kPermThreads, 0, s>>>(topk_idx, topk_w, n, k, E, counts, nb, bases, expert_offsets,
-                                                     src_token, row_expert, row_weight, token_pos);
+  MOE_CUDA_TRY(launch_pdl(permute_scatter_kernel, dim3(nb), dim3(kPermThreads), 0, s, topk_idx, topk_w, n, k, E,
+                          (const int32_t*)counts, nb, (const int32_t*)bases, expert_offsets, src_token, row_expert,
+                          row_weight, token_pos));
   ::moe::count_launch();
   MOE_LAUNCH_CHECK();
   return MOE_OK;
