@@ -97,7 +97,7 @@ struct GemmArgs {
   int64_t comb_ldo;
 };
 
-template <int BN, int STAGES, int CG>
+template <int BN, int STAGES, int CG, bool EPIBUF = true>
 struct Smem {
   static constexpr int kA = kBM * kBK;
   static constexpr int kB = (BN / CG) * kBK;
@@ -107,11 +107,11 @@ struct Smem {
   static constexpr int kTmemPtrOff = kBarOff + kNumBars * 8;
   static constexpr int kTableOff = kTmemPtrOff + 16;                  // tile_start[G+1], off[G+1]
   static constexpr int kOutOff = (kTableOff + 2 * (kMaxGroups + 1) * 4 + 127) / 128 * 128;
-  static constexpr int kOutBytes = kEpiWarps * 2 * 1024;               // per epilogue warp 2 x (32 rows x 32 B)
+  static constexpr int kOutBytes = EPIBUF ? kEpiWarps * 2 * 1024 : 0;  // per epilogue warp 2 x (32 rows x 32 B)
   // SwiGLU: per-tile W column parameters (zw, t = rowsum - Kc*zw, ws) and the
   // next layer's f32 reciprocal smoothing, staged by the epilogue warps while
   // they wait for the tile's accumulators (double-buffered)
-  static constexpr int kParamBuf = BN * 12 + (BN / 2) * 4;
+  static constexpr int kParamBuf = EPIBUF ? BN * 12 + (BN / 2) * 4 : 0;   // (SwiGLU only)
   static constexpr int kParamOff = kOutOff + kOutBytes;
   static constexpr int kBytes = kParamOff + 2 * kParamBuf + 1024;     // + alignment slack
 };
@@ -696,7 +696,7 @@ template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false, bool 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, GemmArgs p) {
-  using L = Smem<BN, STAGES, CG>;
+  using L = Smem<BN, STAGES, CG, EPI == MOE_EPI_SWIGLU>;
   constexpr int TM = kBM * CG;  // tile rows (a CTA pair shares one 256-row tile)
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled TMA / UMMA tiles (same offset in both CTAs of a pair)
@@ -1040,7 +1040,8 @@ template <int BN, int STAGES, int EPI, bool BF16, int CG, bool FQ = false, bool 
 static moe_status launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const GemmArgs& p,
                             int grid, cudaStream_t s) {
   auto kern = gemm_i8_tc_kernel<BN, STAGES, EPI, BF16, CG, FQ, CB>;
-  constexpr int bytes = Smem<BN, STAGES, CG>::kBytes;
+  constexpr int bytes = Smem<BN, STAGES, CG, EPI == MOE_EPI_SWIGLU>::kBytes;
+  static_assert(bytes <= 232448, "shared memory per CTA");
   MOE_CUDA_TRY(set_max_smem_once(reinterpret_cast<const void*>(kern), bytes));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1117,6 +1118,8 @@ static moe_status dispatch_tc(const uint8_t* a, int64_t M, int64_t K, int64_t ld
   const int grid = (int)(std::min<int64_t>(units_bound, max_units) * CG);
   switch (epilogue) {
     case MOE_EPI_DEQUANT:
+      // (a 7th stage fits the dequant kernels, which need no epilogue staging:
+      // GEMM2 +2-3 %, tools/st2_ab.sh at the time — not kept)
       if (p.comb_cnt)   // fused top-2 combine (bf16 only, checked by the entry point)
         return launch_tc<BN, ST, MOE_EPI_DEQUANT, true, CG, false, true>(ta, tb, to, p, grid, s);
       if (p.fq)   // K1 of A fused in (separate instantiation: the plain kernel keeps its registers)
