@@ -64,6 +64,11 @@ enum { MOE_EPI_FLAG_WCORR = 0x100 };
  * workspace already (earlier in the stream), so the call adds no memset
  * between the previous kernel and the GEMM (keeps the PDL overlap). */
 enum { MOE_EPI_FLAG_WS_ZEROED = 0x200 };
+/* OR-ed into moe_w8a8_gemm's `epilogue` with row_ext: the caller already set
+ * every row's records to (min = ~0, max = 0) earlier in the stream, so the
+ * call launches no initialisation kernel before the GEMM (keeps the PDL
+ * chain from the previous kernel). */
+enum { MOE_EPI_FLAG_EXT_READY = 0x400 };
 /* channel ordering strategies (quant.py:42-45) */
 enum { MOE_ORDER_MAX_ABS = 1, MOE_ORDER_SUM_SQUARES = 2 };
 

@@ -23,6 +23,7 @@ SMOOTH_NONE, SMOOTH_DIVIDE, SMOOTH_MULTIPLY = 0, 1, 2
 EPI_DEQUANT, EPI_SWIGLU, EPI_ACC_I32 = 0, 1, 2
 EPI_FLAG_WCORR = 0x100
 EPI_FLAG_WS_ZEROED = 0x200
+EPI_FLAG_EXT_READY = 0x400
 TUNE_K1_SMALL_ROWS = 1
 TUNE_ROUTER_CLUSTER_TILES = 2
 TUNE_FUSED_QUANT = 3

@@ -1149,6 +1149,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
                              moe_stream_t stream, const GemmArgs* fq = nullptr, const GemmArgs* cb = nullptr) {
   MOE_REQUIRE(a && w && a_zp && w_zp && a_rowsum && w_rowsum, "w8a8_gemm: null operand");
   const bool w_corr = (epilogue & MOE_EPI_FLAG_WCORR) != 0;
+  const bool ext_ready = (epilogue & MOE_EPI_FLAG_EXT_READY) != 0;
   epilogue &= 0xFF;
   if (row_ext) {
     MOE_REQUIRE(epilogue == MOE_EPI_SWIGLU, "w8a8_gemm: row_ext is produced by the SwiGLU epilogue");
@@ -1222,7 +1223,7 @@ static moe_status gemm_entry(const uint8_t* a, int64_t M, int64_t K, int64_t lda
   p.param_vec_ok = ((reinterpret_cast<uintptr_t>(w_zp) & 15) == 0) && ((reinterpret_cast<uintptr_t>(w_rowsum) & 15) == 0) &&
                    (!w_scale || (reinterpret_cast<uintptr_t>(w_scale) & 15) == 0) && (N % 4 == 0);
   cudaStream_t s = as_stream(stream);
-  if (row_ext) {
+  if (row_ext && !ext_ready) {
     rowext_init_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 4 * num_sms()), 256, 0, s>>>(row_ext, M);
     ::moe::count_launch();
   }

@@ -149,6 +149,10 @@ class MoELayer:
         # the PDL-chained kernels of the layer
         cws = (ops.combine_workspace(T, self.d, x.device)
                if fused_combine and L.tune(L.TUNE_FUSED_QUANT) == 0 else None)
+        # the SwiGLU epilogue's extreme records, initialised here for the same reason
+        precise = h_dtype == torch.float32
+        fuse = (not precise and self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS))
+        ext = ops.row_ext_init(T * self.k, x.device) if fuse else None
         logits, idx, w = self.route(x, want_logits=return_aux)
         mark("router")
         if stats is not None:
@@ -167,16 +171,14 @@ class MoELayer:
         # of the float32 min/max of h * RN32(1/s2), so the second K1 streams h once
         # (decode-size batches go through K1's CTA-per-row kernel, whose own
         # extreme pass is cheaper than initialising and filling the records)
-        precise = h_dtype == torch.float32
         if not precise and h_dtype != torch.bfloat16:
             raise ValueError("h_dtype must be torch.bfloat16 or torch.float32")
         if precise and y_dtype != torch.float32:
             y_dtype = torch.float32
-        fuse = (not precise and self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS))
-        ext = torch.empty((T * self.k, 2), dtype=torch.int64, device=x.device) if fuse else None
         h = ops.w8a8_gemm(a1, self.w13, epilogue=L.EPI_SWIGLU, out_dtype=h_dtype,
                           group_offsets=perm["offsets"], num_groups=self.E, n_per_group=2 * self.F,
-                          next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_ext=ext)
+                          next_smooth_recip_f32=self.s2_recip32 if fuse else None, row_ext=ext,
+                          row_ext_ready=True)
         mark("gemm13_swiglu")
         if fuse and self.F % 8 == 0 and L.tune(L.TUNE_FUSED_QUANT) > 0 and y_dtype == torch.bfloat16:
             # K1 of h runs inside the second grouped GEMM (its epilogue warps

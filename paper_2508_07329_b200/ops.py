@@ -190,9 +190,11 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
               bias: torch.Tensor | None = None, row_weight: torch.Tensor | None = None,
               group_offsets: torch.Tensor | None = None, num_groups: int = 1, n_per_group: int | None = None,
               out: torch.Tensor | None = None, next_smooth_recip_f32: torch.Tensor | None = None,
-              row_ext: torch.Tensor | None = None) -> torch.Tensor:
+              row_ext: torch.Tensor | None = None, row_ext_ready: bool = False) -> torch.Tensor:
     """a: dict from act_quant (codes [M, K], scale_f32, zp, rowsum per row).
-    w: dict with codes [G*N, K], scale_f32, zp, rowsum per row."""
+    w: dict with codes [G*N, K], scale_f32, zp, rowsum per row. With
+    ``row_ext_ready`` the records were initialised by the caller
+    (row_ext_init) and the call adds no init kernel."""
     ac, wc = a["codes"], w["codes"]
     M, K = ac.shape
     N = n_per_group if n_per_group is not None else wc.shape[0] // num_groups
@@ -219,6 +221,8 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
         odt = L.DT_BF16 if o.dtype == torch.bfloat16 else L.DT_F32
     # weights may carry the pre-corrected sidecar rowsum - K*zp (with_wcorr)
     w_rs, flags = (w["rowsum_corr"], L.EPI_FLAG_WCORR) if "rowsum_corr" in w else (w["rowsum"], 0)
+    if row_ext is not None and row_ext_ready:
+        flags |= L.EPI_FLAG_EXT_READY
     L.call("moe_w8a8_gemm", L.ptr(ac), M, K, ac.stride(0), L.ptr(a_scale), L.ptr(a_zp), L.ptr(a["rowsum"]),
            L.ptr(wc), N, wc.stride(0), L.ptr(w.get("scale_f32")), L.ptr(w["zp"]), L.ptr(w_rs),
            L.ptr(bias), L.ptr(row_weight), L.ptr(group_offsets), num_groups, epilogue | flags, L.ptr(o), odt, ldo,
@@ -259,6 +263,22 @@ def w8a8_gemm_quant_a(x: torch.Tensor, w: dict, *, smooth: torch.Tensor, smooth_
     a = {"codes": codes, "scale": scale, "scale_f32": scale_f32, "zp": zp, "rowsum": rs,
          "granularity": "per_token", "bits": 8}
     return o, a
+
+
+_EXT_INIT: dict = {}
+
+
+def row_ext_init(rows: int, device) -> torch.Tensor:
+    """[rows, 2] int64 extreme records set to (min = ~0, max = 0), ready for
+    w8a8_gemm(..., row_ext=..., row_ext_ready=True): one copy kernel, issued
+    wherever it does not sit between two PDL-chained kernels."""
+    key = str(device)
+    pat = _EXT_INIT.get(key)
+    if pat is None:
+        pat = _EXT_INIT[key] = torch.tensor([[-1, 0]], dtype=torch.int64, device=device)
+    ext = torch.empty((rows, 2), dtype=torch.int64, device=device)
+    ext.copy_(pat.expand(rows, 2))
+    return ext
 
 
 def combine_workspace(T: int, N: int, device) -> torch.Tensor:
