@@ -255,12 +255,15 @@ def test_attention_block_stagewise(cuda):
     oracle (oracle/attn_ref.py), stage by stage on the GPU's own inputs:
     fused W8A8 QKV projection, RoPE on q and k, causal grouped-query
     attention of packed sequences, W8A8 output projection."""
+    _attention_stagewise(256, 4, 2, 32, 64, 3, seed=21)
+
+
+def _attention_stagewise(d, H, Hk, hd, S, B, seed=21):
     from oracle import attn_ref as A
     from paper_2508_07329_b200.attention import W8A8Attention
 
-    rng = np.random.default_rng(21)
-    d, H, Hk, hd, S, B = 256, 4, 2, 32, 64, 3
-    att = W8A8Attention.random(d, H, Hk, hd, seed=5, max_pos=128)
+    rng = np.random.default_rng(seed)
+    att = W8A8Attention.random(d, H, Hk, hd, seed=seed + 5, max_pos=max(128, S))
     x = torch.from_numpy((rng.normal(size=(B * S, d)) * 2).astype(np.float32)).cuda().bfloat16()
     xf = x.double().cpu().numpy()
     wq = att.qkv.w
