@@ -24,6 +24,7 @@ budget = float(sys.argv[1]) if len(sys.argv) > 1 else 180.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
 t_end = time.time() + budget
 n = exp_diff = code_cfgs = 0
+near_ties = []
 codes_total = codes_diff = 0
 while time.time() < t_end:
     R = int(rng.integers(1, 97))
@@ -46,11 +47,21 @@ while time.time() < t_end:
     n += 1
     same_e = got.smoothing.exponent == ref["exponent"]
     exp_diff += not same_e
+    if not same_e:   # how far apart are the two choices in the oracle's own losses?
+        stat = np.maximum(np.abs(x).max(axis=1), 1e-8)
+        qc = Q.cfg(bits, sym, gran)
+        lg = Q.quant_loss(w, x, stat ** got.smoothing.exponent, qc)
+        lr = Q.quant_loss(w, x, stat ** ref["exponent"], qc)
+        gap = abs(lg - lr) / max(abs(lr), 1e-300)
+        near_ties.append(gap)
+        print(f"  exponent {got.smoothing.exponent} vs {ref['exponent']}: oracle losses {lg!r} / {lr!r}, "
+              f"relative gap {gap:.1e}", flush=True)
     d = int((np.asarray(got.quantized.codes) != ref["codes"]).sum())
     codes_total += ref["codes"].size
     codes_diff += d if same_e else 0
     code_cfgs += (d > 0) and same_e
     print(f"R={R} n={nin} T={T} bits={bits} sym={sym} {gran} {ordering}: exponent "
           f"{'=' if same_e else '!='} codes differing {d}/{ref['codes'].size}", flush=True)
-print(f"{n} layers; exponent differs in {exp_diff}; with equal exponents, codes differ in {code_cfgs} layers, "
+print(f"{n} layers; exponent differs in {exp_diff} (largest relative loss gap between the two choices "
+      f"{max(near_ties) if near_ties else 0:.1e}); with equal exponents, codes differ in {code_cfgs} layers, "
       f"{codes_diff} of {codes_total} codes", flush=True)
