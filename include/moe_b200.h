@@ -416,6 +416,13 @@ moe_status moe_w8a8_gemm_quant_a(const void* x, int64_t ldx, const double* smoot
  * workspace: moe_w8a8_gemm_combine_workspace(T, N) bytes (zeroed by the
  * call unless MOE_EPI_FLAG_WS_ZEROED). */
 int64_t moe_w8a8_gemm_combine_workspace(int64_t T, int64_t N);
+/* One kernel preparing a layer step's scratch ahead of its PDL-chained
+ * kernels: zeroes `zero_bytes` (multiple of 16, 16-byte aligned) at `zero`
+ * (the combine workspace; may be NULL) and sets `rows` extreme records of
+ * row_ext (may be NULL) to (min = ~0, max = 0) for moe_w8a8_gemm with
+ * MOE_EPI_FLAG_EXT_READY. */
+moe_status moe_step_init(void* zero, int64_t zero_bytes, unsigned long long* row_ext, int64_t rows,
+                         moe_stream_t stream);
 moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
                                  const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
                                  int64_t ldw, const float* w_scale, const int32_t* w_zp, const int32_t* w_rowsum,

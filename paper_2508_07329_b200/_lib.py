@@ -58,6 +58,7 @@ _SIGS = {
     "moe_w8a8_gemm_quant_a": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I64, _P, _I64,
                                    _I64, _P, _P, _P, _P, _P, _P, _I, _I, _P, _I, _I64, _P, _I64, _P]),
     "moe_w8a8_gemm_combine_workspace": (_I64, [_I64, _I64]),
+    "moe_step_init": (_I, [_P, _I64, _P, _I64, _P]),
     "moe_w8a8_gemm_combine": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _I, _I,
                                    _P, _I64, _P, _P, _I64, _P, _I64, _P, _I64, _P]),
     "moe_rmsnorm_residual": (_I, [_P, _P, _P, _P, _I64, _I64, C.c_float, _P]),

@@ -1312,6 +1312,33 @@ extern "C" moe_status moe_w8a8_gemm_quant_a(
 
 extern "C" int64_t moe_w8a8_gemm_combine_workspace(int64_t T, int64_t N) { return 4 * T * ((N + 31) / 32); }
 
+namespace moe {
+__global__ void step_init_kernel(uint4* zero, int64_t n16, unsigned long long* re, int64_t rows) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride)
+    zero[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += stride) {
+    re[2 * i] = ~0ull;     // min record
+    re[2 * i + 1] = 0ull;  // max record
+  }
+}
+}  // namespace moe
+
+extern "C" moe_status moe_step_init(void* zero, int64_t zero_bytes, unsigned long long* row_ext, int64_t rows,
+                                    moe_stream_t stream) {
+  MOE_REQUIRE(zero_bytes >= 0 && rows >= 0, "step_init: negative sizes");
+  MOE_REQUIRE(!zero_bytes || (zero && zero_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(zero) & 15) == 0),
+              "step_init: zero buffer must be 16-byte aligned and sized");
+  MOE_REQUIRE(!rows || row_ext, "step_init: null row_ext");
+  const int64_t work = std::max<int64_t>(zero_bytes / 16, rows);
+  if (work == 0) return MOE_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 8);
+  step_init_kernel<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<uint4*>(zero), zero_bytes / 16, row_ext, rows);
+  ::moe::count_launch();
+  MOE_LAUNCH_CHECK();
+  return MOE_OK;
+}
+
 extern "C" moe_status moe_w8a8_gemm_combine(const uint8_t* a, int64_t M, int64_t K, int64_t lda, const float* a_scale,
                                             const int32_t* a_zp, const int32_t* a_rowsum, const uint8_t* w, int64_t N,
                                             int64_t ldw, const float* w_scale, const int32_t* w_zp,

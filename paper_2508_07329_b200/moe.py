@@ -147,12 +147,11 @@ class MoELayer:
                          and h_dtype == torch.bfloat16)
         # the fused combine's counters, zeroed first so no memset sits between
         # the PDL-chained kernels of the layer
-        cws = (ops.combine_workspace(T, self.d, x.device)
-               if fused_combine and L.tune(L.TUNE_FUSED_QUANT) == 0 else None)
-        # the SwiGLU epilogue's extreme records, initialised here for the same reason
+        # ... and the SwiGLU epilogue's extreme records, both in one launch
         precise = h_dtype == torch.float32
         fuse = (not precise and self.d % 16 == 0 and self.d >= 128 and T * self.k > L.tune(L.TUNE_K1_SMALL_ROWS))
-        ext = ops.row_ext_init(T * self.k, x.device) if fuse else None
+        cws, ext = ops.step_init(T, self.d, T * self.k, x.device,
+                                 combine=fused_combine and L.tune(L.TUNE_FUSED_QUANT) == 0, records=fuse)
         logits, idx, w = self.route(x, want_logits=return_aux)
         mark("router")
         if stats is not None:

@@ -265,6 +265,18 @@ def w8a8_gemm_quant_a(x: torch.Tensor, w: dict, *, smooth: torch.Tensor, smooth_
     return o, a
 
 
+def step_init(T: int, N: int, rows: int, device, combine: bool, records: bool) -> tuple:
+    """(combine workspace zeroed | None, [rows, 2] extreme records initialised |
+    None), both prepared by one moe_step_init launch."""
+    wsb = L.load().moe_w8a8_gemm_combine_workspace(T, N) if combine else 0
+    wsb16 = (wsb + 15) // 16 * 16
+    ws = torch.empty(max(wsb16, 16), dtype=torch.uint8, device=device) if combine else None
+    ext = torch.empty((rows, 2), dtype=torch.int64, device=device) if records else None
+    if combine or records:
+        L.call("moe_step_init", L.ptr(ws), wsb16, L.ptr(ext), rows if records else 0, _s())
+    return ws, ext
+
+
 _EXT_INIT: dict = {}
 
 
