@@ -194,7 +194,7 @@ def w8a8_gemm(a: dict, w: dict, *, epilogue: int = L.EPI_DEQUANT, out_dtype=torc
     """a: dict from act_quant (codes [M, K], scale_f32, zp, rowsum per row).
     w: dict with codes [G*N, K], scale_f32, zp, rowsum per row. With
     ``row_ext_ready`` the records were initialised by the caller
-    (row_ext_init) and the call adds no init kernel."""
+    (step_init) and the call adds no init kernel."""
     ac, wc = a["codes"], w["codes"]
     M, K = ac.shape
     N = n_per_group if n_per_group is not None else wc.shape[0] // num_groups
@@ -275,22 +275,6 @@ def step_init(T: int, N: int, rows: int, device, combine: bool, records: bool) -
     if combine or records:
         L.call("moe_step_init", L.ptr(ws), wsb16, L.ptr(ext), rows if records else 0, _s())
     return ws, ext
-
-
-_EXT_INIT: dict = {}
-
-
-def row_ext_init(rows: int, device) -> torch.Tensor:
-    """[rows, 2] int64 extreme records set to (min = ~0, max = 0), ready for
-    w8a8_gemm(..., row_ext=..., row_ext_ready=True): one copy kernel, issued
-    wherever it does not sit between two PDL-chained kernels."""
-    key = str(device)
-    pat = _EXT_INIT.get(key)
-    if pat is None:
-        pat = _EXT_INIT[key] = torch.tensor([[-1, 0]], dtype=torch.int64, device=device)
-    ext = torch.empty((rows, 2), dtype=torch.int64, device=device)
-    ext.copy_(pat.expand(rows, 2))
-    return ext
 
 
 def combine_workspace(T: int, N: int, device) -> torch.Tensor:
